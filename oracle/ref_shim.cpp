@@ -1,0 +1,511 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference sources
+// (/root/reference/proj/core/src/*.cpp), compiled in place by
+// oracle/Makefile into oracle/_ref/libzcomm_ref.so.  It lets the Python
+// tests and bench.py's reference arm call the reference's own code:
+//   - as the differential oracle for frames, selector decisions, symbols;
+//   - as the CPU baseline (`--impl reference`).
+// Struct layouts are the zc_* PODs of include/zcomm_b200.h.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "zcomm/bench.hpp"
+#include "zcomm/collectives.hpp"
+#include "zcomm/fixedlen.hpp"
+#include "zcomm/frame.hpp"
+#include "zcomm/huffman.hpp"
+#include "zcomm/quant.hpp"
+#include "zcomm/rea.hpp"
+#include "zcomm_b200.h"
+
+using namespace zcomm;
+
+namespace {
+
+ArbitrationConfig to_cfg(const zc_arb_config* c) {
+  ArbitrationConfig a;
+  if (!c) return a;
+  a.smallBatchThresholdBytes = c->small_batch_threshold_bytes;
+  a.huffmanMinRawBytes = c->huffman_min_raw_bytes;
+  a.minGainPermil = c->min_gain_permil;
+  a.embedCodebook = c->embed_codebook != 0;
+  a.lamEnc = c->lam_enc;
+  a.lamDec = c->lam_dec;
+  a.cost.raw = {c->cost.raw.alpha_sec, c->cost.raw.enc_bytes_per_sec, c->cost.raw.dec_bytes_per_sec};
+  a.cost.fixedlen = {c->cost.fixedlen.alpha_sec, c->cost.fixedlen.enc_bytes_per_sec,
+                     c->cost.fixedlen.dec_bytes_per_sec};
+  a.cost.huffman = {c->cost.huffman.alpha_sec, c->cost.huffman.enc_bytes_per_sec,
+                    c->cost.huffman.dec_bytes_per_sec};
+  return a;
+}
+
+void from_cfg(const ArbitrationConfig& a, zc_arb_config* c) {
+  c->small_batch_threshold_bytes = a.smallBatchThresholdBytes;
+  c->huffman_min_raw_bytes = a.huffmanMinRawBytes;
+  c->min_gain_permil = a.minGainPermil;
+  c->embed_codebook = a.embedCodebook ? 1 : 0;
+  c->lam_enc = a.lamEnc;
+  c->lam_dec = a.lamDec;
+  c->cost.raw = {a.cost.raw.alphaSec, a.cost.raw.encBytesPerSec, a.cost.raw.decBytesPerSec};
+  c->cost.fixedlen = {a.cost.fixedlen.alphaSec, a.cost.fixedlen.encBytesPerSec,
+                      a.cost.fixedlen.decBytesPerSec};
+  c->cost.huffman = {a.cost.huffman.alphaSec, a.cost.huffman.encBytesPerSec,
+                     a.cost.huffman.decBytesPerSec};
+}
+
+TransportHint to_hint(int regime, double beta) {
+  return {regime == 0 ? Regime::IntraNode : Regime::InterNode, beta};
+}
+
+void to_stats(const SampleStats& s, zc_sample_stats* o) {
+  o->sampled_bytes = s.sampledBytes;
+  for (int i = 0; i < 256; ++i) o->hist[i] = s.hist[i];
+  o->max_zigzag = s.maxZigZag;
+  o->ctx_code_len_bits = s.ctxCodeLenBits;
+  o->ctx_code_len_valid = s.ctxCodeLenValid;
+  o->self_code_len_bits = s.selfCodeLenBits;
+  o->self_code_len_valid = s.selfCodeLenValid;
+}
+
+SampleStats from_stats(const zc_sample_stats* o) {
+  SampleStats s;
+  s.sampledBytes = o->sampled_bytes;
+  for (int i = 0; i < 256; ++i) s.hist[i] = o->hist[i];
+  s.maxZigZag = o->max_zigzag;
+  s.ctxCodeLenBits = o->ctx_code_len_bits;
+  s.ctxCodeLenValid = o->ctx_code_len_valid != 0;
+  s.selfCodeLenBits = o->self_code_len_bits;
+  s.selfCodeLenValid = o->self_code_len_valid != 0;
+  return s;
+}
+
+void to_est(const CodecEstimate& e, zc_codec_estimate* o) {
+  o->codec = static_cast<uint32_t>(e.codec);
+  o->admissible = e.admissible;
+  o->predicted_payload = e.predictedPayload;
+  o->enc_sec = e.encSec;
+  o->dec_sec = e.decSec;
+  o->predicted_sec = e.predictedSec;
+}
+
+FrameHeader to_hdr(const zc_frame_header* h) {
+  FrameHeader f;
+  f.magic = h->magic;
+  f.version = h->version;
+  f.codec = static_cast<CodecId>(h->codec);
+  f.flags = h->flags;
+  f.rawBytes = h->raw_bytes;
+  f.payloadBytes = h->payload_bytes;
+  f.params = h->params;
+  return f;
+}
+
+thread_local std::string g_err;
+
+int map_exc() {
+  try {
+    throw;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ZC_ERR_INVALID_ARGUMENT;
+  } catch (const std::overflow_error& e) {
+    g_err = e.what();
+    return ZC_ERR_OVERFLOW;
+  } catch (const LinkPoisoned& e) {
+    g_err = e.what();
+    return ZC_ERR_PEER;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return ZC_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ZC_ERR_RUNTIME;
+  }
+}
+
+CollectiveConfig to_ccfg(const zc_collective_config* c) {
+  CollectiveConfig cc;
+  cc.arb = to_cfg(&c->arb);
+  cc.net.bytesPerSec = c->hint.beta_eff_bytes_per_sec;
+  cc.net.regime = c->hint.regime == 0 ? Regime::IntraNode : Regime::InterNode;
+  cc.pin = static_cast<CodecPin>(c->pin);
+  cc.overlap = c->serialized ? OverlapMode::Serialized : OverlapMode::Pipelined;
+  cc.fusedCodecMinMsgBytes = c->fused_codec_min_msg_bytes;
+  return cc;
+}
+
+void to_wire(const WireStats& s, zc_wire_stats* o) {
+  std::memset(o, 0, sizeof(*o));
+  for (int i = 0; i < 3; ++i) o->frames_by_codec[i] = s.framesByCodec[i];
+  o->raw_bytes = s.rawBytes;
+  o->payload_bytes = s.payloadBytes;
+  o->total_bytes = s.totalBytes;
+  o->wall_codec_sec = s.wallCodecSec;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zr_last_error() { return g_err.c_str(); }
+
+void zr_default_arb_config(zc_arb_config* c) { from_cfg(ArbitrationConfig{}, c); }
+
+// ---------------- frame
+int zr_write_header(const zc_frame_header* h, uint8_t* dst, uint64_t len) {
+  try {
+    write_header(to_hdr(h), {dst, len});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_parse_header(const uint8_t* src, uint64_t len, zc_frame_header* out) {
+  auto h = parse_header({src, len});
+  if (!h) return ZC_ERR_INVALID_ARGUMENT;
+  out->magic = h->magic;
+  out->version = h->version;
+  out->codec = static_cast<uint8_t>(h->codec);
+  out->flags = h->flags;
+  out->raw_bytes = h->rawBytes;
+  out->payload_bytes = h->payloadBytes;
+  out->params = h->params;
+  return 0;
+}
+int zr_validate_header(const zc_frame_header* h, uint64_t region) {
+  return validate_header(to_hdr(h), region) ? 1 : 0;
+}
+uint64_t zr_frame_commit_raw(const uint8_t* raw, uint64_t n, uint8_t* region, uint64_t cap) {
+  return frame_commit_raw({raw, n}, {region, cap});
+}
+
+// ---------------- quant
+int zr_eb_quantize_with_scale(const double* x, uint64_t n, double scale, int32_t* out) {
+  try {
+    auto q = eb_quantize_with_scale({x, n}, scale);
+    std::memcpy(out, q.symbols.data(), n * 4);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_eb_quantize(const double* x, uint64_t n, double rel, int32_t* out, double* scale) {
+  try {
+    auto q = eb_quantize({x, n}, rel);
+    std::memcpy(out, q.symbols.data(), n * 4);
+    *scale = q.meta.scale;
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_eb_quantize_chunk(const double* x, uint64_t n, double scale, int32_t* out) {
+  try {
+    eb_quantize_chunk({x, n}, scale, {out, n});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_dequantize(const int32_t* s, uint64_t n, int mode, double scale, uint32_t levels, double* out) {
+  try {
+    QuantMeta m;
+    m.mode = static_cast<QuantMode>(mode);
+    m.scale = scale;
+    m.levels = levels;
+    dequantize_into({s, n}, m, {out, n});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// ---------------- fixedlen
+uint32_t zr_fixedlen_width(const int32_t* s, uint64_t n) { return fixedlen_width({s, n}); }
+uint64_t zr_fixedlen_encode(const int32_t* s, uint64_t n, uint8_t* out, uint64_t cap, uint32_t* w) {
+  unsigned ww = 0;
+  size_t r = fixedlen_encode({s, n}, {out, cap}, &ww);
+  *w = ww;
+  return r;
+}
+int zr_fixedlen_decode(const zc_frame_header* h, const uint8_t* payload, uint64_t plen, uint8_t* dst,
+                       uint64_t dlen) {
+  return fixedlen_decode_into(to_hdr(h), {payload, plen}, {dst, dlen}) ? 1 : 0;
+}
+
+// ---------------- huffman
+void* zr_huff_ctx_new(const uint64_t* hist) {
+  return new HuffmanContext(huffman_build_context({hist, 256}));
+}
+void* zr_huff_ctx_from_bytes(const uint8_t* sample, uint64_t n) {
+  std::array<uint64_t, 256> h;
+  h.fill(1);
+  for (uint64_t i = 0; i < n; ++i) h[sample[i]]++;
+  return new HuffmanContext(huffman_build_context(h));
+}
+void* zr_huff_ctx_from_lengths(const uint8_t* lens) {
+  auto c = huffman_context_from_lengths({lens, 256});
+  if (!c) return nullptr;
+  return new HuffmanContext(*c);
+}
+void zr_huff_ctx_free(void* c) { delete static_cast<HuffmanContext*>(c); }
+int zr_huff_ctx_valid(void* c) { return static_cast<HuffmanContext*>(c)->valid ? 1 : 0; }
+void zr_huff_ctx_tables(void* c, uint8_t* lens, uint32_t* code, uint32_t* rev, uint16_t* lut,
+                        uint32_t* minmax) {
+  auto* x = static_cast<HuffmanContext*>(c);
+  for (int i = 0; i < 256; ++i) {
+    lens[i] = x->codeLen[i];
+    code[i] = x->code[i];
+    rev[i] = x->revCode[i];
+  }
+  if (lut) {
+    for (size_t i = 0; i < x->rootLut.size(); ++i) lut[i] = x->rootLut[i];
+  }
+  minmax[0] = x->minLen;
+  minmax[1] = x->maxLen;
+}
+int zr_huffman_expected_code_len(void* c, const uint64_t* hist, double* bits) {
+  auto r = huffman_expected_code_len(*static_cast<HuffmanContext*>(c), {hist, 256});
+  if (!r) return 0;
+  *bits = *r;
+  return 1;
+}
+int zr_huffman_self_code_len(const uint64_t* hist, double* bits) {
+  auto r = huffman_self_code_len({hist, 256});
+  if (!r) return 0;
+  *bits = *r;
+  return 1;
+}
+uint64_t zr_huffman_encode(const uint8_t* raw, uint64_t n, void* c, uint8_t* out, uint64_t cap, int embed) {
+  return huffman_encode({raw, n}, *static_cast<HuffmanContext*>(c), {out, cap}, embed != 0);
+}
+int zr_huffman_decode(const zc_frame_header* h, const uint8_t* payload, uint64_t plen, void* c, uint8_t* dst,
+                      uint64_t dlen) {
+  return huffman_decode_into(to_hdr(h), {payload, plen}, static_cast<HuffmanContext*>(c), {dst, dlen}) ? 1
+                                                                                                      : 0;
+}
+
+// ---------------- rea
+void zr_profile_sample(const uint8_t* raw, uint64_t n, void* ctx, zc_sample_stats* out) {
+  to_stats(profile_sample({raw, n}, static_cast<HuffmanContext*>(ctx)), out);
+}
+uint64_t zr_predict_payload(int codec, uint64_t raw, const zc_sample_stats* st, const zc_arb_config* cfg) {
+  return predict_payload(static_cast<CodecId>(codec), raw, from_stats(st), to_cfg(cfg));
+}
+void zr_arbitrate_plan(uint64_t raw, uint64_t cap, const zc_sample_stats* st, int regime, double beta,
+                       void* ctx, const zc_arb_config* cfg, zc_arbitration_plan* out) {
+  auto p = arbitrate_plan(raw, cap, from_stats(st), to_hint(regime, beta), static_cast<HuffmanContext*>(ctx),
+                          to_cfg(cfg));
+  std::memset(out, 0, sizeof(*out));
+  out->choice = static_cast<uint32_t>(p.choice);
+  to_est(p.raw, &out->raw);
+  to_est(p.fixedlen, &out->fixedlen);
+  to_est(p.huffman, &out->huffman);
+}
+void zr_encode_best(const uint8_t* raw, uint64_t n, uint8_t* stage, uint64_t cap, int regime, double beta,
+                    void* ctx, const zc_arb_config* cfg, zc_encode_result* out) {
+  auto r = encode_best({raw, n}, {stage, cap}, to_hint(regime, beta), static_cast<HuffmanContext*>(ctx),
+                       to_cfg(cfg));
+  out->codec = static_cast<uint32_t>(r.codec);
+  out->_pad = 0;
+  out->payload_bytes = r.payloadBytes;
+  out->total_bytes = r.totalBytes;
+}
+
+// ---------------- collectives (Communicator with thread-per-rank, the reference's own runtime)
+// xs: nranks*count doubles (rank-major). out: nranks*count doubles.
+int zr_allreduce_eb(int nranks, const zc_collective_config* c, const double* xs, uint64_t count, double rel,
+                    const uint8_t* sample, uint64_t sampleLen, double* out, zc_wire_stats* wire,
+                    double* wall_sec) {
+  try {
+    Communicator comm(nranks, to_ccfg(c));
+    if (sample) comm.set_shared_huffman_from_bytes({sample, sampleLen});
+    auto t0 = std::chrono::steady_clock::now();
+    comm.run([&](RankCtx& ctx) {
+      auto r = ctx.allreduce_eb({xs + ctx.rank() * count, count}, rel);
+      std::memcpy(out + ctx.rank() * count, r.data(), count * 8);
+    });
+    auto t1 = std::chrono::steady_clock::now();
+    if (wall_sec) *wall_sec = std::chrono::duration<double>(t1 - t0).count();
+    if (wire) to_wire(comm.wire_stats(), wire);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// Symbol-domain allreduce with a shared Huffman context primed from sample bytes
+// (set_shared_huffman_from_bytes).  syms: nranks*count, in/out.  scales: nranks in/out.
+int zr_allreduce_sym(int nranks, const zc_collective_config* c, int32_t* syms, uint64_t count, int mode,
+                     double* scales, uint32_t levels, const uint8_t* sample, uint64_t sampleLen,
+                     zc_wire_stats* wire, double* wall_sec) {
+  try {
+    Communicator comm(nranks, to_ccfg(c));
+    if (sample) comm.set_shared_huffman_from_bytes({sample, sampleLen});
+    auto t0 = std::chrono::steady_clock::now();
+    comm.run([&](RankCtx& ctx) {
+      QuantizedStream q;
+      q.symbols.assign(syms + ctx.rank() * count, syms + (ctx.rank() + 1) * count);
+      q.meta.mode = static_cast<QuantMode>(mode);
+      q.meta.scale = scales[ctx.rank()];
+      q.meta.levels = levels;
+      q.meta.origRawBytes = 4 * count;
+      ctx.allreduce(q);
+      std::memcpy(syms + ctx.rank() * count, q.symbols.data(), count * 4);
+      scales[ctx.rank()] = q.meta.scale;
+    });
+    auto t1 = std::chrono::steady_clock::now();
+    if (wall_sec) *wall_sec = std::chrono::duration<double>(t1 - t0).count();
+    if (wire) to_wire(comm.wire_stats(), wire);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int zr_allgather_sym(int nranks, const zc_collective_config* c, const int32_t* blocks, uint64_t block,
+                     const uint8_t* sample, uint64_t sampleLen, int32_t* out, zc_wire_stats* wire) {
+  try {
+    Communicator comm(nranks, to_ccfg(c));
+    if (sample) comm.set_shared_huffman_from_bytes({sample, sampleLen});
+    comm.run([&](RankCtx& ctx) {
+      auto r = ctx.allgather({blocks + ctx.rank() * block, block});
+      std::memcpy(out + static_cast<size_t>(ctx.rank()) * nranks * block, r.data(), r.size() * 4);
+    });
+    if (wire) to_wire(comm.wire_stats(), wire);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// ---------------- data generators (bench.cpp:18-80, 463-476)
+int zr_gen_data(int dist, double geomP, uint64_t seed, int rank, uint64_t offset, uint64_t count, double* out) {
+  try {
+    DataSpec s;
+    s.dist = static_cast<DataDist>(dist);
+    s.geomP = geomP;
+    s.seed = seed;
+    gen_data_into(s, rank, offset, {out, count});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// ---------------- CPU baseline: the reference's codec round trip over 4 MiB batches on a
+// thread pool (batches are independent).  Quantize (eb_quantize_chunk) -> encode (pin dispatch
+// exactly as send_batch) -> header parse/validate -> decode dispatch (recv_batch) -> dequantize.
+// Returns total payload bytes via *payload and per-codec frame counts via frames[3].
+int zr_codec_roundtrip_mt(const float* x, uint64_t count, double scale, int pin, void* ctx,
+                          const zc_arb_config* cfgIn, int regime, double beta, int nthreads, float* out,
+                          uint64_t* payload, uint64_t* frames, double* wall_sec) {
+  try {
+    ArbitrationConfig cfg = to_cfg(cfgIn);
+    TransportHint hint = to_hint(regime, beta);
+    const HuffmanContext* hctx = static_cast<HuffmanContext*>(ctx);
+    uint64_t perBatch = kBatchRawBytes / 4;
+    uint64_t nb = (count + perBatch - 1) / perBatch;
+    std::atomic<uint64_t> next{0}, pay{0}, f0{0}, f1{0}, f2{0};
+    std::atomic<int> failed{0};
+    auto worker = [&]() {
+      std::vector<double> xd(perBatch), back(perBatch);
+      std::vector<int32_t> syms(perBatch), dec(perBatch);
+      std::vector<uint8_t> stage(kStageBankBytes);
+      for (;;) {
+        uint64_t b = next.fetch_add(1);
+        if (b >= nb) break;
+        uint64_t lo = b * perBatch, n = std::min(perBatch, count - lo);
+        for (uint64_t i = 0; i < n; ++i) xd[i] = x[lo + i];
+        eb_quantize_chunk({xd.data(), n}, scale, {syms.data(), n});
+        std::span<const uint8_t> raw{reinterpret_cast<const uint8_t*>(syms.data()), n * 4};
+        EncodeResult er;
+        switch (pin) {
+          case 0:
+            er = encode_best(raw, stage, hint, hctx, cfg);
+            break;
+          case 2: {
+            unsigned w = 0;
+            size_t p = fixedlen_encode({syms.data(), n}, std::span<uint8_t>(stage).subspan(kHeaderBytes), &w);
+            FrameHeader h;
+            h.codec = CodecId::FixedLen;
+            h.rawBytes = n * 4;
+            h.payloadBytes = p;
+            h.params = w;
+            write_header(h, stage);
+            er = {CodecId::FixedLen, p, kHeaderBytes + p};
+            break;
+          }
+          case 3: {
+            size_t p = huffman_encode(raw, *hctx, std::span<uint8_t>(stage).subspan(kHeaderBytes), false);
+            if (p > 0) {
+              FrameHeader h;
+              h.codec = CodecId::Huffman;
+              h.rawBytes = n * 4;
+              h.payloadBytes = p;
+              write_header(h, stage);
+              er = {CodecId::Huffman, p, kHeaderBytes + p};
+            } else {
+              size_t t = frame_commit_raw(raw, stage);
+              er = {CodecId::Raw, n * 4, t};
+            }
+            break;
+          }
+          default: {
+            size_t t = frame_commit_raw(raw, stage);
+            er = {CodecId::Raw, n * 4, t};
+          }
+        }
+        pay += er.payloadBytes;
+        (er.codec == CodecId::Raw ? f0 : er.codec == CodecId::FixedLen ? f1 : f2)++;
+        auto ph = parse_header({stage.data(), er.totalBytes});
+        bool ok = ph && validate_header(*ph, er.totalBytes);
+        std::span<uint8_t> dst{reinterpret_cast<uint8_t*>(dec.data()), n * 4};
+        std::span<const uint8_t> p{stage.data() + kHeaderBytes, ph->payloadBytes};
+        if (ok) {
+          switch (ph->codec) {
+            case CodecId::Raw:
+              std::memcpy(dst.data(), p.data(), dst.size());
+              break;
+            case CodecId::FixedLen:
+              ok = fixedlen_decode_into(*ph, p, dst);
+              break;
+            case CodecId::Huffman:
+              ok = huffman_decode_into(*ph, p, hctx, dst);
+              break;
+          }
+        }
+        if (!ok) failed = 1;
+        QuantMeta m{QuantMode::ErrorBounded, scale, 0, n * 4};
+        dequantize_into({dec.data(), n}, m, {back.data(), n});
+        if (out)
+          for (uint64_t i = 0; i < n; ++i) out[lo + i] = static_cast<float>(back[i]);
+      }
+    };
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> ts;
+    for (int t = 0; t < std::max(1, nthreads); ++t) ts.emplace_back(worker);
+    for (auto& t : ts) t.join();
+    auto t1 = std::chrono::steady_clock::now();
+    *wall_sec = std::chrono::duration<double>(t1 - t0).count();
+    *payload = pay;
+    frames[0] = f0;
+    frames[1] = f1;
+    frames[2] = f2;
+    if (failed) {
+      g_err = "round trip decode failed";
+      return ZC_ERR_RUNTIME;
+    }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,919 @@
+// zc_comm.cu — Communicator / RankCtx of the reference (collectives.hpp:48-153,
+// collectives.cpp:66-616) on B200: one zc_comm per rank, ring links over NVLink P2P.
+//
+// Memory: each rank owns ONE device allocation ("block") holding its receive banks (frames from
+// its ring predecessor, transport.hpp:106-134 semantics: bank = sequence mod nbanks, reused only
+// after the receiver returns a credit), the flag words of the protocol, its error word, a
+// mailbox for the tiny all-to-all control exchanges (meta records, abs-max), and device-side
+// WireStats.  Multi-process ranks exchange the block through CUDA IPC handles; single-process
+// groups (the analogue of Communicator::run's thread-per-rank, including several ranks on one
+// GPU for loopback testing) share raw pointers.
+//
+// A collective is a sequence of kernels on the rank's stream, with no host round-trip between
+// them: mailbox exchange -> (scale reconciliation) -> one exchange kernel per ring step
+// (zc_encode.cu: per 4 MiB unit, profile/select/encode straight into the successor's bank, then
+// decode the predecessor's frame and int32-add / store it into the local chunk) -> (dequantize).
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "zc_api_internal.h"
+#include "zc_kernels.h"
+
+namespace zc {
+namespace {
+
+constexpr int kMaxRanks = 64;
+constexpr uint64_t kAlign = 256;
+constexpr uint32_t kBlobMagic = 0x5A434231u;  // "ZCB1"
+
+uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  uint32_t nbanks;
+  uint64_t bank_stride, idx_off;
+  uint64_t off_banks, off_ready, off_len, off_credit, off_err, off_mbox, off_mflag, off_wire, off_errall, off_scal,
+      off_peers, total;
+};
+
+Layout make_layout(uint32_t nbanks) {
+  Layout L;
+  L.nbanks = nbanks;
+  L.idx_off = align_up(ZC_STAGE_BANK_BYTES, kAlign);
+  L.bank_stride = L.idx_off + align_up(ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
+  uint64_t o = 0;
+  L.off_banks = o;
+  o += nbanks * L.bank_stride;
+  L.off_ready = o;
+  o += align_up(8ull * nbanks, kAlign);
+  L.off_len = o;
+  o += align_up(8ull * nbanks, kAlign);
+  L.off_credit = o;
+  o += align_up(8ull * nbanks, kAlign);
+  L.off_err = o;
+  o += kAlign;
+  L.off_mbox = o;
+  o += align_up(2ull * kMaxRanks * 32, kAlign);
+  L.off_mflag = o;
+  o += align_up(8ull * kMaxRanks, kAlign);
+  L.off_wire = o;
+  o += align_up(sizeof(zc_wire_stats), kAlign);
+  L.off_errall = o;
+  o += align_up(8ull * kMaxRanks, kAlign);
+  L.off_scal = o;  // 32 doubles of per-collective scalars
+  o += kAlign;
+  L.off_peers = o;  // device array of every rank's block base
+  o += align_up(8ull * kMaxRanks, kAlign);
+  L.total = o;
+  return L;
+}
+
+// Per-collective device scalars (in the block at off_scal).
+struct Scal {
+  double absmax;      // local max|x|
+  double scale;       // shared bin width
+  double requant_f;   // llround(s * f) factor when this rank's scale differs
+  uint32_t requant;   // 1 when requantization is needed
+  uint32_t _p;
+  double my_scale;
+  double gmax;
+  double out;         // allreduce_max result
+};
+
+struct Blob {
+  uint32_t magic;
+  int32_t rank;
+  int32_t nranks;
+  int32_t device;
+  int32_t pid;
+  int32_t nbanks;
+  uint64_t bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+// ------------------------------------------------------------------ control kernels
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+enum MailOp : int { MAIL_MAX = 0, MAIL_META = 1, MAIL_EB_SCALE = 2 };
+
+struct MailArgs {
+  uint8_t* const* peers;  // device array: every rank's block base
+  uint64_t off_mbox, off_mflag, off_err;
+  int rank, nranks, op;
+  unsigned long long epoch;
+  unsigned long long timeout_ns;
+  uint32_t rec[8];        // this rank's 32-byte record (host-provided part)
+  int rec_from_absmax;    // MAIL_EB_SCALE / MAIL_MAX fed by Scal::absmax
+  int rec_scale_from_scal;  // MAIL_META: the record's scale is Scal::scale (allreduce_eb)
+  double rel;
+  Scal* scal;
+};
+
+// Ring-free all-to-all of 32-byte records through every rank's mailbox (parity double-buffered by
+// epoch), then the op's reduction.  This carries the StreamMeta ring (collectives.cpp:437-458)
+// and allreduce_max (:398-421): each is n-1 raw frames per rank in the reference's WireStats,
+// which the host adds (they are 24- and 8-byte control messages either way).
+__global__ void mailbox_kernel(MailArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t* err_self = reinterpret_cast<uint32_t*>(a.peers[a.rank] + a.off_err);
+  const int par = static_cast<int>(a.epoch & 1);
+  uint32_t rec[8];
+  for (int i = 0; i < 8; ++i) rec[i] = a.rec[i];
+  if (a.rec_from_absmax) {
+    unsigned long long b = __double_as_longlong(a.scal->absmax);
+    rec[0] = static_cast<uint32_t>(b);
+    rec[1] = static_cast<uint32_t>(b >> 32);
+  }
+  if (a.rec_scale_from_scal) {
+    unsigned long long b = __double_as_longlong(a.scal->scale);
+    rec[4] = static_cast<uint32_t>(b);
+    rec[5] = static_cast<uint32_t>(b >> 32);
+  }
+  for (int r = 0; r < a.nranks; ++r) {
+    uint32_t* slot = reinterpret_cast<uint32_t*>(a.peers[r] + a.off_mbox + (par * kMaxRanks + a.rank) * 32);
+    for (int i = 0; i < 8; ++i) slot[i] = rec[i];
+  }
+  __threadfence_system();
+  for (int r = 0; r < a.nranks; ++r)
+    st_rel(reinterpret_cast<unsigned long long*>(a.peers[r] + a.off_mflag) + a.rank, a.epoch);
+  const unsigned long long* my_flags = reinterpret_cast<const unsigned long long*>(a.peers[a.rank] + a.off_mflag);
+  const unsigned long long t0 = gtimer();
+  for (int r = 0; r < a.nranks; ++r) {
+    while (ld_acq(my_flags + r) < a.epoch) {
+      if (*reinterpret_cast<volatile uint32_t*>(err_self) != 0) return;
+      if (gtimer() - t0 > a.timeout_ns) {
+        for (int q = 0; q < a.nranks; ++q)
+          atomicOr(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_err), ZC_DERR_TIMEOUT);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+  const uint8_t* mb = a.peers[a.rank] + a.off_mbox + par * kMaxRanks * 32;
+  Scal* s = a.scal;
+  if (a.op == MAIL_MAX || a.op == MAIL_EB_SCALE) {
+    double m = 0.0;
+    bool first = true;
+    for (int r = 0; r < a.nranks; ++r) {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(mb + r * 32);
+      double v = __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(q[0]) |
+                                                             (static_cast<unsigned long long>(q[1]) << 32)));
+      m = first ? v : fmax(m, v);
+      first = false;
+    }
+    s->gmax = m;
+    s->out = m;
+    if (a.op == MAIL_EB_SCALE) s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, a.rel), m);
+  } else {
+    // StreamMeta {mode u8 @0, levels u32 @4, count u64 @8, scale f64 @16} (collectives.cpp:29-58)
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(mb + a.rank * 32);
+    double my_scale = __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(mine[4]) |
+                                                                  (static_cast<unsigned long long>(mine[5]) << 32)));
+    double shared = my_scale;
+    bool mismatch = false;
+    for (int r = 0; r < a.nranks; ++r) {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(mb + r * 32);
+      if ((q[0] & 0xFF) != (mine[0] & 0xFF) || q[1] != mine[1] || q[2] != mine[2] || q[3] != mine[3]) mismatch = true;
+      double sc = __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(q[4]) |
+                                                              (static_cast<unsigned long long>(q[5]) << 32)));
+      shared = fmax(shared, sc);
+    }
+    if (mismatch) {
+      for (int q = 0; q < a.nranks; ++q) atomicOr(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_err), ZC_DERR_MISMATCH);
+    }
+    s->my_scale = my_scale;
+    s->scale = shared;
+    s->requant = (shared != my_scale && my_scale > 0.0) ? 1u : 0u;
+    s->requant_f = my_scale / shared;
+  }
+}
+
+// Requantize to the shared scale: s = llround(s * (scale / shared)) (collectives.cpp:454-458).
+__global__ void requant_kernel(int32_t* sym, uint64_t n, const Scal* s) {
+  if (!s->requant) return;
+  const double f = s->requant_f;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    sym[i] = static_cast<int32_t>(llround(__dmul_rn(static_cast<double>(sym[i]), f)));
+}
+
+// eb_quantize_with_scale with the scale read from device memory (no host round-trip).
+__global__ void quantize_dev_kernel(const float* __restrict__ x, uint64_t n, const Scal* s, int32_t* __restrict__ sym,
+                                    uint32_t* err) {
+  const double scale = s->scale, rcp = 1.0 / scale;
+  uint32_t e = 0;
+  const uint64_t nv = n / 4, stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv; v += stride) {
+    float4 f = __ldg(reinterpret_cast<const float4*>(x) + v);
+    int4 o;
+    o.x = quantize_one(f.x, scale, rcp, e);
+    o.y = quantize_one(f.y, scale, rcp, e);
+    o.z = quantize_one(f.z, scale, rcp, e);
+    o.w = quantize_one(f.w, scale, rcp, e);
+    reinterpret_cast<int4*>(sym)[v] = o;
+  }
+  for (uint64_t i = nv * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    sym[i] = quantize_one(x[i], scale, rcp, e);
+  e = __reduce_or_sync(0xffffffffu, e);
+  if ((threadIdx.x & 31) == 0 && e) atomicOr(err, e);
+}
+
+__global__ void dequantize_dev_kernel(const int32_t* __restrict__ sym, uint64_t n, const Scal* s, void* out, int f64) {
+  const double k = s->scale;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double d = __dmul_rn(k, static_cast<double>(sym[i]));
+    if (f64) static_cast<double*>(out)[i] = d;
+    else static_cast<float*>(out)[i] = __double2float_rn(d);
+  }
+}
+
+__global__ void set_scale_kernel(Scal* s, double rel, int from_absmax) {
+  if (from_absmax) {
+    double m = s->absmax;
+    s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, rel), m);
+  }
+}
+
+int sm_count(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace
+}  // namespace zc
+
+using namespace zc;
+
+struct zc_comm {
+  int rank = 0, nranks = 1, device = 0;
+  zc_collective_config cfg{};
+  cudaStream_t stream = nullptr;
+  Layout lay{};
+  uint8_t* block = nullptr;
+  std::vector<uint8_t*> peer;      // every rank's block base, valid on this device
+  std::vector<bool> ipc_opened;
+  uint8_t** d_peers = nullptr;     // device copy of `peer` (inside the block)
+  zc_huff_ctx* shared = nullptr;   // installed shared Huffman context (owned)
+  uint64_t tx_seq = 0, rx_seq = 0;
+  unsigned long long epoch = 0;
+  zc_wire_stats host_wire{};       // control frames (meta / max) counted on the host
+  int share = 1;                   // ranks sharing this device (loopback groups)
+  bool connected = false;
+  int32_t* sym = nullptr;          // symbol scratch for allreduce_eb
+  uint64_t sym_cap = 0;
+  unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+
+  Scal* scal() const { return reinterpret_cast<Scal*>(block + lay.off_scal); }
+  uint32_t* err_word() const { return reinterpret_cast<uint32_t*>(block + lay.off_err); }
+};
+
+namespace {
+
+int dev_guard(zc_comm* c) { return cuda_err(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+Link make_link(zc_comm* c) {
+  Link L;
+  std::memset(&L, 0, sizeof(L));
+  const int n = c->nranks, next = (c->rank + 1) % n, prev = (c->rank - 1 + n) % n;
+  const Layout& y = c->lay;
+  L.tx_banks = c->peer[next] + y.off_banks;
+  L.tx_ready = reinterpret_cast<unsigned long long*>(c->peer[next] + y.off_ready);
+  L.tx_len = reinterpret_cast<unsigned long long*>(c->peer[next] + y.off_len);
+  L.tx_credit = reinterpret_cast<unsigned long long*>(c->block + y.off_credit);
+  L.rx_banks = c->block + y.off_banks;
+  L.rx_ready = reinterpret_cast<unsigned long long*>(c->block + y.off_ready);
+  L.rx_len = reinterpret_cast<unsigned long long*>(c->block + y.off_len);
+  L.rx_credit = reinterpret_cast<unsigned long long*>(c->peer[prev] + y.off_credit);
+  L.bank_stride = y.bank_stride;
+  L.idx_off = y.idx_off;
+  L.nbanks = y.nbanks;
+  L.nranks = static_cast<uint32_t>(n);
+  L.tx_seq0 = c->tx_seq;
+  L.rx_seq0 = c->rx_seq;
+  L.err_self = c->err_word();
+  L.err_all = reinterpret_cast<uint32_t* const*>(c->block + y.off_errall);
+  L.timeout_ns = c->timeout_ns;
+  L.wire = reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire);
+  const int mc = encode_max_clusters();
+  L.max_clusters = c->share <= 1 ? mc : std::max(1, (mc - 2) / c->share);
+  return L;
+}
+
+uint64_t chunk_lo(uint64_t count, int n, int c) { return static_cast<uint64_t>(c) * count / static_cast<uint64_t>(n); }
+uint64_t nbatches(uint64_t bytes) { return (bytes + ZC_BATCH_RAW_BYTES - 1) / ZC_BATCH_RAW_BYTES; }
+
+EncParams ring_enc(zc_comm* c, const int32_t* src, uint64_t bytes, int pin, int rx_add, int tx) {
+  EncParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.src = src;
+  p.src_kind = SRC_BYTES;
+  p.mode = ENC_SEND;
+  p.pin = pin;
+  p.scale = p.rcp = 1.0;
+  p.total_bytes = bytes;
+  p.unit_bytes = ZC_BATCH_RAW_BYTES;
+  p.nunits = static_cast<uint32_t>(nbatches(bytes));
+  p.stage_len = ZC_STAGE_BANK_BYTES;
+  p.hint = c->cfg.hint;
+  p.cfg = c->cfg.arb;
+  p.ctx = c->shared ? device_tables(c->shared) : nullptr;
+  p.err = c->err_word();
+  p.link_tx = tx;
+  p.link_rx_add = rx_add;
+  p.L = make_link(c);
+  return p;
+}
+
+int launch_mail(zc_comm* c, int op, const uint32_t rec[8], int from_absmax, double rel, int scale_from_scal = 0) {
+  MailArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.peers = c->d_peers;
+  a.off_mbox = c->lay.off_mbox;
+  a.off_mflag = c->lay.off_mflag;
+  a.off_err = c->lay.off_err;
+  a.rank = c->rank;
+  a.nranks = c->nranks;
+  a.op = op;
+  a.epoch = ++c->epoch;
+  a.timeout_ns = c->timeout_ns;
+  if (rec) std::memcpy(a.rec, rec, 32);
+  a.rec_from_absmax = from_absmax;
+  a.rec_scale_from_scal = scale_from_scal;
+  a.rel = rel;
+  a.scal = c->scal();
+  mailbox_kernel<<<1, 32, 0, c->stream>>>(a);
+  return cuda_err(cudaGetLastError(), "mailbox");
+}
+
+void count_ctrl_frames(zc_comm* c, uint64_t bytes) {
+  // n-1 raw frames per rank (collectives.cpp:405-417, 440-445)
+  const uint64_t k = static_cast<uint64_t>(c->nranks - 1);
+  c->host_wire.frames_by_codec[ZC_CODEC_RAW] += k;
+  c->host_wire.raw_bytes += k * bytes;
+  c->host_wire.payload_bytes += k * bytes;
+  c->host_wire.total_bytes += k * (bytes + ZC_HEADER_BYTES);
+}
+
+// One ring step = BatchIo::exchange (collectives.cpp:366-396): send `tx` to the successor and
+// receive `rx` from the predecessor, batch by batch, in ONE kernel (send part, then receive part,
+// per 4 MiB unit).  The receive sink adds (reduce-scatter) or stores (all-gather).
+int exchange_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin,
+                  bool store, const char* what) {
+  EncParams p = ring_enc(c, tx, tx_bytes, pin, 1, 1);
+  p.rx_store = store ? 1 : 0;
+  p.rx_dst = rx;
+  p.rx_total_bytes = rx_bytes;
+  p.rx_nunits = static_cast<uint32_t>(nbatches(rx_bytes));
+  if (p.nunits == 0 && p.rx_nunits == 0) return ZC_OK;
+  if (int rc = cuda_err(launch_encode(p, c->stream), what)) return rc;
+  c->tx_seq += p.nunits;
+  c->rx_seq += p.rx_nunits;
+  return ZC_OK;
+}
+
+// Reduce-scatter then (optionally) all-gather over the ring (collectives.cpp:460-502).  RS frames
+// use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.  An AG step re-encodes the
+// chunk it received in the previous step: frames are a pure function of the bytes, so every hop
+// ships the frame the reference would.
+int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
+  const int n = c->nranks, r = c->rank;
+  const uint64_t msg = count * 4;
+  const int fused_pin = msg >= c->cfg.fused_codec_min_msg_bytes ? c->cfg.pin : ZC_PIN_RAW;
+  auto chunk = [&](int ci, int32_t** base, uint64_t* bytes) {
+    ci = ((ci % n) + n) % n;
+    uint64_t lo = chunk_lo(count, n, ci), hi = chunk_lo(count, n, ci + 1);
+    *base = d_sym + lo;
+    *bytes = (hi - lo) * 4;
+  };
+  int32_t *sb, *rb;
+  uint64_t sby, rby;
+  for (int t = 0; t < n - 1; ++t) {
+    chunk(r - t, &sb, &sby);
+    chunk(r - t - 1, &rb, &rby);
+    if (int rc = exchange_step(c, sb, sby, rb, rby, fused_pin, false, "rs-step")) return rc;
+  }
+  if (!allgather) return ZC_OK;
+  for (int t = 0; t < n - 1; ++t) {
+    chunk(r + 1 - t, &sb, &sby);
+    chunk(r - t, &rb, &rby);
+    if (int rc = exchange_step(c, sb, sby, rb, rby, c->cfg.pin, true, "ag-step")) return rc;
+  }
+  return ZC_OK;
+}
+
+// All-gather of equal blocks (collectives.cpp:525-544): step t sends block (r-t), receives (r-t-1).
+int enqueue_allgather(zc_comm* c, int32_t* d_all, uint64_t block) {
+  const int n = c->nranks, r = c->rank;
+  if (n == 1 || block == 0) return ZC_OK;
+  const uint64_t by = block * 4;
+  for (int t = 0; t < n - 1; ++t) {
+    const int si = ((r - t) % n + n) % n, ri = ((r - t - 1) % n + n) % n;
+    if (int rc = exchange_step(c, d_all + static_cast<uint64_t>(si) * block, by,
+                               d_all + static_cast<uint64_t>(ri) * block, by, c->cfg.pin, true, "ag-step"))
+      return rc;
+  }
+  return ZC_OK;
+}
+
+int enqueue_meta(zc_comm* c, uint64_t count, int mode, double scale, uint32_t levels) {
+  uint32_t rec[8] = {0};
+  rec[0] = static_cast<uint32_t>(mode) & 0xFF;
+  rec[1] = levels;
+  rec[2] = static_cast<uint32_t>(count);
+  rec[3] = static_cast<uint32_t>(count >> 32);
+  uint64_t sb;
+  std::memcpy(&sb, &scale, 8);
+  rec[4] = static_cast<uint32_t>(sb);
+  rec[5] = static_cast<uint32_t>(sb >> 32);
+  count_ctrl_frames(c, 24);
+  return launch_mail(c, MAIL_META, rec, 0, 0.0);
+}
+
+int enqueue_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int mode, double scale, uint32_t levels) {
+  if (c->nranks == 1 || count == 0) return ZC_OK;
+  if (int rc = enqueue_meta(c, count, mode, scale, levels)) return rc;
+  requant_kernel<<<sm_count(c->device) * 4, 256, 0, c->stream>>>(d_sym, count, c->scal());
+  if (int rc = cuda_err(cudaGetLastError(), "requant")) return rc;
+  return enqueue_ring(c, d_sym, count, true);
+}
+
+int ensure_sym(zc_comm* c, uint64_t count) {
+  if (c->sym_cap >= count) return ZC_OK;
+  cudaStreamSynchronize(c->stream);
+  if (c->sym) cudaFree(c->sym);
+  c->sym = nullptr;
+  c->sym_cap = 0;
+  if (int rc = cuda_err(cudaMalloc(&c->sym, std::max<uint64_t>(count, 1) * 4), "malloc symbols")) return rc;
+  c->sym_cap = count;
+  return ZC_OK;
+}
+
+int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64, uint64_t count, double rel) {
+  if (int rc = ensure_sym(c, count)) return rc;
+  Scal* s = c->scal();
+  if (int rc = cuda_err(launch_absmax(d_x, SRC_F32, count, &s->absmax, c->err_word(), c->stream), "absmax")) return rc;
+  if (c->nranks > 1) {
+    count_ctrl_frames(c, 8);
+    if (int rc = launch_mail(c, MAIL_EB_SCALE, nullptr, 1, rel)) return rc;
+  } else {
+    set_scale_kernel<<<1, 1, 0, c->stream>>>(s, rel, 1);
+  }
+  const int g = sm_count(c->device) * 4;
+  quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
+  if (c->nranks > 1 && count > 0) {
+    // allreduce(q) with the shared scale: the meta ring still runs (and checks the counts)
+    uint32_t rec[8] = {0};
+    rec[0] = ZC_QUANT_ERROR_BOUNDED;
+    rec[2] = static_cast<uint32_t>(count);
+    rec[3] = static_cast<uint32_t>(count >> 32);
+    count_ctrl_frames(c, 24);
+    if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
+    if (int rc = enqueue_ring(c, c->sym, count, true)) return rc;
+  }
+  dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym, count, s, d_out, out_f64);
+  return cuda_err(cudaGetLastError(), "dequantize");
+}
+
+// Maps a device error word to the reference's exception kinds (root cause first).
+int status_from_err(uint32_t e) {
+  if (!e) return ZC_OK;
+  if (e & ZC_DERR_OVERFLOW) return set_err(ZC_ERR_OVERFLOW, "symbol sum exceeds 32-bit range");
+  if (e & ZC_DERR_MISMATCH) return set_err(ZC_ERR_INVALID_ARGUMENT, "ranks supplied mismatched streams to allreduce");
+  if (e & ZC_DERR_NONFINITE) return set_err(ZC_ERR_INVALID_ARGUMENT, "input must be finite");
+  if (e & ZC_DERR_RANGE) return set_err(ZC_ERR_INVALID_ARGUMENT, "quantize: bin index exceeds int32 range");
+  if (e & ZC_DERR_CAPACITY) return set_err(ZC_ERR_RUNTIME, "staging capacity exhausted; batch cannot ship even raw");
+  if (e & ZC_DERR_CORRUPT) return set_err(ZC_ERR_RUNTIME, "undecodable frame inside a collective");
+  if (e & ZC_DERR_TIMEOUT) return set_err(ZC_ERR_PEER, "peer did not respond (timeout); link poisoned");
+  return set_err(ZC_ERR_PEER, "link poisoned by an aborting peer");
+}
+
+int finish(zc_comm* c) {
+  if (int rc = cuda_err(cudaStreamSynchronize(c->stream), "collective")) return rc;
+  uint32_t e = 0;
+  if (int rc = cuda_err(cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost), "error word")) return rc;
+  return status_from_err(e);
+}
+
+int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg, zc_comm** out) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return set_err(ZC_ERR_INVALID_ARGUMENT, "communicator needs 1..64 ranks and a valid rank");
+  auto* c = new zc_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  if (cfg) c->cfg = *cfg;
+  else zc_default_collective_config(&c->cfg);
+  // A serialized launch leaves all codec time on the critical path (collectives.cpp:71-74).
+  if (c->cfg.serialized) c->cfg.arb.lam_enc = c->cfg.arb.lam_dec = 1.0;
+  const char* nb = std::getenv("ZC_COMM_BANKS");
+  uint32_t nbanks = nb ? static_cast<uint32_t>(std::max(2, std::min(16, std::atoi(nb)))) : ZC_STAGE_BANKS;
+  const char* to = std::getenv("ZC_COMM_TIMEOUT_MS");
+  if (to) c->timeout_ns = static_cast<unsigned long long>(std::atoll(to)) * 1000000ull;
+  c->lay = make_layout(nbanks);
+  int rc = cuda_err(cudaSetDevice(device), "cudaSetDevice");
+  if (!rc) {
+    preload_encode_kernels();
+    preload_decode_kernels();
+    preload_quant_kernels();
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, mailbox_kernel);
+    cudaFuncGetAttributes(&fa, requant_kernel);
+    cudaFuncGetAttributes(&fa, quantize_dev_kernel);
+    cudaFuncGetAttributes(&fa, dequantize_dev_kernel);
+    cudaFuncGetAttributes(&fa, set_scale_kernel);
+    cudaGetLastError();
+  }
+  if (!rc) rc = cuda_err(cudaMalloc(&c->block, c->lay.total), "cudaMalloc block");
+  if (!rc) rc = cuda_err(cudaMemset(c->block + c->lay.off_ready, 0, c->lay.total - c->lay.off_ready), "memset");
+  if (!rc) rc = cuda_err(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  if (rc) {
+    if (c->block) cudaFree(c->block);
+    delete c;
+    return rc;
+  }
+  c->peer.assign(nranks, nullptr);
+  c->ipc_opened.assign(nranks, false);
+  c->peer[rank] = c->block;
+  c->d_peers = reinterpret_cast<uint8_t**>(c->block + c->lay.off_peers);
+  *out = c;
+  return ZC_OK;
+}
+
+int finalize_peers(zc_comm* c) {
+  std::vector<uint32_t*> errs(c->nranks);
+  for (int r = 0; r < c->nranks; ++r) errs[r] = reinterpret_cast<uint32_t*>(c->peer[r] + c->lay.off_err);
+  int rc = cuda_err(cudaMemcpy(c->block + c->lay.off_errall, errs.data(), 8ull * c->nranks, cudaMemcpyHostToDevice),
+                    "err table");
+  if (!rc) rc = cuda_err(cudaMemcpy(c->d_peers, c->peer.data(), 8ull * c->nranks, cudaMemcpyHostToDevice), "peer table");
+  if (!rc) c->connected = true;
+  return rc;
+}
+
+int reset_state(zc_comm* c) {
+  if (int rc = dev_guard(c)) return rc;
+  if (std::getenv("ZC_DEBUG_NORESET")) return ZC_OK;  // keep the flag state for zc_comm_debug_state
+  cudaStreamSynchronize(c->stream);
+  const Layout& y = c->lay;
+  int rc = cuda_err(cudaMemset(c->block + y.off_ready, 0, y.off_wire - y.off_ready), "reset");
+  c->tx_seq = c->rx_seq = 0;
+  c->epoch = 0;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int zc_comm_create(int rank, int nranks, int device, const zc_collective_config* cfg, zc_comm** out) {
+  return alloc_comm(rank, nranks, device, cfg, out);
+}
+
+int zc_comm_export_size(void) { return static_cast<int>(sizeof(Blob)); }
+
+int zc_comm_export(zc_comm* c, uint8_t* blob) {
+  Blob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.rank = c->rank;
+  b.nranks = c->nranks;
+  b.device = c->device;
+  b.pid = static_cast<int32_t>(getpid());
+  b.nbanks = static_cast<int32_t>(c->lay.nbanks);
+  b.bytes = c->lay.total;
+  if (int rc = dev_guard(c)) return rc;
+  if (c->nranks > 1)
+    if (int rc = cuda_err(cudaIpcGetMemHandle(&b.handle, c->block), "cudaIpcGetMemHandle")) return rc;
+  std::memcpy(blob, &b, sizeof(b));
+  return ZC_OK;
+}
+
+int zc_comm_connect(zc_comm* c, const uint8_t* blobs) {
+  if (int rc = dev_guard(c)) return rc;
+  int same_dev = 0;
+  for (int r = 0; r < c->nranks; ++r) {
+    Blob b;
+    std::memcpy(&b, blobs + r * sizeof(Blob), sizeof(Blob));
+    if (b.magic != kBlobMagic || b.rank != r || b.nranks != c->nranks || b.nbanks != static_cast<int>(c->lay.nbanks) ||
+        b.bytes != c->lay.total)
+      return set_err(ZC_ERR_INVALID_ARGUMENT, "communicator blobs disagree (rank order, size or bank count)");
+    if (b.device == c->device) ++same_dev;
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    if (int rc = cuda_err(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle"))
+      return rc;
+    c->peer[r] = static_cast<uint8_t*>(p);
+    c->ipc_opened[r] = true;
+  }
+  c->share = std::max(1, same_dev);
+  return finalize_peers(c);
+}
+
+int zc_comm_create_group(int nranks, const int* devices, const zc_collective_config* cfg, zc_comm** out) {
+  std::vector<zc_comm*> cs(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (int rc = alloc_comm(r, nranks, devices[r], cfg, &cs[r])) {
+      for (auto* c : cs)
+        if (c) zc_comm_destroy(c);
+      return rc;
+    }
+  }
+  for (int a = 0; a < nranks; ++a) {
+    int share = 0;
+    for (int b = 0; b < nranks; ++b) {
+      if (devices[b] == devices[a]) ++share;
+      cs[a]->peer[b] = cs[b]->block;
+      if (devices[a] != devices[b]) {
+        cudaSetDevice(devices[a]);
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devices[a], devices[b]);
+        if (!can) return set_err(ZC_ERR_CUDA, "devices cannot access each other (no P2P)");
+        cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (int rc = cuda_err(e, "cudaDeviceEnablePeerAccess")) return rc;
+      }
+    }
+    cs[a]->share = share;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    cudaSetDevice(devices[r]);
+    if (int rc = finalize_peers(cs[r])) return rc;
+    out[r] = cs[r];
+  }
+  return ZC_OK;
+}
+
+void zc_comm_destroy(zc_comm* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int r = 0; r < c->nranks; ++r)
+    if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  if (c->sym) cudaFree(c->sym);
+  if (c->block) cudaFree(c->block);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->shared) zc_huff_ctx_destroy(c->shared);
+  delete c;
+}
+
+int zc_comm_rank(const zc_comm* c) { return c->rank; }
+int zc_comm_nranks(const zc_comm* c) { return c->nranks; }
+
+int zc_comm_set_shared_huffman(zc_comm* c, const zc_huff_ctx* ctx) {
+  if (!ctx || !zc_huff_ctx_valid(ctx)) return set_err(ZC_ERR_INVALID_ARGUMENT, "histogram yields no usable code");
+  uint8_t lens[256];
+  zc_huff_ctx_code_lengths(ctx, lens);
+  zc_huff_ctx* copy = nullptr;
+  if (int rc = zc_huff_ctx_from_lengths(lens, &copy)) return rc;
+  if (c->shared) zc_huff_ctx_destroy(c->shared);
+  c->shared = copy;
+  if (int rc = dev_guard(c)) return rc;
+  if (!device_tables(c->shared)) return set_err(ZC_ERR_CUDA, "cannot upload Huffman tables");
+  return ZC_OK;
+}
+
+int zc_comm_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int32_t mode, double* h_scale, uint32_t levels,
+                          void* stream) {
+  (void)stream;
+  if (int rc = dev_guard(c)) return rc;
+  if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = enqueue_allreduce_sym(c, d_sym, count, mode, *h_scale, levels)) return rc;
+  int rc = finish(c);
+  if (!rc && c->nranks > 1 && count > 0) cudaMemcpy(h_scale, &c->scal()->scale, 8, cudaMemcpyDeviceToHost);
+  return rc;
+}
+
+int zc_comm_allreduce_eb_f32(zc_comm* c, const float* d_x, void* d_out, int32_t out_f64, uint64_t count, double rel,
+                             void* stream) {
+  (void)stream;
+  if (!(rel > 0.0) || rel > 1.0) return set_err(ZC_ERR_INVALID_ARGUMENT, "eb_quantize: rel must be in (0, 1]");
+  if (int rc = dev_guard(c)) return rc;
+  if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = enqueue_allreduce_eb(c, d_x, d_out, out_f64, count, rel)) return rc;
+  return finish(c);
+}
+
+int zc_comm_reduce_scatter_sym(zc_comm* c, int32_t* d_sym, uint64_t count, void* stream) {
+  (void)stream;
+  if (int rc = dev_guard(c)) return rc;
+  if (c->nranks == 1 || count == 0) return ZC_OK;
+  if (int rc = enqueue_ring(c, d_sym, count, false)) return rc;
+  return finish(c);
+}
+
+int zc_comm_allgather_sym(zc_comm* c, int32_t* d_all, uint64_t block, void* stream) {
+  (void)stream;
+  if (int rc = dev_guard(c)) return rc;
+  if (c->nranks == 1 || block == 0) return ZC_OK;
+  if (int rc = enqueue_allgather(c, d_all, block)) return rc;
+  return finish(c);
+}
+
+int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
+  (void)stream;
+  if (!std::isfinite(v)) return set_err(ZC_ERR_INVALID_ARGUMENT, "allreduce_max requires finite input");
+  if (c->nranks == 1) {
+    *out = v;
+    return ZC_OK;
+  }
+  if (int rc = dev_guard(c)) return rc;
+  uint32_t rec[8] = {0};
+  uint64_t b;
+  std::memcpy(&b, &v, 8);
+  rec[0] = static_cast<uint32_t>(b);
+  rec[1] = static_cast<uint32_t>(b >> 32);
+  count_ctrl_frames(c, 8);
+  if (int rc = launch_mail(c, MAIL_MAX, rec, 0, 0.0)) return rc;
+  int rc = finish(c);
+  if (!rc) rc = cuda_err(cudaMemcpy(out, &c->scal()->out, 8, cudaMemcpyDeviceToHost), "result");
+  return rc;
+}
+
+int zc_comm_sync(zc_comm* c) {
+  if (int rc = dev_guard(c)) return rc;
+  return finish(c);
+}
+
+int zc_comm_reset(zc_comm* c) { return reset_state(c); }
+
+// Diagnostics: ready[nb], len[nb], credit[nb], err, mailbox flags[nranks], tx_seq, rx_seq, epoch.
+int zc_comm_debug_state(zc_comm* c, uint64_t* out, int cap) {
+  if (int rc = dev_guard(c)) return rc;
+  const Layout& y = c->lay;
+  std::vector<uint64_t> v;
+  std::vector<uint64_t> tmp(y.nbanks);
+  for (uint64_t off : {y.off_ready, y.off_len, y.off_credit}) {
+    cudaMemcpy(tmp.data(), c->block + off, 8 * y.nbanks, cudaMemcpyDeviceToHost);
+    v.insert(v.end(), tmp.begin(), tmp.end());
+  }
+  uint32_t e = 0;
+  cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost);
+  v.push_back(e);
+  std::vector<uint64_t> mf(c->nranks);
+  cudaMemcpy(mf.data(), c->block + y.off_mflag, 8 * c->nranks, cudaMemcpyDeviceToHost);
+  v.insert(v.end(), mf.begin(), mf.end());
+  v.push_back(c->tx_seq);
+  v.push_back(c->rx_seq);
+  v.push_back(c->epoch);
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int zc_comm_wire_stats(zc_comm* c, zc_wire_stats* out) {
+  if (int rc = dev_guard(c)) return rc;
+  zc_wire_stats d;
+  if (int rc = cuda_err(cudaMemcpy(&d, c->block + c->lay.off_wire, sizeof(d), cudaMemcpyDeviceToHost), "wire")) return rc;
+  for (int i = 0; i < 3; ++i) d.frames_by_codec[i] += c->host_wire.frames_by_codec[i];
+  d.raw_bytes += c->host_wire.raw_bytes;
+  d.payload_bytes += c->host_wire.payload_bytes;
+  d.total_bytes += c->host_wire.total_bytes;
+  d.wall_codec_sec = 0.0;
+  *out = d;
+  return ZC_OK;
+}
+
+int zc_comm_reset_stats(zc_comm* c) {
+  if (int rc = dev_guard(c)) return rc;
+  c->host_wire = zc_wire_stats{};
+  return cuda_err(cudaMemset(c->block + c->lay.off_wire, 0, sizeof(zc_wire_stats)), "reset stats");
+}
+
+// ---- single-process groups: every rank's collective enqueued before any is awaited (the
+// Communicator::run analogue; ranks' kernels must run concurrently).
+int zc_group_allreduce_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count, int32_t mode,
+                           double* h_scales, uint32_t levels) {
+  int rc = ZC_OK;
+  for (int r = 0; r < n && !rc; ++r) {
+    if ((rc = dev_guard(cs[r]))) break;
+    rc = enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels);
+  }
+  int first = rc;
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+  }
+  if (first) {
+    std::string msg = zc_last_error();
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+    return first;
+  }
+  for (int r = 0; r < n; ++r)
+    if (n > 1 && count > 0) cudaMemcpy(&h_scales[r], &cs[r]->scal()->scale, 8, cudaMemcpyDeviceToHost);
+  return ZC_OK;
+}
+
+int zc_group_allreduce_eb_f32(zc_comm* const* cs, int n, const float* const* d_xs, void* const* d_outs, int32_t out_f64,
+                              uint64_t count, double rel) {
+  if (!(rel > 0.0) || rel > 1.0) return set_err(ZC_ERR_INVALID_ARGUMENT, "eb_quantize: rel must be in (0, 1]");
+  int rc = ZC_OK;
+  // every allocation before any rank's kernels run: cudaFree/cudaMalloc may wait for the device
+  for (int r = 0; r < n && !rc; ++r) {
+    if ((rc = dev_guard(cs[r]))) break;
+    rc = ensure_sym(cs[r], count);
+  }
+  for (int r = 0; r < n && !rc; ++r) {
+    if ((rc = dev_guard(cs[r]))) break;
+    rc = enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel);
+  }
+  int first = rc;
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+  }
+  if (first) {
+    std::string msg = zc_last_error();
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+  }
+  return first;
+}
+
+int zc_group_allgather_sym(zc_comm* const* cs, int n, int32_t* const* d_alls, uint64_t block) {
+  // enqueue-only variant of zc_comm_allgather_sym for every rank, then one sync per rank
+  int first = ZC_OK;
+  for (int r = 0; r < n && !first; ++r) {
+    if ((first = dev_guard(cs[r]))) break;
+    first = enqueue_allgather(cs[r], d_alls[r], block);
+  }
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+  }
+  if (first) {
+    std::string msg = zc_last_error();
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+  }
+  return first;
+}
+
+int zc_group_reduce_scatter_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count) {
+  int first = ZC_OK;
+  if (n > 1 && count > 0)
+    for (int r = 0; r < n && !first; ++r) {
+      if ((first = dev_guard(cs[r]))) break;
+      first = enqueue_ring(cs[r], d_syms[r], count, false);
+    }
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+  }
+  if (first) {
+    std::string msg = zc_last_error();
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+  }
+  return first;
+}
+
+int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* outs) {
+  for (int r = 0; r < n; ++r)
+    if (!std::isfinite(vs[r])) return set_err(ZC_ERR_INVALID_ARGUMENT, "allreduce_max requires finite input");
+  if (n == 1) {
+    outs[0] = vs[0];
+    return ZC_OK;
+  }
+  int first = ZC_OK;
+  for (int r = 0; r < n && !first; ++r) {
+    if ((first = dev_guard(cs[r]))) break;
+    uint32_t rec[8] = {0};
+    uint64_t b;
+    std::memcpy(&b, &vs[r], 8);
+    rec[0] = static_cast<uint32_t>(b);
+    rec[1] = static_cast<uint32_t>(b >> 32);
+    count_ctrl_frames(cs[r], 8);
+    first = launch_mail(cs[r], MAIL_MAX, rec, 0, 0.0);
+  }
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+    if (!e) cudaMemcpy(&outs[r], &cs[r]->scal()->out, 8, cudaMemcpyDeviceToHost);
+  }
+  return first;
+}
+
+}  // extern "C"

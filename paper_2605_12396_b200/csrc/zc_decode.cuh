@@ -1,0 +1,361 @@
+// zc_decode.cuh — device-side frame checks and decoders shared by the standalone decode kernel
+// (zc_decode.cu) and the fused ring-step kernels (zc_encode.cu).
+//
+// Reference (relative to /root/reference/proj/core/):
+//   recv_batch header checks + raw-copy fallback   collectives.cpp:304-348
+//   fixedlen_decode_into                           fixedlen.cpp:39-65
+//   huffman_decode_into                            huffman.cpp:248-316
+//   RS sink (int64-checked add)                    collectives.cpp:480-491
+//   dequantize_into                                quant.cpp:107-127
+#pragma once
+#include "zc_huff_device.cuh"
+#include "zc_kernels.h"
+
+namespace zc {
+
+constexpr uint32_t kFallback = 0xFFFFFFFFu;
+
+struct FrameCheck {
+  zc_frame_header h;
+  uint64_t region;
+  uint32_t codec;  // codec to run, or kFallback
+  uint32_t need_seq;
+};
+
+// Loads honour the producer: frames written during this kernel or by a peer GPU are read through
+// L2 (ld.global.cg); immutable inputs use the read-only path.
+template <bool kCoherent>
+__device__ __forceinline__ uint32_t ld32(const uint32_t* p) {
+  if (kCoherent) return __ldcg(p);
+  return __ldg(p);
+}
+template <bool kCoherent>
+__device__ __forceinline__ uint4 ld128(const uint4* p) {
+  if (kCoherent) return __ldcg(p);
+  return __ldg(p);
+}
+template <bool kCoherent>
+__device__ __forceinline__ uint8_t ld8(const uint8_t* p) {
+  if (kCoherent) return static_cast<uint8_t>(__ldcg(reinterpret_cast<const char*>(p)));
+  return __ldg(p);
+}
+
+// 32-bit word w of a byte stream of `len` bytes; bytes past the end read as zero.
+template <bool kCoherent>
+__device__ __forceinline__ uint32_t stream_word(const uint8_t* s, uint64_t len, uint64_t w) {
+  uint64_t b = w * 4;
+  if (b + 4 <= len) return ld32<kCoherent>(reinterpret_cast<const uint32_t*>(s) + w);
+  uint32_t v = 0;
+  for (uint32_t j = 0; j < 4; ++j)
+    if (b + j < len) v |= static_cast<uint32_t>(ld8<kCoherent>(s + b + j)) << (8 * j);
+  return v;
+}
+
+// Output sink for decoded symbol vectors.
+struct Sink {
+  int kind;      // OutKind
+  void* out;     // base of the whole message (raw byte offsets index it)
+  double scale;  // dequantization factor
+};
+
+// Writes 4 decoded symbol words (16 raw bytes; nb valid) at raw byte offset `ob` of the output.
+__device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_t w[4], uint32_t nb, uint32_t& err) {
+  switch (k.kind) {
+    case OUT_F32: {
+      float* o = static_cast<float*>(k.out) + ob / 4;
+      float f[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        f[i] = __double2float_rn(__dmul_rn(k.scale, static_cast<double>(static_cast<int32_t>(w[i]))));
+      if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (static_cast<uint32_t>(i) < nb / 4) o[i] = f[i];
+      }
+      break;
+    }
+    case OUT_F64: {
+      double* o = static_cast<double*>(k.out) + ob / 4;
+      double d[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = __dmul_rn(k.scale, static_cast<double>(static_cast<int32_t>(w[i])));
+      if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        reinterpret_cast<double2*>(o)[0] = make_double2(d[0], d[1]);
+        reinterpret_cast<double2*>(o)[1] = make_double2(d[2], d[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (static_cast<uint32_t>(i) < nb / 4) o[i] = d[i];
+      }
+      break;
+    }
+    case OUT_ADD_I32: {
+      int32_t* o = static_cast<int32_t*>(k.out) + ob / 4;
+      if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        int4 a = __ldcg(reinterpret_cast<const int4*>(o));
+        long long s0 = static_cast<long long>(a.x) + static_cast<int32_t>(w[0]);
+        long long s1 = static_cast<long long>(a.y) + static_cast<int32_t>(w[1]);
+        long long s2 = static_cast<long long>(a.z) + static_cast<int32_t>(w[2]);
+        long long s3 = static_cast<long long>(a.w) + static_cast<int32_t>(w[3]);
+        bool ovf = (s0 != static_cast<int32_t>(s0)) | (s1 != static_cast<int32_t>(s1)) |
+                   (s2 != static_cast<int32_t>(s2)) | (s3 != static_cast<int32_t>(s3));
+        if (ovf) err |= ZC_DERR_OVERFLOW;
+        *reinterpret_cast<int4*>(o) = make_int4(static_cast<int32_t>(s0), static_cast<int32_t>(s1),
+                                                static_cast<int32_t>(s2), static_cast<int32_t>(s3));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (static_cast<uint32_t>(i) < nb / 4) {
+            long long s = static_cast<long long>(o[i]) + static_cast<int32_t>(w[i]);
+            if (s != static_cast<int32_t>(s)) err |= ZC_DERR_OVERFLOW;
+            o[i] = static_cast<int32_t>(s);
+          }
+        }
+      }
+      break;
+    }
+    default: {
+      uint8_t* o = static_cast<uint8_t*>(k.out) + ob;
+      if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j)
+          if (j < nb) o[j] = static_cast<uint8_t>(w[j >> 2] >> (8 * (j & 3)));
+      }
+    }
+  }
+}
+
+// Header checks of recv_batch (collectives.cpp:313-321) and of the codec decoders' preambles
+// (fixedlen.cpp:41-47, huffman.cpp:249-265).  hdr == nullptr: parse the header from the stage.
+// bare: `hdr` describes a payload that starts at the stage (no header bytes, no raw fallback).
+template <bool kCoherent>
+__device__ __forceinline__ void check_frame(const uint8_t* stage, uint64_t region, uint64_t R, const zc_frame_header* hdr,
+                                            bool bare, const DevHuff* ctx, bool have_index, FrameCheck& fc) {
+  fc.need_seq = 0;
+  fc.region = region;
+  if (bare) {
+    fc.h = *hdr;
+  } else {
+    if (region < kHeaderBytes) {
+      fc.codec = kFallback;
+      return;
+    }
+    uint64_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t lo = ld32<kCoherent>(reinterpret_cast<const uint32_t*>(stage) + 2 * i);
+      uint32_t hi = ld32<kCoherent>(reinterpret_cast<const uint32_t*>(stage) + 2 * i + 1);
+      w[i] = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+    }
+    fc.h = header_from_words(w);
+    if (!validate_header(fc.h, region) || fc.h.raw_bytes != R) {
+      fc.codec = kFallback;
+      return;
+    }
+  }
+  const zc_frame_header& h = fc.h;
+  const uint64_t plen = bare ? region : h.payload_bytes;
+  fc.codec = h.codec;
+  if (h.codec == ZC_CODEC_FIXEDLEN) {
+    uint32_t w = static_cast<uint32_t>(h.params);
+    bool ok = !(w < 1 || w > 32 || h.params > 32) && h.raw_bytes != 0 && h.raw_bytes % 4 == 0 && R >= h.raw_bytes;
+    if (ok) {
+      uint64_t need = packed_bytes(h.raw_bytes / 4, w);
+      ok = h.payload_bytes >= need && plen >= need;
+    }
+    if (!ok) fc.codec = kFallback;
+  } else if (h.codec == ZC_CODEC_HUFFMAN) {
+    bool ok = R >= h.raw_bytes && h.payload_bytes <= plen;
+    if (ok) {
+      if (h.flags & ZC_FLAG_EMBEDDED_CODEBOOK)
+        ok = h.params == ZC_HUFF_CODEBOOK_BYTES && h.payload_bytes >= ZC_HUFF_CODEBOOK_BYTES;
+      else
+        ok = h.params == 0 && ctx != nullptr && ctx->valid;
+    }
+    if (!ok) fc.codec = kFallback;
+    else if (!have_index) fc.need_seq = 1;
+  } else if (h.codec == ZC_CODEC_RAW && bare) {
+    fc.codec = kFallback;
+  }
+}
+
+// Decodes a Huffman symbol run starting at `bitpos` into `n` bytes handed to put(j, byte).
+// Mirrors huffman.cpp:281-314 with bits past the stream end reading as zero.  Returns false on
+// an undecodable code or an overrun; *end receives the final bit position.
+template <bool kCoherent, typename Put>
+__device__ __forceinline__ bool huff_run(const DevHuff* t, const uint8_t* s, uint64_t slen, uint64_t bitpos, uint64_t n,
+                                         uint64_t* end, Put put) {
+  const uint64_t total = slen * 8;
+  uint64_t wpos = bitpos >> 5;
+  const uint32_t sh = static_cast<uint32_t>(bitpos & 31);
+  unsigned long long acc = stream_word<kCoherent>(s, slen, wpos++) >> sh;
+  uint32_t nbits = 32 - sh;
+  for (uint64_t j = 0; j < n; ++j) {
+    if (nbits < 32) {
+      acc |= static_cast<unsigned long long>(stream_word<kCoherent>(s, slen, wpos++)) << nbits;
+      nbits += 32;
+    }
+    const uint16_t e = t->lut[acc & ((1u << ZC_HUFF_ROOT_BITS) - 1)];
+    uint32_t l = e >> 8;
+    uint32_t sym = e & 0xFFu;
+    if (l == 0) {
+      const uint64_t avail = total > bitpos ? total - bitpos : 0;
+      unsigned long long val = 0;
+      uint32_t k = 0;
+      bool found = false;
+      while (k < t->max_len) {
+        if (k >= avail) return false;
+        val = (val << 1) | ((acc >> k) & 1ull);
+        ++k;
+        if (k >= t->min_len && t->count_at_len[k] > 0 && val >= t->first_code[k] &&
+            val < t->first_code[k] + t->count_at_len[k]) {
+          sym = t->sym_order[t->first_index[k] + static_cast<uint32_t>(val - t->first_code[k])];
+          l = k;
+          found = true;
+          break;
+        }
+      }
+      if (!found) return false;
+    }
+    if (bitpos + l > total) return false;
+    acc >>= l;
+    nbits -= l;
+    bitpos += l;
+    put(j, sym);
+  }
+  *end = bitpos;
+  return true;
+}
+
+// Decode tables for a Huffman frame into shared memory: the embedded codebook rebuilt (with the
+// reference's validation) or a copy of the shared context.  All threads call.
+template <bool kCoherent>
+__device__ __forceinline__ bool load_huff_tables(const FrameCheck& fc, const uint8_t* payload, const DevHuff* g,
+                                                 DevHuff* t, uint32_t* flag, uint8_t* lens_tmp) {
+  if (fc.h.flags & ZC_FLAG_EMBEDDED_CODEBOOK) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lens_tmp[i] = ld8<kCoherent>(payload + i);
+    __syncthreads();
+    return cta_decode_tables(lens_tmp, t, flag);
+  }
+  for (int i = threadIdx.x; i < (1 << ZC_HUFF_ROOT_BITS); i += blockDim.x) t->lut[i] = g->lut[i];
+  if (threadIdx.x < 256) t->sym_order[threadIdx.x] = g->sym_order[threadIdx.x];
+  if (threadIdx.x < 33) {
+    t->count_at_len[threadIdx.x] = g->count_at_len[threadIdx.x];
+    t->first_index[threadIdx.x] = g->first_index[threadIdx.x];
+    t->first_code[threadIdx.x] = g->first_code[threadIdx.x];
+  }
+  if (threadIdx.x == 0) {
+    t->min_len = g->min_len;
+    t->max_len = g->max_len;
+    t->valid = g->valid;
+  }
+  __syncthreads();
+  return true;
+}
+
+// Decodes vectors [v0, v1) (16-byte units of raw output) of one checked frame into `sink` at raw
+// offset obase.  Every thread of the CTA calls (uniform control flow).  FixedLen/RAW/fallback
+// are streaming; Huffman runs one thread per 1 KiB grain from the companion index (v0 must be a
+// multiple of 64).  Returns flag bits for the caller: 1 = index inconsistent with the payload,
+// 2 = undecodable Huffman stream.  words: >= 32 * nwarps * ... per-warp scratch of 136 words.
+template <bool kCoherent>
+__device__ uint32_t decode_slice(const FrameCheck& fc, const uint8_t* payload, uint64_t R, uint64_t v0, uint64_t v1,
+                                 const Sink& sink, uint64_t obase, const uint32_t* idx, const DevHuff* ctx,
+                                 DevHuff* s_t, uint32_t* s_flag, uint8_t* s_lens_tmp, uint32_t* s_words,
+                                 uint32_t& err) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  uint32_t flags = 0;
+  const uint32_t codec = fc.codec;
+  if (codec == kFallback) {
+    // raw-copy fallback (collectives.cpp:330-336): the payload region verbatim, min(dst, have)
+    const uint64_t have = fc.region > kHeaderBytes ? fc.region - kHeaderBytes : 0;
+    const uint64_t lim = R < have ? R : have;
+    for (uint64_t v = v0 + tid; v < v1; v += nthr) {
+      if (v * 16 >= lim) break;
+      uint32_t nb = static_cast<uint32_t>(lim - v * 16 < 16 ? lim - v * 16 : 16);
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = stream_word<kCoherent>(payload, lim, v * 4 + k);
+      emit16(sink, obase + v * 16, w, nb, err);
+    }
+  } else if (codec == ZC_CODEC_RAW) {
+    for (uint64_t v = v0 + tid; v < v1; v += nthr) {
+      uint32_t nb = static_cast<uint32_t>(R - v * 16 < 16 ? R - v * 16 : 16);
+      uint32_t w[4];
+      if (nb == 16) {
+        uint4 x = ld128<kCoherent>(reinterpret_cast<const uint4*>(payload) + v);
+        w[0] = x.x;
+        w[1] = x.y;
+        w[2] = x.z;
+        w[3] = x.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = stream_word<kCoherent>(payload, R, v * 4 + k);
+      }
+      emit16(sink, obase + v * 16, w, nb, err);
+    }
+  } else if (codec == ZC_CODEC_FIXEDLEN) {
+    const uint32_t width = static_cast<uint32_t>(fc.h.params);
+    const uint32_t w4 = 4 * width;
+    const uint64_t P = fc.h.payload_bytes;
+    const unsigned long long mask = width == 32 ? 0xffffffffull : ((1ull << width) - 1);
+    uint32_t* sw = s_words + warp * 136;
+    for (uint64_t c = v0 / 32 + warp; c * 32 < v1; c += nthr / 32) {
+      for (uint32_t k = lane; k < w4 + 1; k += 32) sw[k] = stream_word<kCoherent>(payload, P, c * w4 + k);
+      __syncwarp();
+      const uint64_t v = c * 32 + lane;
+      if (v < v1) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t bit = (lane * 4 + k) * width;
+          const uint32_t wi = bit >> 5, sh = bit & 31;
+          unsigned long long x = (static_cast<unsigned long long>(sw[wi + 1]) << 32) | sw[wi];
+          w[k] = static_cast<uint32_t>(unzigzag32(static_cast<uint32_t>((x >> sh) & mask)));
+        }
+        uint32_t nb = static_cast<uint32_t>(R - v * 16 < 16 ? R - v * 16 : 16);
+        emit16(sink, obase + v * 16, w, nb, err);
+      }
+      __syncwarp();
+    }
+  } else if (codec == ZC_CODEC_HUFFMAN && !fc.need_seq) {
+    const bool ok = load_huff_tables<kCoherent>(fc, payload, ctx, s_t, s_flag, s_lens_tmp);
+    const bool emb = (fc.h.flags & ZC_FLAG_EMBEDDED_CODEBOOK) != 0;
+    if (!ok) {
+      flags |= 2u;
+    } else {
+      const uint8_t* s = payload + (emb ? ZC_HUFF_CODEBOOK_BYTES : 0);
+      const uint64_t slen = fc.h.payload_bytes - (emb ? ZC_HUFF_CODEBOOK_BYTES : 0);
+      const uint64_t Rh = fc.h.raw_bytes;
+      const uint64_t ngr = (Rh + kIndexGrain - 1) / kIndexGrain;
+      const uint64_t g0 = v0 / 64, g1 = min(ngr, (v1 + 63) / 64);
+      for (uint64_t g = g0 + tid; g < g1; g += nthr) {
+        const uint64_t b0 = g * kIndexGrain;
+        const uint64_t n = Rh - b0 < kIndexGrain ? Rh - b0 : kIndexGrain;
+        unsigned long long lo = 0, hi = 0;
+        uint64_t endb = 0;
+        const uint64_t start = ld32<kCoherent>(idx + g);
+        bool good = huff_run<kCoherent>(s_t, s, slen, start, n, &endb, [&](uint64_t j, uint32_t sym) {
+          const uint32_t k = static_cast<uint32_t>(j & 15);
+          if (k < 8) lo |= static_cast<unsigned long long>(sym) << (8 * k);
+          else hi |= static_cast<unsigned long long>(sym) << (8 * (k - 8));
+          if (k == 15 || j + 1 == n) {
+            uint32_t ww[4] = {static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32), static_cast<uint32_t>(hi),
+                              static_cast<uint32_t>(hi >> 32)};
+            emit16(sink, obase + b0 + (j & ~15ull), ww, k + 1, err);
+            lo = hi = 0;
+          }
+        });
+        if (!good) flags |= 2u;
+        else if (g + 1 < ngr && endb != ld32<kCoherent>(idx + g + 1)) flags |= 1u;
+      }
+    }
+  }
+  return flags;
+}
+
+}  // namespace zc

@@ -1,0 +1,928 @@
+// zc_encode.cu — fused quantize -> profile -> select -> encode -> frame, one thread-block cluster
+// per frame unit (normally a 4 MiB batch); plus the ring-step variants used by the collectives.
+//
+// Reference path (relative to /root/reference/proj/core/):
+//   RankCtx::send_batch codec dispatch    collectives.cpp:201-302
+//   encode_best (Algorithm 1)             rea.cpp:178-238
+//   profile_sample / arbitrate_plan       rea.cpp:93-176
+//   fixedlen_encode                       fixedlen.cpp:8-37
+//   huffman_encode                        huffman.cpp:216-246
+//   write_header / frame_commit_raw       frame.cpp:35-81
+//   eb_quantize_chunk (fused, optional)   quant.cpp:22-62
+//   RS step: recv -> add sink -> send     collectives.cpp:472-492
+//   AG step                               collectives.cpp:494-502
+//
+// B200 design: a cluster of CL=8 CTAs owns one unit.  Phase 1 streams the unit once from HBM
+// (quantizing fp32 on the fly when the source is a float tensor) and computes the FixedLen width
+// (max zig-zag over the whole unit), the 64 KiB profile histogram (shared-memory bins,
+// warp-aggregated atomics via __match_any_sync) and, when needed, Huffman bit totals.  The
+// per-CTA partials meet in CTA 0 through distributed shared memory; CTA 0 runs the bit-exact
+// selector (zc_common.cuh) and broadcasts the decision.  Phase 2 re-reads the unit — an L2 hit,
+// because the kernel is persistent with only as many clusters resident as keep the in-flight
+// units inside the 126 MB L2 — and materialises the chosen codec straight into the stage, which
+// in ring mode is the successor's receive bank (NVLink stores).  Symbols produced from fp32
+// never touch HBM.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "zc_decode.cuh"
+#include "zc_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace zc {
+namespace {
+
+constexpr int CL = 8;     // CTAs per cluster (= per frame unit)
+constexpr int NT = 512;   // threads per CTA
+constexpr int NW = NT / 32;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t CODEC_NONE = 0xFFu;
+constexpr int TILE_WORDS = NT * 16 + 64;  // Huffman tile: NT vectors x 16 bytes x <= 32 bits
+constexpr int ZZ_STRIDE = 132;            // FixedLen transpose buffer per warp (128 + pad)
+constexpr uint64_t SLICE_ALIGN = 64;      // CTA slices in 16-byte vectors: 1 KiB Huffman grains
+
+struct Bound {
+  unsigned long long head_idx, tail_idx;
+  uint32_t head_val, tail_val, has_head, has_tail;
+};
+
+struct Ctrl {
+  uint32_t maxzz, wmaxzz, zero_len, go;  // per-CTA partials; go: CTA 0's wait verdict
+  unsigned long long bits;
+  uint32_t codec, width, pending, _p;    // decision (CTA 0)
+  unsigned long long payload;
+  unsigned long long rx_len;
+  unsigned long long slice_base[CL];
+};
+
+union __align__(16) Scratch {
+  uint32_t tile[TILE_WORDS];
+  uint32_t zz[NW][ZZ_STRIDE];
+  struct {
+    unsigned long long keys[256];
+    unsigned long long w[512];
+    int parent[512];
+    uint8_t depth[512];
+  } tree;
+  struct {
+    DevHuff t;
+    uint32_t words[NW * 136];
+  } dec;
+};
+
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ ring flag protocol
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_err(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// Spins until *f >= v.  Gives up (false) when any rank has raised an error bit (the poison of
+// transport.cpp:90-95) or after the timeout, which it raises itself.
+__device__ bool wait_geq(const unsigned long long* f, unsigned long long v, const Link& L) {
+  const unsigned long long t0 = globaltimer();
+  for (uint32_t it = 0;; ++it) {
+    if (ld_acquire_sys(f) >= v) return true;
+    if (ld_err(L.err_self) != 0) return false;
+    if ((it & 255) == 255 && globaltimer() - t0 > L.timeout_ns) {
+      for (uint32_t r = 0; r < L.nranks; ++r) atomicOr(L.err_all[r], ZC_DERR_TIMEOUT);
+      return false;
+    }
+    __nanosleep(32);
+  }
+}
+
+__device__ __forceinline__ void broadcast_err(const Link& L, uint32_t err) {
+  for (uint32_t r = 0; r < L.nranks; ++r) atomicOr(L.err_all[r], err);
+}
+
+__device__ __forceinline__ void wire_add(zc_wire_stats* w, uint32_t codec, uint64_t raw, uint64_t payload,
+                                         uint64_t index_bytes) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(&w->frames_by_codec[codec]), 1ull);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&w->raw_bytes), static_cast<unsigned long long>(raw));
+  atomicAdd(reinterpret_cast<unsigned long long*>(&w->payload_bytes), static_cast<unsigned long long>(payload));
+  atomicAdd(reinterpret_cast<unsigned long long*>(&w->total_bytes), static_cast<unsigned long long>(payload + kHeaderBytes));
+  if (index_bytes) atomicAdd(reinterpret_cast<unsigned long long*>(&w->index_bytes), static_cast<unsigned long long>(index_bytes));
+}
+
+// Loads raw vector v (16 bytes) of the unit: bytes [16v, 16v+16) ∩ [0, R).  Float sources are
+// quantized here (4 elements -> 4 int32 symbols).  Missing bytes are zero; nb = valid bytes.
+// kCoh: the source was written earlier in this kernel (ring mode), so bypass the read-only path.
+template <int SRC, bool kCoh>
+__device__ __forceinline__ void load_vec(const EncParams& p, uint64_t uoff, uint64_t R, uint64_t v, uint32_t w[4],
+                                         uint32_t& nb, uint32_t& err) {
+  const uint64_t b0 = v * 16;
+  nb = static_cast<uint32_t>(R - b0 < 16 ? R - b0 : 16);
+  if (SRC == SRC_BYTES) {
+    const uint8_t* s = static_cast<const uint8_t*>(p.src) + uoff + b0;
+    if (nb == 16 && aligned16(s)) {
+      uint4 x = ld128<kCoh>(reinterpret_cast<const uint4*>(s));
+      w[0] = x.x;
+      w[1] = x.y;
+      w[2] = x.z;
+      w[3] = x.w;
+    } else {
+      w[0] = w[1] = w[2] = w[3] = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < 16; ++j)
+        if (j < nb) w[j >> 2] |= static_cast<uint32_t>(ld8<kCoh>(s + j)) << (8 * (j & 3));
+    }
+  } else if (SRC == SRC_F32) {
+    const float* s = static_cast<const float*>(p.src) + (uoff + b0) / 4;
+    float f[4] = {0.f, 0.f, 0.f, 0.f};
+    if (nb == 16 && aligned16(s)) {
+      float4 x = __ldg(reinterpret_cast<const float4*>(s));
+      f[0] = x.x;
+      f[1] = x.y;
+      f[2] = x.z;
+      f[3] = x.w;
+    } else {
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j)
+        if (j < nb / 4) f[j] = __ldg(s + j);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (static_cast<uint32_t>(k) < nb / 4)
+                 ? static_cast<uint32_t>(quantize_one(static_cast<double>(f[k]), p.scale, p.rcp, err))
+                 : 0u;
+  } else {
+    const double* s = static_cast<const double*>(p.src) + (uoff + b0) / 4;
+    double f[4] = {0.0, 0.0, 0.0, 0.0};
+    if (nb == 16 && aligned16(s)) {
+      double2 a = __ldg(reinterpret_cast<const double2*>(s));
+      double2 b = __ldg(reinterpret_cast<const double2*>(s) + 1);
+      f[0] = a.x;
+      f[1] = a.y;
+      f[2] = b.x;
+      f[3] = b.y;
+    } else {
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j)
+        if (j < nb / 4) f[j] = __ldg(s + j);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (static_cast<uint32_t>(k) < nb / 4) ? static_cast<uint32_t>(quantize_one(f[k], p.scale, p.rcp, err)) : 0u;
+  }
+}
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t w[4], uint32_t j) {
+  return (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+}
+
+// Stores one 32-bit word of the payload at byte offset 4*gw, never past `limit` payload bytes.
+__device__ __forceinline__ void store_word_safe(uint8_t* payload, uint64_t gw, uint32_t val, uint64_t limit) {
+  uint64_t b = gw * 4;
+  if (b + 4 <= limit) {
+    reinterpret_cast<uint32_t*>(payload)[gw] = val;
+  } else {
+    for (uint32_t j = 0; j < 4 && b + j < limit; ++j) payload[b + j] = static_cast<uint8_t>(val >> (8 * j));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T block_reduce_max(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T r = red[0];
+  for (int i = 1; i < NW; ++i) r = max(r, red[i]);
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long block_reduce_sum(unsigned long long v, unsigned long long* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  unsigned long long r = 0;
+  for (int i = 0; i < NW; ++i) r += red[i];
+  return r;
+}
+
+// Exclusive scan of a u32 across the CTA; *total receives the sum.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = x;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+  for (int i = 0; i < NW; ++i) {
+    uint32_t r = red[i];
+    if (i < warp) before += r;
+    tot += r;
+  }
+  *total = tot;
+  return before + x - v;
+}
+
+// Slice of the unit owned by cluster rank `crank`, in 16-byte vectors; multiples of 64 vectors
+// (1 KiB) so FixedLen chunks (128 symbols) and Huffman index grains never straddle CTAs.
+__device__ __forceinline__ void unit_slice(uint64_t R, uint32_t crank, uint64_t& v0, uint64_t& v1) {
+  const uint64_t nvec = (R + 15) / 16;
+  const uint64_t per = ((nvec + SLICE_ALIGN * CL - 1) / (SLICE_ALIGN * CL)) * SLICE_ALIGN;
+  v0 = min(nvec, per * crank);
+  v1 = min(nvec, per * (crank + 1));
+}
+
+template <int SRC, bool kRing>
+__global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
+  constexpr bool kCoh = kRing;  // ring sources are rewritten by this kernel's decode-add phase
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t crank = cluster.block_rank();
+  const uint32_t cid = blockIdx.x / CL;
+  const uint32_t ncl = gridDim.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  __shared__ uint32_t s_hist[256];   // profile window histogram (this CTA's share)
+  __shared__ uint32_t s_fhist[256];  // full-unit histogram (embedded codebook only)
+  __shared__ unsigned long long s_enc[256];
+  __shared__ uint8_t s_lens[256];   // per-unit embedded code lengths
+  __shared__ uint8_t s_clens[256];  // shared-context code lengths
+  __shared__ uint8_t s_slens[256];  // window self-code lengths (selfCodeLenBits)
+  __shared__ zc_sample_stats s_st;
+  __shared__ unsigned long long s_red[NW];
+  __shared__ uint32_t s_red32[NW];
+  __shared__ Ctrl s_ctrl;
+  __shared__ Bound s_bound[2];
+  __shared__ FrameCheck s_fc;
+  __shared__ uint32_t s_flag;
+  __shared__ Scratch s_x;
+
+  const bool bare = p.mode == ENC_BARE_FL || p.mode == ENC_BARE_HF;
+  const bool autolike = p.mode == ENC_BEST || (p.mode == ENC_SEND && p.pin == ZC_PIN_AUTO);
+  const bool embed = p.cfg.embed_codebook != 0 && !bare;
+  const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
+  for (int i = tid; i < 256; i += NT) {
+    s_clens[i] = ctx_ok ? p.ctx->len[i] : 0;
+    if (!embed) s_enc[i] = ctx_ok ? p.ctx->enc[i] : 0ull;
+  }
+  uint32_t err = 0;
+
+  // Ring mode runs one step of BatchIo::exchange (collectives.cpp:366-396): for every unit u, the
+  // send part (encode unit u of the outgoing chunk into the successor's bank) and then the
+  // receive part (unit u of the incoming chunk from the predecessor's frame, decoded and added
+  // into — or stored over — the local chunk).  Send-before-receive within a unit, and units in
+  // order, make the ring deadlock-free for any number of banks: a send waits only for credits of
+  // earlier units of the same step, a receive only for the predecessor's send of the same unit.
+  const uint32_t n_tx = (!kRing || p.link_tx) ? p.nunits : 0u;
+  const uint32_t n_rx = (kRing && p.link_rx_add) ? p.rx_nunits : 0u;
+  const uint32_t n_all = n_tx > n_rx ? n_tx : n_rx;
+  for (uint32_t u = cid, it = 0; u < n_all; u += ncl, ++it) {
+    const uint32_t par = it & 1u;
+    const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
+    const uint64_t R = u < n_tx ? ((p.total_bytes - uoff) < p.unit_bytes ? (p.total_bytes - uoff) : p.unit_bytes) : 0;
+    uint64_t v0, v1;
+    unit_slice(R, crank, v0, v1);
+    const uint64_t W = R < kSampleWindow ? R : kSampleWindow;
+    // Output stage: the successor's bank in ring mode, else stage u of the caller's array.
+    uint64_t tx_seq = 0, tx_bank = 0;
+    uint8_t* stage;
+    uint32_t* uindex;
+    if (kRing) {
+      tx_seq = p.L.tx_seq0 + u + 1;
+      tx_bank = (p.L.tx_seq0 + u) % p.L.nbanks;
+      stage = p.L.tx_banks + tx_bank * p.L.bank_stride;
+      uindex = reinterpret_cast<uint32_t*>(stage + p.L.idx_off);
+    } else {
+      stage = p.stages + static_cast<uint64_t>(u) * p.stride;
+      uindex = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
+    }
+    const uint64_t hdr = bare ? 0 : kHeaderBytes;
+    uint8_t* payload = stage + hdr;
+    const uint64_t pcap = p.stage_len > hdr ? p.stage_len - hdr : 0;
+    const bool stage_ok = bare || p.stage_len > kHeaderBytes;
+
+    if (tid == 0) {
+      s_ctrl.maxzz = s_ctrl.wmaxzz = s_ctrl.zero_len = 0;
+      s_ctrl.bits = 0;
+      s_ctrl.pending = 0;
+      s_ctrl.go = 1;
+      s_bound[par].has_head = s_bound[par].has_tail = 0;
+    }
+    for (int i = tid; i < 256; i += NT) {
+      s_hist[i] = 0;
+      s_fhist[i] = 0;
+    }
+    __syncthreads();
+
+    if (u < n_tx) {  // ======== send part (the whole encoder)
+    // What phase 1 must compute (uniform over the cluster).
+    const bool small = autolike && R <= p.cfg.small_batch_threshold_bytes;
+    const bool need_profile = p.mode == ENC_PROFILE || (autolike && !small);
+    const bool need_maxzz = need_profile || p.mode == ENC_BARE_FL || (p.mode == ENC_SEND && p.pin == ZC_PIN_FIXEDLEN);
+    const bool pin_huff = p.mode == ENC_BARE_HF || (p.mode == ENC_SEND && p.pin == ZC_PIN_HUFFMAN);
+    const bool need_full_hist = embed && (pin_huff || need_profile);
+    const bool p1_hbits = pin_huff && !embed;
+
+    // ---------------- phase 1: one streaming pass
+    uint32_t mz = 0, wmz = 0, zero = 0;
+    unsigned long long hb = 0;
+    if (stage_ok && s_ctrl.go && (need_maxzz || need_profile || need_full_hist || p1_hbits)) {
+      for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 32; base < v1; base += NT) {
+        const uint64_t v = base + lane;
+        const bool act = v < v1;
+        uint32_t w[4] = {0, 0, 0, 0}, nb = 0;
+        if (act) load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+        const uint32_t nwhole = nb >> 2;
+        if (need_maxzz) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (static_cast<uint32_t>(k) < nwhole) mz = max(mz, zigzag32(static_cast<int32_t>(w[k])));
+        }
+        if (need_profile && __any_sync(FULL, act && v * 16 < W)) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (act && v * 16 + 4 * k + 4 <= W) wmz = max(wmz, zigzag32(static_cast<int32_t>(w[k])));
+          // warp-aggregated shared-memory histogram of the profile window
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            const bool in = act && j < nb && v * 16 + j < W;
+            const uint32_t key = in ? byte_of(w, j) : 256u + lane;
+            const uint32_t peers = __match_any_sync(FULL, key);
+            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[key], __popc(peers));
+          }
+        }
+        if (need_full_hist) {
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            const bool in = act && j < nb;
+            const uint32_t key = in ? byte_of(w, j) : 256u + lane;
+            const uint32_t peers = __match_any_sync(FULL, key);
+            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_fhist[key], __popc(peers));
+          }
+        }
+        if (p1_hbits && act) {
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            if (j < nb) {
+              uint32_t l = static_cast<uint32_t>(s_enc[byte_of(w, j)] >> 32);
+              hb += l;
+              zero |= (l == 0);
+            }
+          }
+        }
+      }
+    }
+    {
+      uint32_t r = block_reduce_max(mz, s_red32);
+      uint32_t r2 = block_reduce_max(wmz, s_red32);
+      uint32_t r3 = block_reduce_max(zero, s_red32);
+      unsigned long long r4 = block_reduce_sum(hb, s_red);
+      if (tid == 0) {
+        s_ctrl.maxzz = r;
+        s_ctrl.wmaxzz = r2;
+        s_ctrl.zero_len = r3;
+        s_ctrl.bits = r4;
+      }
+    }
+    cluster.sync();  // A: partials visible cluster-wide
+
+    // ---------------- decision (CTA 0)
+    if (crank == 0) {
+      if (need_profile || need_full_hist) {
+        for (int i = tid; i < 256; i += NT) {
+          uint32_t h = 0, fh = 0;
+          for (int r = 0; r < CL; ++r) {
+            h += cluster.map_shared_rank(s_hist, r)[i];
+            fh += cluster.map_shared_rank(s_fhist, r)[i];
+          }
+          s_hist[i] = h;
+          s_fhist[i] = fh;
+        }
+      }
+      __syncthreads();
+      uint32_t maxzz = 0, wmaxzz = 0, zl = 0;
+      unsigned long long bits = 0;
+      if (tid == 0) {
+        for (int r = 0; r < CL; ++r) {
+          Ctrl* c = cluster.map_shared_rank(&s_ctrl, r);
+          maxzz = max(maxzz, c->maxzz);
+          wmaxzz = max(wmaxzz, c->wmaxzz);
+          zl |= c->zero_len;
+          s_ctrl.slice_base[r] = bits;
+          bits += c->bits;
+        }
+      }
+      // sample statistics (rea.cpp:93-118)
+      const bool want_self = need_profile && (embed || p.stats != nullptr);
+      if (need_profile) {
+        if (want_self) cta_huff_lengths(s_hist, s_slens, s_x.tree.keys, s_x.tree.w, s_x.tree.parent, s_x.tree.depth);
+        if (warp == 0) {
+          double el = 0.0, sl = 0.0;
+          bool v = ctx_ok && warp_mean_len(s_hist, s_clens, el);
+          bool sv = want_self && warp_mean_len(s_hist, s_slens, sl);
+          if (lane == 0) {
+            s_st.sampled_bytes = W;
+            s_st.max_zigzag = wmaxzz;
+            s_st.ctx_code_len_bits = v ? el : 0.0;
+            s_st.ctx_code_len_valid = v ? 1u : 0u;
+            s_st.self_code_len_bits = sv ? sl : 0.0;
+            s_st.self_code_len_valid = sv ? 1u : 0u;
+          }
+        }
+        for (int i = tid; i < 256; i += NT) s_st.hist[i] = s_hist[i];
+        __syncthreads();
+        if (p.stats != nullptr) {
+          zc_sample_stats* o = p.stats + u;
+          for (int i = tid; i < 256; i += NT) o->hist[i] = s_st.hist[i];
+          if (tid == 0) {
+            o->sampled_bytes = s_st.sampled_bytes;
+            o->max_zigzag = s_st.max_zigzag;
+            o->ctx_code_len_bits = s_st.ctx_code_len_bits;
+            o->self_code_len_bits = s_st.self_code_len_bits;
+            o->ctx_code_len_valid = s_st.ctx_code_len_valid;
+            o->self_code_len_valid = s_st.self_code_len_valid;
+          }
+        }
+      }
+      // embedded codebook: build this unit's code from its full histogram (rea.cpp:214-221)
+      if (need_full_hist) {
+        cta_huff_lengths(s_fhist, s_lens, s_x.tree.keys, s_x.tree.w, s_x.tree.parent, s_x.tree.depth);
+        if (tid == 0) canonical_enc(s_lens, s_enc);
+        __syncthreads();
+      }
+      if (tid == 0) {
+        uint32_t codec = ZC_CODEC_RAW, width = 0, pending = 0;
+        unsigned long long payload = R;
+        if (!s_ctrl.go) {
+          codec = CODEC_NONE;
+        } else if (!stage_ok) {
+          codec = CODEC_NONE;
+          if (p.mode == ENC_SEND) err |= ZC_DERR_CAPACITY;
+        } else if (p.mode == ENC_PROFILE) {
+          codec = CODEC_NONE;
+        } else if (p.mode == ENC_BARE_FL) {
+          width = width_from_maxzz(maxzz);
+          payload = packed_bytes(R / 4, width);
+          codec = (R > 0 && payload <= pcap) ? ZC_CODEC_FIXEDLEN : CODEC_NONE;
+        } else if (p.mode == ENC_BARE_HF) {
+          unsigned long long bytes = (bits + 7) / 8 + (p.embed ? ZC_HUFF_CODEBOOK_BYTES : 0);
+          bool ok = ctx_ok && !zl && (R > 0 || p.embed) && bytes <= pcap;
+          codec = ok ? ZC_CODEC_HUFFMAN : CODEC_NONE;
+          payload = bytes;
+        } else {
+          if (autolike) {
+            if (!small) {
+              zc_arbitration_plan plan = arbitrate_plan(R, pcap, s_st, p.hint, ctx_ok, p.cfg);
+              if (plan.choice == ZC_CODEC_FIXEDLEN) {
+                width = width_from_maxzz(maxzz);
+                unsigned long long pay = packed_bytes(R / 4, width);
+                if (pay > 0 && pay <= pcap && gain_ok(R, pay, p.cfg.min_gain_permil)) {
+                  codec = ZC_CODEC_FIXEDLEN;
+                  payload = pay;
+                }
+              } else if (plan.choice == ZC_CODEC_HUFFMAN) {
+                pending = 1;
+              }
+            }
+          } else if (p.pin == ZC_PIN_FIXEDLEN) {
+            if (R >= 4 && R % 4 == 0) {
+              width = width_from_maxzz(maxzz);
+              unsigned long long pay = packed_bytes(R / 4, width);
+              if (pay > 0 && pay <= pcap) {
+                codec = ZC_CODEC_FIXEDLEN;
+                payload = pay;
+              }
+            }
+          } else if (p.pin == ZC_PIN_HUFFMAN) {
+            if (embed) {
+              pending = 1;
+            } else if (ctx_ok) {
+              unsigned long long bytes = (bits + 7) / 8;
+              if (!zl && bytes > 0 && bytes <= pcap) {
+                codec = ZC_CODEC_HUFFMAN;
+                payload = bytes;
+              }
+            }
+          }
+          if (codec == ZC_CODEC_RAW && !pending && R > pcap) {
+            codec = CODEC_NONE;  // cannot ship even raw
+            if (p.mode == ENC_SEND) err |= ZC_DERR_CAPACITY;
+          }
+        }
+        // ring: the successor must have returned this bank before we overwrite it
+        if (kRing && codec != CODEC_NONE && tx_seq > p.L.nbanks) {
+          if (!wait_geq(&p.L.tx_credit[tx_bank], tx_seq - p.L.nbanks, p.L)) {
+            codec = CODEC_NONE;
+            pending = 0;
+            err |= ZC_DERR_ABORT;
+          }
+        }
+        s_ctrl.codec = codec;
+        s_ctrl.width = width;
+        s_ctrl.pending = pending;
+        s_ctrl.payload = payload;
+      }
+    }
+    cluster.sync();  // B: decision visible
+    Ctrl* c0 = cluster.map_shared_rank(&s_ctrl, 0);
+    const uint32_t pending = c0->pending;
+
+    if (pending) {
+      if (embed && crank != 0) {
+        for (int i = tid; i < 256; i += NT) {
+          s_enc[i] = cluster.map_shared_rank(s_enc, 0)[i];
+          s_lens[i] = cluster.map_shared_rank(s_lens, 0)[i];
+        }
+        __syncthreads();
+      }
+      // ---------------- phase 2a: Huffman bit count of this CTA's slice
+      unsigned long long b = 0;
+      uint32_t z = 0;
+      for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 32; base < v1; base += NT) {
+        const uint64_t v = base + lane;
+        if (v < v1) {
+          uint32_t w[4], nb;
+          load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            if (j < nb) {
+              uint32_t l = static_cast<uint32_t>(s_enc[byte_of(w, j)] >> 32);
+              b += l;
+              z |= (l == 0);
+            }
+          }
+        }
+      }
+      unsigned long long tb = block_reduce_sum(b, s_red);
+      uint32_t tz = block_reduce_max(z, s_red32);
+      if (tid == 0) {
+        s_ctrl.bits = tb;
+        s_ctrl.zero_len = tz;
+      }
+      cluster.sync();  // C
+      if (crank == 0 && tid == 0) {
+        unsigned long long bits = 0;
+        uint32_t zl = 0;
+        for (int r = 0; r < CL; ++r) {
+          Ctrl* c = cluster.map_shared_rank(&s_ctrl, r);
+          s_ctrl.slice_base[r] = bits;
+          bits += c->bits;
+          zl |= c->zero_len;
+        }
+        unsigned long long bytes = (bits + 7) / 8 + (embed ? ZC_HUFF_CODEBOOK_BYTES : 0);
+        bool ok = !zl && bytes > 0 && bytes <= pcap && (!autolike || gain_ok(R, bytes, p.cfg.min_gain_permil));
+        if (ok) {
+          s_ctrl.codec = ZC_CODEC_HUFFMAN;
+          s_ctrl.payload = bytes;
+        } else {
+          s_ctrl.codec = R <= pcap ? ZC_CODEC_RAW : CODEC_NONE;
+          s_ctrl.payload = R;
+          if (R > pcap && p.mode == ENC_SEND) err |= ZC_DERR_CAPACITY;
+        }
+      }
+      cluster.sync();  // D
+    }
+    const uint32_t codec = c0->codec;
+    const uint32_t width = c0->width;
+    const unsigned long long P = c0->payload;
+
+    // ---------------- phase 2b: materialise
+    if (codec == ZC_CODEC_RAW) {
+      for (uint64_t v = v0 + tid; v < v1; v += NT) {
+        uint32_t w[4], nb;
+        load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+        uint8_t* d = payload + v * 16;
+        if (nb == 16 && aligned16(d)) {
+          *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j)
+            if (j < nb) d[j] = static_cast<uint8_t>(byte_of(w, j));
+        }
+      }
+    } else if (codec == ZC_CODEC_FIXEDLEN) {
+      // warp-level bit packing: 128 symbols (32 vectors) -> 4*width words, LSB-first
+      uint32_t* zz = s_x.zz[warp];
+      const uint32_t w4 = 4 * width;
+      for (uint64_t c = v0 / 32 + warp; c * 32 < v1; c += NW) {
+        const uint64_t v = c * 32 + lane;
+        uint32_t w[4] = {0, 0, 0, 0}, nb = 0;
+        if (v < v1) load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          zz[lane * 4 + k] = (static_cast<uint32_t>(k) < (nb >> 2)) ? zigzag32(static_cast<int32_t>(w[k])) : 0u;
+        if (lane == 0) zz[128] = 0;
+        __syncwarp();
+        for (uint32_t k = lane; k < w4; k += 32) {
+          const uint32_t bitpos = k * 32;
+          uint32_t i = bitpos / width;
+          const uint32_t o = bitpos - i * width;
+          unsigned long long acc = zz[i] >> o;
+          uint32_t filled = width - o;
+          ++i;
+          while (filled < 32 && i < 128) {
+            acc |= static_cast<unsigned long long>(zz[i]) << filled;
+            filled += width;
+            ++i;
+          }
+          const uint64_t gw = c * w4 + k;
+          if (gw * 4 < P) store_word_safe(payload, gw, static_cast<uint32_t>(acc), P);
+        }
+        __syncwarp();
+      }
+    } else if (codec == ZC_CODEC_HUFFMAN) {
+      const uint64_t cb = (embed || (bare && p.embed)) ? ZC_HUFF_CODEBOOK_BYTES : 0;
+      uint8_t* sp = payload + cb;  // code stream start (after an embedded codebook)
+      const uint64_t Ps = P - cb;
+      if (cb && crank == 0)
+        for (int i = tid; i < 256; i += NT) payload[i] = embed ? s_lens[i] : s_clens[i];
+      unsigned long long base_bits = c0->slice_base[crank];
+      uint32_t* tile = s_x.tile;
+      for (int i = tid; i < TILE_WORDS; i += NT) tile[i] = 0;
+      bool first_tile = true;
+      uint32_t end_mod = 0;
+      __syncthreads();
+      for (uint64_t t0 = v0; t0 < v1; t0 += NT) {
+        const uint64_t v = t0 + tid;
+        uint32_t w[4] = {0, 0, 0, 0}, nb = 0;
+        if (v < v1) load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+        unsigned long long ev[16];
+        uint32_t L = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j) {
+          ev[j] = j < nb ? s_enc[byte_of(w, j)] : 0ull;
+          L += static_cast<uint32_t>(ev[j] >> 32);
+        }
+        uint32_t ttot;
+        const uint32_t off = block_excl_scan(L, s_red32, &ttot);
+        if (v < v1 && uindex != nullptr && (v & 63) == 0) uindex[v >> 6] = static_cast<uint32_t>(base_bits + off);
+        {
+          uint32_t lp = static_cast<uint32_t>(base_bits & 31) + off;
+          uint32_t wi = lp >> 5, nbit = lp & 31;
+          unsigned long long acc = 0;
+          bool firstw = true;
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            const unsigned long long e = ev[j];
+            if (!(e >> 32)) continue;
+            acc |= (e & 0xffffffffull) << nbit;
+            nbit += static_cast<uint32_t>(e >> 32);
+            if (nbit >= 32) {
+              if (firstw) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+              else tile[wi] = static_cast<uint32_t>(acc);
+              firstw = false;
+              ++wi;
+              acc >>= 32;
+              nbit -= 32;
+            }
+          }
+          if (nbit > 0) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+        }
+        __syncthreads();
+        const uint32_t endb = static_cast<uint32_t>(base_bits & 31) + ttot;
+        const uint32_t full = endb >> 5;
+        const uint64_t gw0 = base_bits >> 5;
+        for (uint32_t i = tid; i < full; i += NT) {
+          if (i == 0 && first_tile) {
+            s_bound[par].head_idx = gw0;
+            s_bound[par].head_val = tile[0];
+            s_bound[par].has_head = 1;
+          } else {
+            store_word_safe(sp, gw0 + i, tile[i], Ps);
+          }
+        }
+        const uint32_t carry = (endb & 31) ? tile[full] : 0u;
+        __syncthreads();
+        for (uint32_t i = tid; i <= full + 1 && i < static_cast<uint32_t>(TILE_WORDS); i += NT) tile[i] = 0;
+        __syncthreads();
+        if (tid == 0) tile[0] = carry;
+        if (full > 0) first_tile = false;
+        base_bits += ttot;
+        end_mod = static_cast<uint32_t>(base_bits & 31);
+        __syncthreads();
+      }
+      if (tid == 0 && v0 < v1 && end_mod != 0) {
+        s_bound[par].tail_idx = base_bits >> 5;
+        s_bound[par].tail_val = tile[0];
+        s_bound[par].has_tail = 1;
+      }
+      __syncthreads();
+    }
+    if (kRing) __threadfence_system();  // our peer-bank stores before CTA 0's release
+    cluster.sync();  // E: every CTA's output and boundary words complete
+
+    if (crank == 0 && tid == 0) {
+      if (codec == ZC_CODEC_HUFFMAN) {
+        const uint64_t cb = (embed || (bare && p.embed)) ? ZC_HUFF_CODEBOOK_BYTES : 0;
+        uint8_t* sp = payload + cb;
+        const uint64_t Ps = P - cb;
+        unsigned long long cur_idx = ~0ull;
+        uint32_t cur = 0;
+        for (int r = 0; r < CL; ++r) {
+          Bound* bd = &cluster.map_shared_rank(s_bound, r)[par];
+          for (int k = 0; k < 2; ++k) {
+            bool has = k == 0 ? bd->has_head : bd->has_tail;
+            if (!has) continue;
+            unsigned long long idx = k == 0 ? bd->head_idx : bd->tail_idx;
+            uint32_t val = k == 0 ? bd->head_val : bd->tail_val;
+            if (idx == cur_idx) {
+              cur |= val;
+            } else {
+              if (cur_idx != ~0ull) store_word_safe(sp, cur_idx, cur, Ps);
+              cur_idx = idx;
+              cur = val;
+            }
+          }
+        }
+        if (cur_idx != ~0ull) store_word_safe(sp, cur_idx, cur, Ps);
+      }
+      if (bare) {
+        if (p.bare_payload) p.bare_payload[u] = codec == CODEC_NONE ? 0ull : P;
+        if (p.bare_width) p.bare_width[u] = width;
+      } else if (p.mode != ENC_PROFILE) {
+        zc_encode_result res;
+        res._pad = 0;
+        if (codec == CODEC_NONE) {
+          res.codec = ZC_CODEC_RAW;
+          res.payload_bytes = 0;
+          res.total_bytes = 0;
+        } else {
+          const uint16_t flags = (codec == ZC_CODEC_HUFFMAN && embed) ? ZC_FLAG_EMBEDDED_CODEBOOK : 0;
+          const uint64_t params = codec == ZC_CODEC_FIXEDLEN                 ? width
+                                  : (codec == ZC_CODEC_HUFFMAN && embed) ? ZC_HUFF_CODEBOOK_BYTES
+                                                                          : 0;
+          zc_frame_header h = make_header(codec, flags, R, P, params);
+          uint64_t hw[4];
+          header_words(h, hw);
+          uint64_t* hp = reinterpret_cast<uint64_t*>(stage);
+          hp[0] = hw[0];
+          hp[1] = hw[1];
+          hp[2] = hw[2];
+          hp[3] = hw[3];
+          res.codec = codec;
+          res.payload_bytes = P;
+          res.total_bytes = kHeaderBytes + P;
+        }
+        if (p.results) p.results[u] = res;
+        if (kRing && codec != CODEC_NONE) {
+          wire_add(p.L.wire, codec, R, P, codec == ZC_CODEC_HUFFMAN ? 4 * ((R + kIndexGrain - 1) / kIndexGrain) : 0);
+          __threadfence_system();
+          p.L.tx_len[tx_bank] = kHeaderBytes + P;
+          st_release_sys(&p.L.tx_ready[tx_bank], tx_seq);
+        }
+      }
+    }
+    __syncthreads();
+    }  // ======== end of send part
+
+    if (u < n_rx) {  // ======== receive part: predecessor's frame -> decode -> add / store
+      const uint64_t rR = (p.rx_total_bytes - uoff) < p.unit_bytes ? (p.rx_total_bytes - uoff) : p.unit_bytes;
+      uint64_t r0, r1;
+      unit_slice(rR, crank, r0, r1);
+      const uint64_t rx_seq = p.L.rx_seq0 + u + 1;
+      const uint64_t rx_bank = (p.L.rx_seq0 + u) % p.L.nbanks;
+      const uint8_t* rx_stage = p.L.rx_banks + rx_bank * p.L.bank_stride;
+      if (crank == 0 && tid == 0) {
+        bool ok = wait_geq(&p.L.rx_ready[rx_bank], rx_seq, p.L);
+        s_ctrl.go = ok ? 1u : 0u;
+        s_ctrl.rx_len = ok ? ld_acquire_sys(&p.L.rx_len[rx_bank]) : 0ull;
+      }
+      cluster.sync();
+      const Ctrl* c0 = cluster.map_shared_rank(&s_ctrl, 0);
+      const uint32_t go = c0->go;
+      const unsigned long long rlen = c0->rx_len;
+      if (go) {
+        if (tid == 0) check_frame<true>(rx_stage, rlen, rR, nullptr, false, p.ctx, true, s_fc);
+        __syncthreads();
+        Sink sink{p.rx_store ? OUT_BYTES : OUT_ADD_I32, p.rx_dst, 1.0};
+        uint32_t f = decode_slice<true>(s_fc, rx_stage + kHeaderBytes, rR, r0, r1, sink, uoff,
+                                        reinterpret_cast<const uint32_t*>(rx_stage + p.L.idx_off), p.ctx, &s_x.dec.t,
+                                        &s_flag, s_lens, s_x.dec.words, err);
+        if (s_fc.codec == kFallback || f) err |= ZC_DERR_CORRUPT;
+      } else {
+        err |= ZC_DERR_ABORT;
+      }
+      __syncthreads();
+      cluster.sync();  // every CTA is done with the receive bank
+      if (crank == 0 && tid == 0 && go) st_release_sys(&p.L.rx_credit[rx_bank], rx_seq);
+      __syncthreads();
+    }
+  }
+  // CTA 0 reads its peers' shared memory after the last barrier of a unit: nobody may exit first.
+  cluster.sync();
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err) {
+    if (kRing) broadcast_err(p.L, err);
+    else atomicOr(p.err, err);
+  }
+}
+
+int g_max_clusters = -1;
+
+template <typename K>
+int query_max_clusters(K kern) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(NT);
+  cfg.gridDim = dim3(CL * 64);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 16;
+  }
+  return n;
+}
+
+template <typename K, typename P>
+cudaError_t launch_cluster(K kern, const P& p, uint32_t nunits, int cap, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(NT);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int mc = encode_max_clusters();
+  int ncl = std::min<int>(static_cast<int>(nunits), cap > 0 ? std::min(cap, mc) : mc);
+  cfg.gridDim = dim3(CL * std::max(1, ncl));
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int SRC>
+cudaError_t launch_t(const EncParams& p, cudaStream_t s) {
+  if (p.link_tx || p.link_rx_add) {
+    const uint32_t units = std::max(p.link_tx ? p.nunits : 0u, p.link_rx_add ? p.rx_nunits : 0u);
+    return launch_cluster(encode_kernel<SRC, true>, p, units, p.L.max_clusters, s);
+  }
+  return launch_cluster(encode_kernel<SRC, false>, p, p.nunits, 0, s);
+}
+
+}  // namespace
+
+// Forces module loading of every kernel here.  With lazy loading, the first launch of a kernel
+// can wait for the device to go idle — fatal when a peer-waiting ring kernel is running.
+void preload_encode_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_BYTES, false>);
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_BYTES, true>);
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_F32, false>);
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_F32, true>);
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_F64, false>);
+  cudaFuncGetAttributes(&a, encode_kernel<SRC_F64, true>);
+  encode_max_clusters();
+  cudaGetLastError();
+}
+
+// Persistent-grid size: the smaller of what fits co-resident and the L2 residency cap (in-flight
+// units x 4 MiB kept well inside the 126 MB L2 so phase-2 re-reads hit).  ZC_ENCODE_CLUSTERS
+// overrides the cap for experiments.
+int encode_max_clusters() {
+  if (g_max_clusters < 0) {
+    int n = std::min(query_max_clusters(encode_kernel<SRC_F32, false>), query_max_clusters(encode_kernel<SRC_BYTES, true>));
+    const char* env = std::getenv("ZC_ENCODE_CLUSTERS");
+    int cap = env ? std::atoi(env) : 16;
+    g_max_clusters = std::max(1, std::min(n, cap));
+  }
+  return g_max_clusters;
+}
+
+cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
+  if (p.nunits == 0 && !(p.link_rx_add && p.rx_nunits > 0)) return cudaSuccess;
+  switch (p.src_kind) {
+    case SRC_F32:
+      return launch_t<SRC_F32>(p, s);
+    case SRC_F64:
+      return launch_t<SRC_F64>(p, s);
+    default:
+      return launch_t<SRC_BYTES>(p, s);
+  }
+}
+
+
+}  // namespace zc

@@ -1,0 +1,123 @@
+// zc_kernels.h — host launchers of the sm_100a kernels (internal to libzcomm_b200.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zc_common.cuh"
+
+namespace zc {
+
+enum SrcKind : int { SRC_BYTES = 0, SRC_F32 = 1, SRC_F64 = 2 };
+enum OutKind : int { OUT_BYTES = 0, OUT_F32 = 1, OUT_F64 = 2, OUT_ADD_I32 = 3 };
+
+// Encode modes.
+enum EncMode : int {
+  ENC_SEND = 0,     // send_batch semantics: pin dispatch, raw fallback, capacity error bit
+  ENC_BEST = 1,     // encode_best semantics (result {0,0,0} instead of an error bit)
+  ENC_BARE_FL = 2,  // fixedlen_encode: bare payload, no header, 0 on capacity shortfall
+  ENC_BARE_HF = 3,  // huffman_encode: bare payload (+ codebook when embed), 0 on failure
+  ENC_PROFILE = 4,  // profile_sample only
+};
+
+// One rank's view of its two ring links (collectives.cpp:76-84 links, transport.hpp:106-134
+// staging banks).  Receive banks live in the RECEIVER's HBM; the sender's kernel stores the
+// frame straight into them over NVLink (or same-device memory in loopback groups) and publishes
+// {length, sequence} with a system-scope release; the receiver's kernel acquires the sequence,
+// consumes the frame and returns the bank with a release on the sender's credit word.
+struct Link {
+  uint8_t* tx_banks;               // successor's receive banks (peer-mapped)
+  unsigned long long* tx_ready;    // successor's ready words [nbanks]
+  unsigned long long* tx_len;      // successor's frame-length words [nbanks]
+  unsigned long long* tx_credit;   // our credit words [nbanks], written by the successor
+  const uint8_t* rx_banks;         // our receive banks
+  unsigned long long* rx_ready;    // our ready words
+  unsigned long long* rx_len;      // our frame-length words
+  unsigned long long* rx_credit;   // predecessor's credit words (peer-mapped)
+  uint64_t bank_stride;            // bytes per bank (frame region + companion index)
+  uint64_t idx_off;                // companion index offset inside a bank
+  uint32_t nbanks;
+  uint32_t nranks;
+  uint64_t tx_seq0, rx_seq0;       // frames already sent / received on this link
+  uint32_t* err_self;              // our error word
+  uint32_t* const* err_all;        // every rank's error word (device array of peer pointers)
+  unsigned long long timeout_ns;
+  zc_wire_stats* wire;             // device-side WireStats accumulation (own memory)
+  int max_clusters;                // residency cap for this launch (loopback groups share a GPU)
+};
+
+struct EncParams {
+  const void* src;
+  int src_kind;
+  int mode;
+  int pin;
+  int embed;           // bare huffman: prepend codebook
+  double scale, rcp;   // float sources
+  uint64_t total_bytes;
+  uint64_t unit_bytes;
+  uint32_t nunits;
+  uint32_t _pad;
+  uint8_t* stages;
+  uint64_t stride;
+  uint64_t stage_len;  // bytes available at each stage (header included unless bare)
+  zc_transport_hint hint;
+  zc_arb_config cfg;
+  const DevHuff* ctx;  // may be null
+  zc_encode_result* results;
+  uint32_t* index;     // companion index, index_stride u32 per unit (may be null)
+  uint64_t index_stride;
+  uint32_t* err;
+  zc_sample_stats* stats;  // per-unit stats (may be null)
+  uint64_t* bare_payload;  // bare modes: payload bytes
+  uint32_t* bare_width;    // bare fixedlen: width
+  // ring mode (fused reduce-scatter step): frames go to the successor's banks; with rx_add the
+  // predecessor's frame for the same unit is first decoded and added into `src` (the local
+  // chunk), and the sum is what gets encoded — decode -> reduce -> re-encode in one kernel.
+  int link_tx;
+  int link_rx_add;  // receive part enabled (the reduce-scatter sink adds)
+  int rx_store;     // receive sink stores the decoded symbols instead of adding (all-gather step)
+  void* rx_dst;     // incoming chunk (local symbols)
+  uint64_t rx_total_bytes;
+  uint32_t rx_nunits;
+  Link L;
+};
+
+struct DecParams {
+  const uint8_t* stages;
+  uint64_t stride;
+  uint64_t region;         // bytes of each received region when frame_len is null
+  const zc_encode_result* frame_len;  // per-unit committed frame (total_bytes) or null
+  uint64_t total_bytes;    // raw bytes of the message
+  uint64_t unit_bytes;
+  uint32_t nunits;
+  int out_kind;
+  void* out;
+  double scale;            // dequantization factor for OUT_F32 / OUT_F64
+  const DevHuff* ctx;
+  const uint32_t* index;   // may be null
+  uint64_t index_stride;
+  uint32_t* codec_out;     // per unit decoded codec, or 0xFFFFFFFF for the raw fallback (may be null)
+  uint32_t* flags;         // per unit scratch: 1 = needs sequential Huffman decode (device, >= nunits)
+  uint32_t* err;
+  int bare;                // bare decode: `stages` is one payload and `hdr` describes it
+  zc_frame_header hdr;
+  int32_t* ok_out;         // bare decode result
+};
+
+cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
+int encode_max_clusters();
+// Force module loading of every kernel (lazy loading may otherwise stall a launch behind a
+// running peer-waiting kernel).
+void preload_encode_kernels();
+void preload_decode_kernels();
+void preload_quant_kernels();
+cudaError_t launch_decode(const DecParams& p, cudaStream_t s);
+cudaError_t launch_absmax(const void* x, int src_kind, uint64_t n, double* out, uint32_t* err, cudaStream_t s);
+cudaError_t launch_quantize(const void* x, int src_kind, uint64_t n, double scale, int32_t* sym, uint32_t* err,
+                            cudaStream_t s);
+cudaError_t launch_dequantize(const int32_t* sym, uint64_t n, double k, int prequant, void* out, int out_f64,
+                              cudaStream_t s);
+cudaError_t launch_commit_raw(const uint8_t* raw, uint64_t n, uint8_t* region, uint64_t cap, uint64_t* total,
+                              cudaStream_t s);
+cudaError_t launch_hist(const uint8_t* d, uint64_t n, uint64_t* hist, cudaStream_t s);
+
+}  // namespace zc

@@ -1,0 +1,386 @@
+"""GPU parity: quantizer, frame, FixedLen, Huffman, selector and encode_best on sm_100a vs the
+oracle (oracle/zc_oracle.c, itself pinned to the compiled reference in test_oracle.py).
+
+Bar: bit-exact symbols, selector decisions, frame bytes; round trips exact."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_12396_b200 import abi
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
+DEV = "cuda"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def npy(x):
+    return x.cpu().numpy()
+
+
+def hdr(codec, raw, payload, params, flags=0):
+    h = abi.FrameHeader()
+    h.magic, h.version, h.codec, h.flags = abi.FRAME_MAGIC, abi.FRAME_VERSION, codec, flags
+    h.raw_bytes, h.payload_bytes, h.params = raw, payload, params
+    return h
+
+
+# ------------------------------------------------------------------ quantizer
+def _tie_heavy(n, scale, rng):
+    """Values whose quotient lands exactly on / right next to half-integers."""
+    k = rng.integers(-30000, 30000, n).astype(np.float64)
+    x = (k + 0.5) * scale
+    x[::3] = np.nextafter(x[::3], np.inf)
+    x[1::3] = np.nextafter(x[1::3], -np.inf)
+    return x
+
+
+@pytest.mark.parametrize("scale", [2e-4, 0.21, 1.0, 3.0e-7, 0.1])
+def test_quantize_f64_bitexact(zc, port, scale):
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.normal(0, 3, 200001), _tie_heavy(50000, scale, rng), [0.0, -0.0, scale / 2, -scale / 2]])
+    got = npy(zc.eb_quantize_with_scale(t(x), scale))
+    exp = np.zeros(len(x), np.int32)
+    assert port.lib.zo_eb_quantize_f64(x, len(x), scale, exp) == 0
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("scale", [2e-4, 2e-3 * 3.7, 1e-6])
+def test_quantize_f32_bitexact(zc, port, scale):
+    rng = np.random.default_rng(2)
+    x = np.concatenate([rng.normal(0, 1, 1 << 20), _tie_heavy(1 << 16, scale, rng)]).astype(np.float32)
+    got = npy(zc.eb_quantize_with_scale(t(x), scale))
+    rc, exp = port.eb_quantize_f32(x, scale)
+    assert rc == 0 and np.array_equal(got, exp)
+
+
+def test_quantize_hand_example_and_errors(zc):
+    # quant.cpp hand example (test_quant.cpp:20-30): [1.0, 1.05], rel 0.1 -> scale 0.21, symbols [5, 5]
+    sym, scale = zc.eb_quantize(t(np.array([1.0, 1.05], np.float32)), 0.1)
+    assert abs(scale - 0.21) < 1e-7 and npy(sym).tolist() == [5, 5]
+    sym, scale = zc.eb_quantize(t(np.zeros(3, np.float32)), 1e-4)
+    assert scale == 1.0 and npy(sym).tolist() == [0, 0, 0]
+    with pytest.raises(ValueError):
+        zc.eb_quantize_with_scale(t(np.array([1.0, np.nan])), 0.1)
+    with pytest.raises(ValueError):
+        zc.eb_quantize_with_scale(t(np.array([np.inf])), 0.1)
+    with pytest.raises(ValueError):
+        zc.eb_quantize_with_scale(t(np.array([3.0e9])), 1.0)
+    with pytest.raises(ValueError):
+        zc.eb_quantize(t(np.array([1.0], np.float32)), 1.5)
+    with pytest.raises(ValueError):
+        zc.eb_quantize_with_scale(t(np.array([1.0])), 0.0)
+
+
+def test_dequantize_bitexact(zc, port):
+    rng = np.random.default_rng(3)
+    s = rng.integers(-2**31, 2**31, 100003, dtype=np.int64).astype(np.int32)
+    for mode, scale, levels in [(0, 2e-4, 0), (1, 3.75, 7), (2, 1.0, 0)]:
+        exp = np.zeros(len(s))
+        port.lib.zo_dequantize_f64(s, len(s), mode, scale, levels, exp)
+        got = npy(zc.dequantize(t(s), mode, scale, levels, torch.float64))
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+        got32 = npy(zc.dequantize(t(s), mode, scale, levels, torch.float32))
+        assert np.array_equal(got32, exp.astype(np.float32))
+
+
+# ------------------------------------------------------------------ frame
+def test_header_roundtrip_and_validate(zc, port):
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        h = hdr(int(rng.integers(0, 3)), int(rng.integers(1, 2**40)), int(rng.integers(0, 2**40)),
+                int(rng.integers(0, 2**63)), int(rng.integers(0, 2**16)))
+        b = zc.write_header(h)
+        ob = np.zeros(32, np.uint8)
+        port.lib.zo_write_header(C.byref(h), ob)
+        assert b == ob.tobytes()
+        g = zc.parse_header(b)
+        assert (g.magic, g.codec, g.raw_bytes, g.payload_bytes, g.params, g.flags) == \
+            (h.magic, h.codec, h.raw_bytes, h.payload_bytes, h.params, h.flags)
+        for region in (31, 32, 33, h.payload_bytes + 32, h.payload_bytes + 31):
+            assert zc.validate_header(h, region) == bool(port.lib.zo_validate_header(C.byref(h), region))
+    assert zc.parse_header(b"\0" * 31) is None
+
+
+def test_commit_raw_capacity(zc):
+    raw = t(np.arange(8, dtype=np.uint8))
+    assert zc.frame_commit_raw(raw, torch.zeros(40, dtype=torch.uint8, device=DEV)) == 40
+    assert zc.frame_commit_raw(raw, torch.zeros(39, dtype=torch.uint8, device=DEV)) == 0
+
+
+# ------------------------------------------------------------------ fixedlen
+def test_fixedlen_golden(zc):
+    # test_fixedlen.cpp:51-75, 115-125
+    p, w = zc.fixedlen_encode(t(np.array([0, 1, -1, 2], np.int32)), 8)
+    assert w == 3 and npy(p).tolist() == [0x50, 0x08]
+    p, w = zc.fixedlen_encode(t(np.zeros(4, np.int32)), 8)
+    assert w == 1 and npy(p).tolist() == [0]
+    p, w = zc.fixedlen_encode(t(np.array([-2**31, 2**31 - 1, 0, -1], np.int32)), 32)
+    assert w == 32 and p.numel() == 16
+    ok, back = zc.fixedlen_decode(hdr(1, 16, 16, 32), p, 16)
+    assert ok and npy(back).view(np.int32).tolist() == [-2**31, 2**31 - 1, 0, -1]
+    p, w = zc.fixedlen_encode(t(np.array([100, -200, 300], np.int32)), 2)
+    assert p.numel() == 0
+
+
+def test_fixedlen_random_vs_oracle(zc, port):
+    rng = np.random.default_rng(9)
+    for it in range(60):
+        n = int(rng.integers(1, 5000)) if it % 3 else int(rng.integers(100000, 300000))
+        shift = int(rng.integers(0, 28))
+        s = (rng.integers(-2**31, 2**31, n, dtype=np.int64) >> shift).astype(np.int32)
+        cap = 4 * n + 8
+        out = np.zeros(cap, np.uint8)
+        w = C.c_uint32()
+        pn = port.lib.zo_fixedlen_encode(s, n, out, cap, C.byref(w))
+        got, gw = zc.fixedlen_encode(t(s), cap)
+        assert gw == w.value and got.numel() == pn
+        assert np.array_equal(npy(got), out[:pn])
+        ok, back = zc.fixedlen_decode(hdr(1, 4 * n, pn, gw), got, 4 * n)
+        assert ok and np.array_equal(npy(back).view(np.int32), s)
+
+
+def test_fixedlen_decode_rejects(zc):
+    p, w = zc.fixedlen_encode(t(np.array([1, 2, 3, 4, 5], np.int32)), 32)
+    assert not zc.fixedlen_decode(hdr(1, 20, p.numel(), 0), p, 20)[0]
+    assert not zc.fixedlen_decode(hdr(1, 20, p.numel(), 33), p, 20)[0]
+    assert not zc.fixedlen_decode(hdr(1, 18, p.numel(), w), p, 20)[0]
+    assert not zc.fixedlen_decode(hdr(1, 20, p.numel() - 1, w), p, 20)[0]
+    assert not zc.fixedlen_decode(hdr(1, 20, p.numel(), w), p, 19)[0]
+
+
+# ------------------------------------------------------------------ huffman
+def _hist(b):
+    return np.bincount(np.asarray(b, np.uint8), minlength=256).astype(np.uint64)
+
+
+def test_huffman_context_matches_oracle(zc, port):
+    rng = np.random.default_rng(5)
+    cases = [np.array([1, 1, 2, 2] + [0] * 252, np.uint64)]
+    cases[0] = np.zeros(256, np.uint64)
+    cases[0][[10, 20, 30, 40]] = [1, 1, 2, 2]
+    fib = np.zeros(256, np.uint64)
+    a, b = 1, 1
+    for i in range(40):
+        fib[i] = a
+        a, b = b, a + b
+    cases.append(fib)
+    for _ in range(60):
+        h = np.zeros(256, np.uint64)
+        live = int(rng.integers(1, 256))
+        h[rng.choice(256, live, replace=False)] = rng.integers(1, 10**6, live)
+        cases.append(h)
+    for h in cases:
+        c = zc.HuffmanContext.from_hist(h)
+        o = port.huff_from_hist(h)
+        assert c.valid == bool(o.valid)
+        assert c.code_lengths == list(o.len)
+        code, rev = c.codes()
+        assert code == list(o.code) and rev == list(o.rev)
+    # tie-break pin: weights {1,1,2,2} on {10,20,30,40} -> all length 2
+    c = zc.HuffmanContext.from_hist(cases[0])
+    assert [c.code_lengths[s] for s in (10, 20, 30, 40)] == [2, 2, 2, 2]
+    assert not zc.HuffmanContext.from_hist(np.zeros(256, np.uint64)).valid
+
+
+@pytest.mark.parametrize("n", [1, 100, 1023, 1024, 1025, 65536, 300001, 4 << 20])
+def test_huffman_encode_decode_vs_oracle(zc, port, n):
+    rng = np.random.default_rng(n)
+    raw = np.minimum(rng.geometric(0.3, n) - 1, 255).astype(np.uint8)
+    sample = raw[: min(n, 1 << 20)]
+    c = zc.HuffmanContext.from_bytes(sample)
+    o = port.huff_from_bytes(sample)
+    cap = 2 * n + 64
+    out = np.zeros(cap, np.uint8)
+    pn = port.lib.zo_huffman_encode(raw, n, C.byref(o), out, cap, 0)
+    got, idx = zc.huffman_encode(t(raw), c, cap, with_index=True)
+    assert got.numel() == pn and np.array_equal(npy(got), out[:pn])
+    h = hdr(2, n, pn, 0)
+    ok, back = zc.huffman_decode(h, got, c, n, index=idx)
+    assert ok and np.array_equal(npy(back), raw)
+    if n <= 65536:  # sequential path (frames without a companion index)
+        ok, back = zc.huffman_decode(h, got, c, n)
+        assert ok and np.array_equal(npy(back), raw)
+
+
+def test_huffman_embedded_and_failures(zc, port):
+    raw = np.full(1000, 7, np.uint8)
+    c = zc.HuffmanContext.from_hist(_hist(raw))
+    p = zc.huffman_encode(t(raw), c, 256 + 1000, embed=True)
+    assert p.numel() == 256 + 125  # test_huffman.cpp:112-123
+    ok, back = zc.huffman_decode(hdr(2, 1000, p.numel(), 256, abi.FLAG_EMBEDDED_CODEBOOK), p, None, 1000)
+    assert ok and np.array_equal(npy(back), raw)
+    # unseen symbol under the shared context -> failure sentinel 0
+    c2 = zc.HuffmanContext.from_hist(_hist(np.array([1, 2, 3], np.uint8)))
+    assert zc.huffman_encode(t(np.array([1, 9], np.uint8)), c2, 64).numel() == 0
+    # capacity shortfall
+    assert zc.huffman_encode(t(np.arange(256, dtype=np.uint8)), zc.HuffmanContext.from_bytes(b""), 10).numel() == 0
+    # shared frame without a context / with params != 0
+    p = zc.huffman_encode(t(raw), c, 2000)
+    assert not zc.huffman_decode(hdr(2, 1000, p.numel(), 0), p, None, 1000)[0]
+    assert not zc.huffman_decode(hdr(2, 1000, p.numel(), 5), p, c, 1000)[0]
+    # truncated stream -> overrun
+    assert not zc.huffman_decode(hdr(2, 1000, p.numel() - 1, 0), p[:-1], c, 1000)[0]
+
+
+# ------------------------------------------------------------------ selector
+def _stats_equal(a, b):
+    return (a.sampled_bytes == b.sampled_bytes and list(a.hist) == list(b.hist) and a.max_zigzag == b.max_zigzag
+            and a.ctx_code_len_valid == b.ctx_code_len_valid and a.self_code_len_valid == b.self_code_len_valid
+            and (not a.ctx_code_len_valid or a.ctx_code_len_bits == b.ctx_code_len_bits)
+            and (not a.self_code_len_valid or a.self_code_len_bits == b.self_code_len_bits))
+
+
+@pytest.mark.parametrize("n", [0, 3, 4096, 65535, 65536, 65537, 1 << 20])
+def test_profile_sample_vs_oracle(zc, port, n):
+    rng = np.random.default_rng(n + 11)
+    raw = (rng.normal(0, 300, (n + 3) // 4).astype(np.int32)).view(np.uint8)[:n]
+    sample = raw[: min(n, 1 << 16)]
+    c = zc.HuffmanContext.from_bytes(sample)
+    o = port.huff_from_bytes(sample)
+    for with_ctx in (False, True):
+        got = zc.profile_sample(t(raw) if n else torch.zeros(0, dtype=torch.uint8, device=DEV), c if with_ctx else None)
+        exp = port.profile(raw, o if with_ctx else None)
+        assert _stats_equal(got, exp)
+
+
+def test_arbitrate_random_triples_vs_oracle(zc, port):
+    """Host build of the selector vs the oracle (test_rea.cpp:186-225 style)."""
+    rng = np.random.default_rng(63)
+    shared = port.huff_from_bytes(np.minimum(rng.geometric(0.3, 65536) - 1, 255).astype(np.uint8))
+    gshared = zc.HuffmanContext.from_lengths(list(shared.len))
+    for k in range(300):
+        p = 0.05 + 0.9 * rng.random()
+        raw = np.minimum(rng.geometric(p, 8192 + int(rng.integers(0, 65536))) - 1, 255).astype(np.uint8)
+        use = k % 3 != 0
+        st = port.profile(raw, shared if use else None)
+        cfg = abi.default_arb_config()
+        cfg.min_gain_permil = int(rng.integers(0, 200))
+        cfg.lam_enc = int(rng.integers(0, 101)) / 100.0
+        cfg.lam_dec = int(rng.integers(0, 101)) / 100.0
+        cfg.embed_codebook = 1 if k % 4 == 0 else 0
+        cfg.huffman_min_raw_bytes = 1 << int(rng.integers(10, 18))
+        hint = abi.make_hint(10 ** (8 + 3.5 * rng.random()), k & 1)
+        cap = len(raw) // 2 + int(rng.integers(0, 2 * len(raw)))
+        plan = zc.arbitrate_plan(len(raw), cap, st, hint, gshared if use else None, cfg)
+        exp = abi.ArbitrationPlan()
+        port.lib.zo_arbitrate_plan(len(raw), cap, C.byref(st), C.byref(hint), C.byref(shared) if use else None,
+                                   C.byref(cfg), C.byref(exp))
+        assert bytes(plan) == bytes(exp)
+
+
+def _stream_cases():
+    rng = np.random.default_rng(79)
+    geo = np.minimum(rng.geometric(0.7, 1 << 20) - 1, 255).astype(np.int32)
+    return {
+        "const0": np.zeros(1 << 20, np.int32),
+        "narrow": (rng.integers(0, 7, 60000) - 3).astype(np.int32),
+        "wide_skew": np.where(rng.integers(0, 2, 60000) == 1, 0x40000000, -0x40000000).astype(np.int32),
+        "noise": rng.integers(0, 256, 240000).astype(np.uint8),
+        "geometric": geo,
+        "gauss": (rng.normal(0, 1, 1 << 20) / 2e-4).round().astype(np.int32),
+        "small": np.arange(1000, dtype=np.int32),
+        "odd_bytes": rng.integers(0, 4, 100003).astype(np.uint8),
+        "adversarial": np.concatenate([np.zeros(64 * 1024, np.uint8), rng.integers(0, 256, 192 * 1024).astype(np.uint8)]),
+    }
+
+
+@pytest.mark.parametrize("beta", [1.0e9, 10 * 2**30, 200 * 2**30, 900e9])
+def test_encode_best_frames_vs_oracle(zc, port, beta):
+    cases = _stream_cases()
+    sample = cases["wide_skew"].view(np.uint8)
+    c, o = zc.HuffmanContext.from_bytes(sample), port.huff_from_bytes(sample)
+    cfg = abi.default_arb_config()
+    cfg.huffman_min_raw_bytes = 16 * 1024
+    hint = abi.make_hint(beta)
+    for name, arr in cases.items():
+        raw = arr.view(np.uint8)
+        for cap in (abi.STAGE_BANK_BYTES, len(raw) + 32, len(raw) // 2 + 40):
+            r, frame = zc.encode_best(t(raw), cap, hint, c, cfg)
+            er = abi.EncodeResult()
+            stage = np.zeros(cap, np.uint8)
+            port.lib.zo_encode_best(raw, len(raw), stage, cap, C.byref(hint), C.byref(o), C.byref(cfg), C.byref(er))
+            assert (r.codec, r.payload_bytes, r.total_bytes) == (er.codec, er.payload_bytes, er.total_bytes), (name, cap)
+            assert np.array_equal(npy(frame), stage[: er.total_bytes]), (name, cap)
+
+
+def test_encode_best_degenerate(zc):
+    hint = abi.make_hint(1e10)
+    r, _ = zc.encode_best(torch.zeros(0, dtype=torch.uint8, device=DEV), 1024, hint)
+    assert r.total_bytes == 0
+    raw = t(np.ones(100, np.uint8))
+    assert zc.encode_best(raw, 32, hint)[0].total_bytes == 0
+    assert zc.encode_best(raw, 82, hint)[0].total_bytes == 0
+    r, f = zc.encode_best(t(np.zeros(4096, np.uint8)), abi.STAGE_BANK_BYTES, abi.make_hint(1e9))
+    assert (r.codec, r.payload_bytes, r.total_bytes) == (0, 4096, 4128)
+
+
+def test_selector_stress_c4(zc, port):
+    """BASELINE config 4: constant / low-entropy / uniform batches -> FixedLen / Huffman / RAW at 10 GiB/s."""
+    rng = np.random.default_rng(0xC4)
+    b0 = np.zeros(1 << 20, np.int32)
+    x = port.gen_data(2, 5, 0, 1 << 20, geom_p=0.7)
+    amax = np.abs(x).max()
+    b1 = np.zeros(1 << 20, np.int32)
+    port.lib.zo_eb_quantize_f64(x, len(x), 2 * 1e-4 * amax, b1)
+    b2 = rng.integers(0, 2**32, 1 << 20, dtype=np.uint64).astype(np.uint32).view(np.int32)
+    msg = np.concatenate([b0, b1, b2])
+    sample = msg.view(np.uint8)
+    c, o = zc.HuffmanContext.from_bytes(sample), port.huff_from_bytes(sample)
+    fr = zc.encode_batches(t(msg), abi.PIN_AUTO, ctx=c)
+    codecs = [r.codec for r in fr.encode_results()]
+    exp = port.encode_batches(msg, abi.PIN_AUTO, ctx=o)
+    assert codecs == [e[0].codec for e in exp] == [abi.CODEC_FIXEDLEN, abi.CODEC_HUFFMAN, abi.CODEC_RAW]
+    for b, (er, ef) in enumerate(exp):
+        assert np.array_equal(npy(fr.frame(b)), ef)
+    back = zc.decode_batches(fr, c)
+    assert np.array_equal(npy(back), msg)
+
+
+# ------------------------------------------------------------------ batched hot path
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_RAW, abi.PIN_FIXEDLEN, abi.PIN_HUFFMAN])
+@pytest.mark.parametrize("count", [1000, 1 << 20, (9 << 20) // 4 + 3])
+def test_encode_batches_f32_fused_vs_oracle(zc, port, pin, count):
+    rng = np.random.default_rng(count + pin)
+    x = rng.normal(0, 1, count).astype(np.float32)
+    scale = 2e-4
+    rc, sym = port.eb_quantize_f32(x, scale)
+    assert rc == 0
+    raw = sym.view(np.uint8)
+    sample = raw[: 4 << 20]
+    c, o = zc.HuffmanContext.from_bytes(sample), port.huff_from_bytes(sample)
+    hint = abi.make_hint()
+    fr = zc.encode_batches(t(x), pin, scale=scale, hint=hint, ctx=c)
+    fr2 = zc.encode_batches(t(sym), pin, hint=hint, ctx=c)
+    exp = port.encode_batches(raw, pin, hint, o)
+    assert fr.nbatches == len(exp)
+    for b, (er, ef) in enumerate(exp):
+        for f in (fr, fr2):
+            r = f.encode_results()[b]
+            assert (r.codec, r.payload_bytes, r.total_bytes) == (er.codec, er.payload_bytes, er.total_bytes)
+            assert np.array_equal(npy(f.frame(b)), ef)
+    assert np.array_equal(npy(zc.decode_batches(fr, c)), sym)
+    y = npy(zc.decode_batches(fr, c, scale=scale))
+    deq = np.zeros(count, np.float32)
+    port.lib.zo_dequantize_f32(sym, count, 0, scale, 0, deq)
+    assert np.array_equal(y, deq)
+    assert np.max(np.abs(y.astype(np.float64) - x)) <= scale / 2 * (1 + 1e-6) + 1e-7
+
+
+def test_decode_fallback_on_corrupt_header(zc, port):
+    rng = np.random.default_rng(0xC5)
+    sym = (rng.integers(0, 512, 300000) - 256).astype(np.int32)
+    fr = zc.encode_batches(t(sym), abi.PIN_AUTO)
+    # corrupt the magic of the only frame: raw-copy fallback of the payload region
+    fr.stages[0] ^= 0xFF
+    codecs = torch.zeros(1, dtype=torch.int32, device=DEV)
+    out = zc.decode_batches(fr, None, codecs=codecs)
+    frame = npy(fr.stages[: fr.encode_results()[0].total_bytes])
+    cdc, exp = port.recv_batch(frame, len(sym) * 4)
+    assert cdc == -1 and int(codecs.item()) == -1
+    have = len(frame) - 32  # min(dst, have) bytes are the payload region verbatim (collectives.cpp:330-336)
+    assert np.array_equal(npy(out).view(np.uint8)[:have], exp[:have])
