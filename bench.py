@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 compressed-collectives hot path.
+
+N=1 (default): BASELINE config 0 — single-rank codec round trip on 64 Mi synthetic Gaussian fp32
+elements, absolute error bound 1e-4 (bin width 2e-4): fused quantize + 64 KiB histogram + selector
++ encode into 4 MiB-batch frames, then decode + dequantize back to fp32.  One step = one round
+trip over the whole array.  value = codec GB/s over raw symbol bytes (4 B/element, the
+codec_bench.cpp:49 convention) per round trip.  The selector runs with the reference's default
+inter-node hint (10 GiB/s, transport.hpp:33-35), so it picks FixedLen on Gaussian data; the
+Huffman-pinned round trip of the same config is reported beside it.
+
+N>1 (torchrun): compressed ring AllReduce (allreduce_eb) of BASELINE config 1 (N=2: 256 MB
+Laplacian per rank, abs eb 1e-4) or config 2 (N=4/8: 512^3 smooth field per rank, rel 1e-3);
+value = algbw = bytes per rank / time (the max over ranks).
+
+--impl reference: the reference's own CPU implementation of the same round trip (oracle/_ref,
+compiled from /root/reference sources) on all host cores, over a bounded sample per step.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+COUNT_C0 = 64 << 20          # config 0: 64 Mi fp32 elements
+ABS_EB = 1e-4
+SCALE = 2 * ABS_EB           # eb_quantize_with_scale bin width for an absolute bound
+BETA = 10.0 * 1073741824.0   # reference default hint (inter-node, 10 GiB/s)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic(kernel):
+    """dram read+write bytes per launch from the committed ncu capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------- N = 1
+def codec_bench(args):
+    import torch
+    from paper_2605_12396_b200 import abi, zcomm
+
+    L = zcomm.lib()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    count = args.count
+    raw_bytes = 4 * count
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    x = torch.randn(count, generator=g, device=dev, dtype=torch.float32)
+    hint = abi.make_hint(BETA)
+    cfg = zcomm.default_arb_config()
+    # shared Huffman context primed like prime_shared_huffman (bench.cpp:169-204): rank 0's first
+    # <= 1 Mi symbols under the run's scale, +1 smoothing
+    prime = zcomm.eb_quantize_with_scale(x[: 1 << 20], SCALE)
+    ctx = zcomm.HuffmanContext.from_bytes(prime)
+    fr = zcomm.alloc_frames(raw_bytes, dev)
+    out = torch.empty(count, dtype=torch.float32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    codecs = torch.zeros(fr.nbatches, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    s = C.c_void_p(stream.cuda_stream)
+    P = zcomm._ptr
+
+    def encode(pin):
+        zcomm.check(L.zc_encode_batches_f32(P(x), count, SCALE, P(fr.stages), zcomm.STAGE_STRIDE,
+                                            abi.STAGE_BANK_BYTES, pin, C.byref(hint), ctx.handle, C.byref(cfg),
+                                            P(fr.results), P(fr.index), P(err), s))
+
+    def decode(dst):
+        zcomm.check(L.zc_decode_batches_f32(P(fr.stages), zcomm.STAGE_STRIDE, abi.STAGE_BANK_BYTES,
+                                            P(fr.results), count, SCALE, ctx.handle, P(fr.index), P(dst),
+                                            P(codecs), s))
+
+    def run(pin, steps, warmup, with_clocks=False):
+        for _ in range(warmup):
+            encode(pin)
+            decode(out)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = Clocks(0)
+        if with_clocks:
+            clk.__enter__()
+            time.sleep(0.3)
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(steps):
+            ev[i][0].record(stream)
+            encode(pin)
+            ev[i][1].record(stream)
+            decode(out)
+            ev[i][2].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if with_clocks:
+            clk.__exit__()
+        total = start.elapsed_time(end) / steps
+        enc = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+        dec = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
+        res = fr.encode_results()
+        payload = sum(r.payload_bytes for r in res)
+        frames = [0, 0, 0]
+        for r in res:
+            frames[r.codec] += 1
+        e = int(err.item())
+        if e:
+            raise RuntimeError(f"device error word 0x{e:x}")
+        return {"ms": total, "enc_ms": enc, "dec_ms": dec, "payload": payload, "frames": frames,
+                "clocks": clk.summary() if with_clocks else None}
+
+    auto = run(abi.PIN_AUTO, args.steps, args.warmup, with_clocks=True)
+    # correctness guard on the measured output: the eb bound plus the one fp32 rounding of the output
+    y = out
+    maxerr = float((y.double() - x.double()).abs().max().item())
+    bound = ABS_EB * (1 + 1e-9) + float(x.abs().max().item()) * 2.0 ** -24
+    if not maxerr <= bound:
+        raise RuntimeError(f"round trip exceeds the error bound: {maxerr} > {bound}")
+    huff = run(abi.PIN_HUFFMAN, max(3, args.steps // 2), args.warmup)
+
+    # e2e: the public C-ABI path from pinned HOST buffers, copies inside the timed region
+    hx = torch.empty(count, dtype=torch.float32, pin_memory=True)
+    hx.copy_(x.cpu())
+    hy = torch.empty(count, dtype=torch.float32, pin_memory=True)
+    dx = torch.empty_like(x)
+    for _ in range(args.warmup):
+        dx.copy_(hx, non_blocking=True)
+        encode(abi.PIN_AUTO)
+        decode(out)
+        hy.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        dx.copy_(hx, non_blocking=True)
+        zcomm.check(L.zc_encode_batches_f32(P(dx), count, SCALE, P(fr.stages), zcomm.STAGE_STRIDE,
+                                            abi.STAGE_BANK_BYTES, abi.PIN_AUTO, C.byref(hint), ctx.handle,
+                                            C.byref(cfg), P(fr.results), P(fr.index), P(err), s))
+        decode(out)
+        hy.copy_(out, non_blocking=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = t0.elapsed_time(t1) / args.steps
+    if not torch.equal(hy, y.cpu()):
+        raise RuntimeError("e2e output differs from the device-resident run")
+
+    peak, peak_kind = peaks()
+    gbs = lambda ms: raw_bytes / (ms * 1e-3) / 1e9  # noqa: E731
+    P_auto, F = auto["payload"], fr.nbatches
+    enc_bytes = 4 * count + P_auto + 32 * F     # fp32 read + frames written
+    dec_bytes = P_auto + 32 * F + 4 * count     # frames read + fp32 written
+    dom = "encode" if auto["enc_ms"] >= auto["dec_ms"] else "decode"
+    dom_ms = max(auto["enc_ms"], auto["dec_ms"])
+    dom_bytes = enc_bytes if dom == "encode" else dec_bytes
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = load_traffic("zc_encode_f32" if dom == "encode" else "zc_decode")
+    line = {
+        "metric": "codec GB/s (quantize+histogram+select+encode+decode+dequantize round trip, raw symbol bytes)",
+        "value": round(gbs(auto["ms"]), 2),
+        "unit": "GB/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(auto["ms"], 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32->int32 (fp64 quantizer arithmetic)",
+        "data": "synthetic: torch.randn N(0,1) fp32, seed 1",
+        "config": {
+            "workload": "BASELINE config 0: single-rank codec round trip, 64 Mi Gaussian fp32, abs eb 1e-4",
+            "count": count, "raw_bytes": raw_bytes, "scale": SCALE, "pin": "auto (encode_best)",
+            "hint_beta_bytes_per_sec": BETA, "batches": F, "batch_bytes": abi.BATCH_RAW_BYTES,
+            "l2": "inputs (256 MiB fp32) exceed the 126 MB L2; no flush needed",
+        },
+        "compression_ratio": round(raw_bytes / P_auto, 4),
+        "frames_by_codec": {"raw": auto["frames"][0], "fixedlen": auto["frames"][1], "huffman": auto["frames"][2]},
+        "encode_ms": round(auto["enc_ms"], 4), "decode_ms": round(auto["dec_ms"], 4),
+        "encode_gbs": round(gbs(auto["enc_ms"]), 2), "decode_gbs": round(gbs(auto["dec_ms"]), 2),
+        "huffman_pinned": {
+            "value": round(gbs(huff["ms"]), 2), "unit": "GB/s", "ms_per_step": round(huff["ms"], 4),
+            "compression_ratio": round(raw_bytes / huff["payload"], 4),
+            "encode_gbs": round(gbs(huff["enc_ms"]), 2), "decode_gbs": round(gbs(huff["dec_ms"]), 2),
+            "frames_by_codec": {"raw": huff["frames"][0], "fixedlen": huff["frames"][1], "huffman": huff["frames"][2]},
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": dom_bytes,
+            "roundtrip_frac": round((enc_bytes + dec_bytes) / (auto["ms"] * 1e-3) / 1e9 / peak, 4),
+        },
+        "e2e": {"value": round(gbs(e2e_ms), 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": 4 * count, "d2h_bytes_per_step": 4 * count},
+        "gpu_launches": args.steps * 3,
+        "clocks": auto["clocks"],
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(x[: args.cpu_sample].cpu().numpy(), prime.cpu().numpy(), 0)
+    return line
+
+
+# ------------------------------------------------------------------------- CPU baseline / reference
+def cpu_baseline(xs, prime_syms, pin, threads=None, reps=1):
+    """The reference's codec round trip (oracle/_ref: encode_best / send_batch + decode dispatch +
+    dequantize per 4 MiB batch, bench-style) on a thread pool over the host cores."""
+    import numpy as np
+    import oracle
+    from paper_2605_12396_b200 import abi
+    ref = oracle.ref()
+    kind = "reference"
+    if ref is None:
+        raise RuntimeError("oracle/_ref is not built; the CPU baseline needs the compiled reference")
+    threads = threads or os.cpu_count()
+    x = np.ascontiguousarray(xs, np.float32)
+    ctx = ref.huff_from_bytes(np.ascontiguousarray(prime_syms).view(np.uint8))
+    cfg = abi.default_arb_config()
+    pay = C.c_uint64()
+    frames = np.zeros(3, np.uint64)
+    wall = C.c_double()
+    best = None
+    for _ in range(reps):
+        rc = ref.lib.zr_codec_roundtrip_mt(x, len(x), SCALE, pin, ctx, C.byref(cfg), abi.REGIME_INTER, BETA, threads,
+                                           None, C.byref(pay), frames, C.byref(wall))
+        if rc:
+            raise RuntimeError(ref.error())
+        best = wall.value if best is None else min(best, wall.value)
+    return {"value": round(4 * len(x) / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{len(x)} Gaussian fp32 elements ({len(x) * 4 >> 20} MiB, {int(frames.sum())} batches) "
+                      f"of the same workload, {'auto' if pin == 0 else 'pinned'} codec",
+            "compression_ratio": round(4 * len(x) / max(pay.value, 1), 4), "seconds": round(best, 3)}
+
+
+def reference_arm(args):
+    import numpy as np
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    n = args.cpu_sample
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(n).astype(np.float32)
+    prime = np.clip(np.round(x[: 1 << 20].astype(np.float64) / SCALE), -2**31, 2**31 - 1).astype(np.int32)
+    for _ in range(args.warmup):
+        cpu_baseline(x[: min(n, 4 << 20)], prime, 0)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(x, prime, 0))
+    t_all = time.perf_counter() - t_all
+    v = statistics.mean(r["value"] for r in vals)
+    cb = dict(vals[-1])
+    cb["value"] = round(v, 3)
+    return {
+        "metric": "codec GB/s (quantize+histogram+select+encode+decode+dequantize round trip, raw symbol bytes)",
+        "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_all / args.steps, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32->int32 (fp64 quantizer arithmetic)",
+        "data": "synthetic: numpy standard_normal fp32, seed 1", "impl": "reference",
+        "config": {"workload": "BASELINE config 0: single-rank codec round trip, Gaussian fp32, abs eb 1e-4",
+                   "count": n, "scale": SCALE, "pin": "auto (encode_best)", "hint_beta_bytes_per_sec": BETA},
+        "cpu_baseline": cb,
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ---------------------------------------------------------------------------------------- N > 1
+def allreduce_bench(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_12396_b200 import abi, zcomm
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev_index = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dist.init_process_group("gloo")
+    dev = torch.device("cuda", dev_index)
+    if world == 2:
+        count, workload, rel_mode = 64 << 20, "BASELINE config 1: ring AllReduce, 256 MB Laplacian per rank, abs eb 1e-4", "abs"
+        g = torch.Generator(device=dev)
+        g.manual_seed(100 + rank)
+        u = torch.rand(count, generator=g, device=dev, dtype=torch.float64) - 0.5
+        x = (-1e-2 * torch.sign(u) * torch.log1p(-2 * u.abs())).float()
+    else:
+        count, workload, rel_mode = 512 * 512 * 512, "BASELINE config 2: ring RS+AG, 512^3 smooth field per rank, rel eb 1e-3", "rel"
+        i = torch.arange(512, device=dev, dtype=torch.float32)
+        f = (torch.sin(2 * torch.pi * i / 512)[:, None, None] * torch.cos(4 * torch.pi * i / 512)[None, :, None]
+             + 0.5 * torch.sin(6 * torch.pi * (i + 7 * rank) / 512)[None, None, :])
+        x = f.reshape(-1).contiguous()
+        del f
+    if args.count:
+        count = args.count
+        x = x[:count].contiguous()
+    comm = zcomm.Communicator(rank, world, dev_index)
+    if rel_mode == "abs":
+        gmax = torch.tensor([x.abs().max().item()], dtype=torch.float64)
+        dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+        rel = ABS_EB / gmax.item()
+    else:
+        rel = 1e-3
+    out = torch.empty_like(x)
+    for _ in range(args.warmup):
+        comm.allreduce_eb(x, rel, out)
+    comm.wire_stats()
+    lib = zcomm.lib()
+    lib.zc_comm_reset_stats(comm._h)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    clk = Clocks(dev_index)
+    with clk:
+        for _ in range(args.steps):
+            comm.allreduce_eb(x, rel, out)
+        torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([dt], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = t.item()
+    w = comm.wire_stats()
+    line = None
+    if rank == 0:
+        S = 4 * count
+        cr = w.raw_bytes / max(w.payload_bytes, 1)
+        algbw = S / dt / 1e9
+        line = {
+            "metric": "compressed AllReduce algbw GB/s", "value": round(algbw, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32->int32", "data": "synthetic",
+            "config": {"workload": workload, "count_per_rank": count, "pin": "auto", "hint_beta_bytes_per_sec": BETA},
+            "compression_ratio": round(cr, 4), "busbw": round(algbw * 2 * (world - 1) / world, 2),
+            "aggregate_gbs": round(world * S / dt / 1e9, 2),
+            "frames_by_codec": list(w.frames_by_codec), "clocks": clk.summary(),
+            "e2e": None, "gpu_launches": None,
+        }
+    comm.close()
+    dist.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--count", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=16 << 20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        line = reference_arm(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        line = allreduce_bench(args)
+    else:
+        args.count = args.count or COUNT_C0
+        line = codec_bench(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
