@@ -62,6 +62,8 @@ struct Scratch {
   uint32_t* flags = nullptr;
   uint64_t nflags = 0;
   uint32_t* sink = nullptr;
+  void* task = nullptr;  // task-kernel unit states
+  size_t task_bytes = 0;
 };
 static std::mutex g_scratch_mu;
 static std::map<std::pair<int, void*>, Scratch> g_scratch;
@@ -96,6 +98,20 @@ int encode_common(EncParams& p, cudaStream_t s) {
   Scratch* sc = scratch_for(s, 1);
   if (!sc) return set_err(ZC_ERR_CUDA, "cannot allocate scratch (no CUDA device?)");
   if (p.err == nullptr) p.err = sc->sink;
+  // The batched send path (many frames, shared or no Huffman context) runs on the persistent
+  // task kernel; single frames, bare codecs, profiling and embedded codebooks on the cluster one.
+  if (p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook && std::getenv("ZC_NO_TASKS") == nullptr) {
+    const size_t need = task_scratch_bytes(p.nunits);
+    if (sc->task_bytes < need) {
+      cudaStreamSynchronize(s);
+      if (sc->task) cudaFree(sc->task);
+      sc->task = nullptr;
+      sc->task_bytes = 0;
+      if (int rc = cuda_err(cudaMalloc(&sc->task, need), "task scratch")) return rc;
+      sc->task_bytes = need;
+    }
+    return cuda_err(launch_encode_tasks(p, sc->task, s), "encode");
+  }
   return cuda_err(launch_encode(p, s), "encode");
 }
 

@@ -143,19 +143,23 @@ ZC_HD double u64_to_double(uint64_t v) {
 // so whenever q' is farther than that from a half-integer both round to the same integer and
 // the round-half-even magic-constant conversion equals llround.  Near a tie, or near the int32
 // limit, the exact IEEE division decides.  err |= ZC_DERR_* on non-finite input / range.
+//
+// The fast-path test is integer work on high words: |q| < 2^30 (so |q'-q| < 2^-21, and no int32
+// range issue) and |r| < 0.5 - 2^-19 (r = q' - RNE(q'), exact); 2^-19 > 2^-21 keeps the decision
+// safe, and only ~4e-6 of inputs take the division.
 __device__ __forceinline__ int32_t quantize_one(double x, double scale, double rcp, uint32_t& err) {
-  if (!isfinite(x)) {
+  if ((__double2hiint(x) & 0x7ff00000) == 0x7ff00000) {  // Inf / NaN
     err |= ZC_DERR_NONFINITE;
     return 0;
   }
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  double q = __dmul_rn(x, rcp);
-  double aq = fabs(q);
-  double t = __dadd_rn(q, kMagic);
-  double kd = __dsub_rn(t, kMagic);
-  double r = __dsub_rn(q, kd);  // exact, |r| <= 0.5
-  double tol = __dmul_rn(aq, 0x1.0p-48) + 0x1.0p-60;
-  if (aq < 2147483000.0 && fabs(fabs(r) - 0.5) > tol) {
+  const double q = __dmul_rn(x, rcp);
+  const double t = __dadd_rn(q, kMagic);
+  const double kd = __dsub_rn(t, kMagic);
+  const double r = __dsub_rn(q, kd);  // exact, |r| <= 0.5
+  const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
+  const uint32_t rhi = static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu;
+  if (qhi < 0x41D00000u && rhi < 0x3FDFFFF0u) {  // |q| < 2^30, |r| < 0.5 - 2^-19
     return static_cast<int32_t>(__double2loint(t));
   }
   double qe = __ddiv_rn(x, scale);
@@ -164,6 +168,19 @@ __device__ __forceinline__ int32_t quantize_one(double x, double scale, double r
     return 0;
   }
   return static_cast<int32_t>(llround(qe));
+}
+
+// Branch-free fast path of quantize_one for finite inputs: returns the symbol and sets `slow` when
+// this input must instead go through quantize_one (near a tie or |q| >= 2^30).
+__device__ __forceinline__ int32_t quantize_fast(double x, double rcp, bool& slow) {
+  const double kMagic = 6755399441055744.0;
+  const double q = __dmul_rn(x, rcp);
+  const double t = __dadd_rn(q, kMagic);
+  const double r = __dsub_rn(q, __dsub_rn(t, kMagic));
+  const uint32_t qhi = static_cast<uint32_t>(__double2hiint(q)) & 0x7fffffffu;
+  const uint32_t rhi = static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu;
+  slow |= !(qhi < 0x41D00000u && rhi < 0x3FDFFFF0u);
+  return static_cast<int32_t>(__double2loint(t));
 }
 
 // ------------------------------------------------------------------ selector (rea.cpp:22-176)

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
 
   __shared__ FrameCheck fc;
   __shared__ DevHuff s_t;
-  __shared__ uint32_t s_words[(DT / 32) * 136];
+  __shared__ uint32_t s_words[(DT / 32) * 136 * 4];
   __shared__ uint8_t s_lens[256];
   __shared__ uint32_t s_flag;
   uint32_t err = 0;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
   if (fc.codec == kFallback && p.bare) return;
   Sink sink{p.out_kind, p.out, p.scale};
   const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
-  uint32_t f = decode_slice<false>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
+  uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
   f = __reduce_or_sync(FULL, f);
   if (lane == 0 && f) atomicOr(&p.flags[u], f);
   err = __reduce_or_sync(FULL, err);

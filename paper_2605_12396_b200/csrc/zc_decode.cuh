@@ -51,6 +51,11 @@ __device__ __forceinline__ uint32_t stream_word(const uint8_t* s, uint64_t len, 
   return v;
 }
 
+// Exact int32 -> double without the conversion pipe: (2^52 + 2^31 + s) - (2^52 + 2^31).
+__device__ __forceinline__ double i2d(uint32_t s) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(s ^ 0x80000000u)), 4503601774854144.0);
+}
+
 // Output sink for decoded symbol vectors.
 struct Sink {
   int kind;      // OutKind
@@ -65,8 +70,7 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
       float* o = static_cast<float*>(k.out) + ob / 4;
       float f[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        f[i] = __double2float_rn(__dmul_rn(k.scale, static_cast<double>(static_cast<int32_t>(w[i]))));
+      for (int i = 0; i < 4; ++i) f[i] = __double2float_rn(__dmul_rn(k.scale, i2d(w[i])));
       if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
         *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
       } else {
@@ -80,7 +84,7 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
       double* o = static_cast<double*>(k.out) + ob / 4;
       double d[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = __dmul_rn(k.scale, static_cast<double>(static_cast<int32_t>(w[i])));
+      for (int i = 0; i < 4; ++i) d[i] = __dmul_rn(k.scale, i2d(w[i]));
       if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
         reinterpret_cast<double2*>(o)[0] = make_double2(d[0], d[1]);
         reinterpret_cast<double2*>(o)[1] = make_double2(d[2], d[3]);
@@ -262,8 +266,8 @@ __device__ __forceinline__ bool load_huff_tables(const FrameCheck& fc, const uin
 // are streaming; Huffman runs one thread per 1 KiB grain from the companion index (v0 must be a
 // multiple of 64).  Returns flag bits for the caller: 1 = index inconsistent with the payload,
 // 2 = undecodable Huffman stream.  words: >= 32 * nwarps * ... per-warp scratch of 136 words.
-template <bool kCoherent>
-__device__ uint32_t decode_slice(const FrameCheck& fc, const uint8_t* payload, uint64_t R, uint64_t v0, uint64_t v1,
+template <bool kCoherent, int kDecU>
+__device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* payload, uint64_t R, uint64_t v0, uint64_t v1,
                                  const Sink& sink, uint64_t obase, const uint32_t* idx, const DevHuff* ctx,
                                  DevHuff* s_t, uint32_t* s_flag, uint8_t* s_lens_tmp, uint32_t* s_words,
                                  uint32_t& err) {
@@ -299,26 +303,53 @@ __device__ uint32_t decode_slice(const FrameCheck& fc, const uint8_t* payload, u
       emit16(sink, obase + v * 16, w, nb, err);
     }
   } else if (codec == ZC_CODEC_FIXEDLEN) {
+    // A chunk of 128 symbols occupies exactly 4*width payload words.  Each warp stages U chunks'
+    // words in shared memory (every lane issues its <= 5 loads per chunk before any is used),
+    // then each lane extracts its 4 symbols per chunk with a 64-bit funnel read.
     const uint32_t width = static_cast<uint32_t>(fc.h.params);
     const uint32_t w4 = 4 * width;
     const uint64_t P = fc.h.payload_bytes;
     const unsigned long long mask = width == 32 ? 0xffffffffull : ((1ull << width) - 1);
-    uint32_t* sw = s_words + warp * 136;
-    for (uint64_t c = v0 / 32 + warp; c * 32 < v1; c += nthr / 32) {
-      for (uint32_t k = lane; k < w4 + 1; k += 32) sw[k] = stream_word<kCoherent>(payload, P, c * w4 + k);
-      __syncwarp();
-      const uint64_t v = c * 32 + lane;
-      if (v < v1) {
-        uint32_t w[4];
+    uint32_t* sw = s_words + warp * 136 * kDecU;
+    const uint64_t nwarps = nthr / 32;
+    for (uint64_t c0 = v0 / 32 + warp; c0 * 32 < v1; c0 += nwarps * kDecU) {
+      uint32_t t[kDecU][5];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t bit = (lane * 4 + k) * width;
-          const uint32_t wi = bit >> 5, sh = bit & 31;
-          unsigned long long x = (static_cast<unsigned long long>(sw[wi + 1]) << 32) | sw[wi];
-          w[k] = static_cast<uint32_t>(unzigzag32(static_cast<uint32_t>((x >> sh) & mask)));
+      for (int k = 0; k < kDecU; ++k) {
+        const uint64_t gw0 = (c0 + k * nwarps) * w4;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const uint32_t kk = lane + 32 * j;
+          const uint64_t g = gw0 + kk;
+          t[k][j] = 0;
+          if (kk <= w4 && (c0 + k * nwarps) * 32 < v1) {
+            if (g * 4 + 4 <= P) t[k][j] = ld32<kCoherent>(reinterpret_cast<const uint32_t*>(payload) + g);
+            else t[k][j] = stream_word<kCoherent>(payload, P, g);
+          }
         }
-        uint32_t nb = static_cast<uint32_t>(R - v * 16 < 16 ? R - v * 16 : 16);
-        emit16(sink, obase + v * 16, w, nb, err);
+      }
+#pragma unroll
+      for (int k = 0; k < kDecU; ++k)
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+          if (lane + 32 * j <= w4) sw[k * 136 + lane + 32 * j] = t[k][j];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kDecU; ++k) {
+        const uint64_t v = (c0 + k * nwarps) * 32 + lane;
+        if (v < v1) {
+          const uint32_t* s = sw + k * 136;
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t bit = (lane * 4 + q) * width;
+            const uint32_t wi = bit >> 5, sh = bit & 31;
+            unsigned long long x = (static_cast<unsigned long long>(s[wi + 1]) << 32) | s[wi];
+            w[q] = static_cast<uint32_t>(unzigzag32(static_cast<uint32_t>((x >> sh) & mask)));
+          }
+          uint32_t nb = static_cast<uint32_t>(R - v * 16 < 16 ? R - v * 16 : 16);
+          emit16(sink, obase + v * 16, w, nb, err);
+        }
       }
       __syncwarp();
     }

@@ -27,228 +27,13 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "zc_decode.cuh"
-#include "zc_kernels.h"
+#include "zc_encode_common.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace zc {
 namespace {
 
-constexpr int CL = 8;     // CTAs per cluster (= per frame unit)
-constexpr int NT = 512;   // threads per CTA
-constexpr int NW = NT / 32;
-constexpr unsigned FULL = 0xffffffffu;
-constexpr uint32_t CODEC_NONE = 0xFFu;
-constexpr int TILE_WORDS = NT * 16 + 64;  // Huffman tile: NT vectors x 16 bytes x <= 32 bits
-constexpr int ZZ_STRIDE = 132;            // FixedLen transpose buffer per warp (128 + pad)
-constexpr uint64_t SLICE_ALIGN = 64;      // CTA slices in 16-byte vectors: 1 KiB Huffman grains
-
-struct Bound {
-  unsigned long long head_idx, tail_idx;
-  uint32_t head_val, tail_val, has_head, has_tail;
-};
-
-struct Ctrl {
-  uint32_t maxzz, wmaxzz, zero_len, go;  // per-CTA partials; go: CTA 0's wait verdict
-  unsigned long long bits;
-  uint32_t codec, width, pending, _p;    // decision (CTA 0)
-  unsigned long long payload;
-  unsigned long long rx_len;
-  unsigned long long slice_base[CL];
-};
-
-union __align__(16) Scratch {
-  uint32_t tile[TILE_WORDS];
-  uint32_t zz[NW][ZZ_STRIDE];
-  struct {
-    unsigned long long keys[256];
-    unsigned long long w[512];
-    int parent[512];
-    uint8_t depth[512];
-  } tree;
-  struct {
-    DevHuff t;
-    uint32_t words[NW * 136];
-  } dec;
-};
-
-__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// ------------------------------------------------------------------ ring flag protocol
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint32_t ld_err(const uint32_t* p) {
-  return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-
-// Spins until *f >= v.  Gives up (false) when any rank has raised an error bit (the poison of
-// transport.cpp:90-95) or after the timeout, which it raises itself.
-__device__ bool wait_geq(const unsigned long long* f, unsigned long long v, const Link& L) {
-  const unsigned long long t0 = globaltimer();
-  for (uint32_t it = 0;; ++it) {
-    if (ld_acquire_sys(f) >= v) return true;
-    if (ld_err(L.err_self) != 0) return false;
-    if ((it & 255) == 255 && globaltimer() - t0 > L.timeout_ns) {
-      for (uint32_t r = 0; r < L.nranks; ++r) atomicOr(L.err_all[r], ZC_DERR_TIMEOUT);
-      return false;
-    }
-    __nanosleep(32);
-  }
-}
-
-__device__ __forceinline__ void broadcast_err(const Link& L, uint32_t err) {
-  for (uint32_t r = 0; r < L.nranks; ++r) atomicOr(L.err_all[r], err);
-}
-
-__device__ __forceinline__ void wire_add(zc_wire_stats* w, uint32_t codec, uint64_t raw, uint64_t payload,
-                                         uint64_t index_bytes) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(&w->frames_by_codec[codec]), 1ull);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&w->raw_bytes), static_cast<unsigned long long>(raw));
-  atomicAdd(reinterpret_cast<unsigned long long*>(&w->payload_bytes), static_cast<unsigned long long>(payload));
-  atomicAdd(reinterpret_cast<unsigned long long*>(&w->total_bytes), static_cast<unsigned long long>(payload + kHeaderBytes));
-  if (index_bytes) atomicAdd(reinterpret_cast<unsigned long long*>(&w->index_bytes), static_cast<unsigned long long>(index_bytes));
-}
-
-// Loads raw vector v (16 bytes) of the unit: bytes [16v, 16v+16) ∩ [0, R).  Float sources are
-// quantized here (4 elements -> 4 int32 symbols).  Missing bytes are zero; nb = valid bytes.
-// kCoh: the source was written earlier in this kernel (ring mode), so bypass the read-only path.
-template <int SRC, bool kCoh>
-__device__ __forceinline__ void load_vec(const EncParams& p, uint64_t uoff, uint64_t R, uint64_t v, uint32_t w[4],
-                                         uint32_t& nb, uint32_t& err) {
-  const uint64_t b0 = v * 16;
-  nb = static_cast<uint32_t>(R - b0 < 16 ? R - b0 : 16);
-  if (SRC == SRC_BYTES) {
-    const uint8_t* s = static_cast<const uint8_t*>(p.src) + uoff + b0;
-    if (nb == 16 && aligned16(s)) {
-      uint4 x = ld128<kCoh>(reinterpret_cast<const uint4*>(s));
-      w[0] = x.x;
-      w[1] = x.y;
-      w[2] = x.z;
-      w[3] = x.w;
-    } else {
-      w[0] = w[1] = w[2] = w[3] = 0;
-#pragma unroll
-      for (uint32_t j = 0; j < 16; ++j)
-        if (j < nb) w[j >> 2] |= static_cast<uint32_t>(ld8<kCoh>(s + j)) << (8 * (j & 3));
-    }
-  } else if (SRC == SRC_F32) {
-    const float* s = static_cast<const float*>(p.src) + (uoff + b0) / 4;
-    float f[4] = {0.f, 0.f, 0.f, 0.f};
-    if (nb == 16 && aligned16(s)) {
-      float4 x = __ldg(reinterpret_cast<const float4*>(s));
-      f[0] = x.x;
-      f[1] = x.y;
-      f[2] = x.z;
-      f[3] = x.w;
-    } else {
-#pragma unroll
-      for (uint32_t j = 0; j < 4; ++j)
-        if (j < nb / 4) f[j] = __ldg(s + j);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      w[k] = (static_cast<uint32_t>(k) < nb / 4)
-                 ? static_cast<uint32_t>(quantize_one(static_cast<double>(f[k]), p.scale, p.rcp, err))
-                 : 0u;
-  } else {
-    const double* s = static_cast<const double*>(p.src) + (uoff + b0) / 4;
-    double f[4] = {0.0, 0.0, 0.0, 0.0};
-    if (nb == 16 && aligned16(s)) {
-      double2 a = __ldg(reinterpret_cast<const double2*>(s));
-      double2 b = __ldg(reinterpret_cast<const double2*>(s) + 1);
-      f[0] = a.x;
-      f[1] = a.y;
-      f[2] = b.x;
-      f[3] = b.y;
-    } else {
-#pragma unroll
-      for (uint32_t j = 0; j < 4; ++j)
-        if (j < nb / 4) f[j] = __ldg(s + j);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      w[k] = (static_cast<uint32_t>(k) < nb / 4) ? static_cast<uint32_t>(quantize_one(f[k], p.scale, p.rcp, err)) : 0u;
-  }
-}
-
-__device__ __forceinline__ uint32_t byte_of(const uint32_t w[4], uint32_t j) {
-  return (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-}
-
-// Stores one 32-bit word of the payload at byte offset 4*gw, never past `limit` payload bytes.
-__device__ __forceinline__ void store_word_safe(uint8_t* payload, uint64_t gw, uint32_t val, uint64_t limit) {
-  uint64_t b = gw * 4;
-  if (b + 4 <= limit) {
-    reinterpret_cast<uint32_t*>(payload)[gw] = val;
-  } else {
-    for (uint32_t j = 0; j < 4 && b + j < limit; ++j) payload[b + j] = static_cast<uint8_t>(val >> (8 * j));
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ T block_reduce_max(T v, T* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  T r = red[0];
-  for (int i = 1; i < NW; ++i) r = max(r, red[i]);
-  return r;
-}
-
-__device__ __forceinline__ unsigned long long block_reduce_sum(unsigned long long v, unsigned long long* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  unsigned long long r = 0;
-  for (int i = 0; i < NW; ++i) r += red[i];
-  return r;
-}
-
-// Exclusive scan of a u32 across the CTA; *total receives the sum.
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  __syncthreads();
-  if (lane == 31) red[warp] = x;
-  __syncthreads();
-  uint32_t before = 0, tot = 0;
-  for (int i = 0; i < NW; ++i) {
-    uint32_t r = red[i];
-    if (i < warp) before += r;
-    tot += r;
-  }
-  *total = tot;
-  return before + x - v;
-}
-
-// Slice of the unit owned by cluster rank `crank`, in 16-byte vectors; multiples of 64 vectors
-// (1 KiB) so FixedLen chunks (128 symbols) and Huffman index grains never straddle CTAs.
-__device__ __forceinline__ void unit_slice(uint64_t R, uint32_t crank, uint64_t& v0, uint64_t& v1) {
-  const uint64_t nvec = (R + 15) / 16;
-  const uint64_t per = ((nvec + SLICE_ALIGN * CL - 1) / (SLICE_ALIGN * CL)) * SLICE_ALIGN;
-  v0 = min(nvec, per * crank);
-  v1 = min(nvec, per * (crank + 1));
-}
 
 template <int SRC, bool kRing>
 __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
@@ -267,12 +52,14 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
   __shared__ uint8_t s_slens[256];  // window self-code lengths (selfCodeLenBits)
   __shared__ zc_sample_stats s_st;
   __shared__ unsigned long long s_red[NW];
+  __shared__ double s_redd[NW];
   __shared__ uint32_t s_red32[NW];
   __shared__ Ctrl s_ctrl;
   __shared__ Bound s_bound[2];
   __shared__ FrameCheck s_fc;
   __shared__ uint32_t s_flag;
-  __shared__ Scratch s_x;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  Scratch& s_x = *reinterpret_cast<Scratch*>(s_dyn);
 
   const bool bare = p.mode == ENC_BARE_FL || p.mode == ENC_BARE_HF;
   const bool autolike = p.mode == ENC_BEST || (p.mode == ENC_SEND && p.pin == ZC_PIN_AUTO);
@@ -341,49 +128,117 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
     const bool p1_hbits = pin_huff && !embed;
 
     // ---------------- phase 1: one streaming pass
+    // Float sources: llround(x/scale) is monotone in x and zig-zag is V-shaped, so the unit's max
+    // zig-zag symbol is max(zz(q(min x)), zz(q(max x))): this pass only tracks min/max (plus the
+    // finiteness of every element) and quantizes just the 64 KiB profile window.  Every element is
+    // quantized exactly once, in phase 2.  Symbol sources track the zig-zag max directly.
+    constexpr bool kFloat = SRC != SRC_BYTES;
+    const bool need_syms = need_full_hist || p1_hbits;  // per-element symbols needed in this pass
     uint32_t mz = 0, wmz = 0, zero = 0;
+    Range rg;
     unsigned long long hb = 0;
+    // Vectors [v0, gend) take the general path (profile window, Huffman/embedded work, tails,
+    // unaligned sources); [gend, vfull) is the bulk: full vectors, min/max or zig-zag max only.
+    const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
+    const uint64_t vfull = min(v1, R / 16);
+    const bool bulk = fast_ok && !need_syms && need_maxzz;
+    const uint64_t wvec = need_profile ? (W + 15) / 16 : 0;
+    const uint64_t gend = bulk ? min(v1, max(v0, wvec)) : v1;
+    if (stage_ok && s_ctrl.go && bulk) {
+      constexpr int U = 8;
+      for (uint64_t base = gend + static_cast<uint64_t>(warp) * 32; base < vfull; base += NT * U) {
+        RawVec rv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const uint64_t v = base + static_cast<uint64_t>(k) * NT + lane;
+          if (v < vfull) fetch_full<SRC, kCoh>(p, uoff, v, rv[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const uint64_t v = base + static_cast<uint64_t>(k) * NT + lane;
+          if (v < vfull) {
+            if (kFloat) {
+              minmax_full<SRC>(rv[k], rg);
+            } else {
+              mz = max(mz, max(max(zigzag32(static_cast<int32_t>(rv[k].a.x)), zigzag32(static_cast<int32_t>(rv[k].a.y))),
+                               max(zigzag32(static_cast<int32_t>(rv[k].a.z)), zigzag32(static_cast<int32_t>(rv[k].a.w)))));
+            }
+          }
+        }
+      }
+      // the partial last vector of a unit, if any
+      if (vfull < v1 && vfull >= gend) {
+        const uint64_t v = vfull;
+        if (tid == 0) {
+          RawVec rv;
+          fetch<SRC, kCoh>(p, uoff, R, v, rv);
+          if (kFloat) {
+            minmax_vec<SRC>(rv, rg);
+          } else {
+            uint32_t w[4];
+            to_words<SRC>(p, rv, w, err);
+            for (uint32_t q = 0; q < (rv.nb >> 2); ++q) mz = max(mz, zigzag32(static_cast<int32_t>(w[q])));
+          }
+        }
+      }
+    }
     if (stage_ok && s_ctrl.go && (need_maxzz || need_profile || need_full_hist || p1_hbits)) {
-      for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 32; base < v1; base += NT) {
-        const uint64_t v = base + lane;
-        const bool act = v < v1;
-        uint32_t w[4] = {0, 0, 0, 0}, nb = 0;
-        if (act) load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
-        const uint32_t nwhole = nb >> 2;
-        if (need_maxzz) {
+      constexpr int U = 4;
+      for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 32; base < gend; base += NT * U) {
+        RawVec rv[U];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (static_cast<uint32_t>(k) < nwhole) mz = max(mz, zigzag32(static_cast<int32_t>(w[k])));
+        for (int k = 0; k < U; ++k) {
+          const uint64_t v = base + static_cast<uint64_t>(k) * NT + lane;
+          if (v < gend) fetch<SRC, kCoh>(p, uoff, R, v, rv[k]);
         }
-        if (need_profile && __any_sync(FULL, act && v * 16 < W)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (act && v * 16 + 4 * k + 4 <= W) wmz = max(wmz, zigzag32(static_cast<int32_t>(w[k])));
-          // warp-aggregated shared-memory histogram of the profile window
-#pragma unroll
-          for (uint32_t j = 0; j < 16; ++j) {
-            const bool in = act && j < nb && v * 16 + j < W;
-            const uint32_t key = in ? byte_of(w, j) : 256u + lane;
-            const uint32_t peers = __match_any_sync(FULL, key);
-            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[key], __popc(peers));
+        for (int k = 0; k < U; ++k) {
+          const uint64_t v = base + static_cast<uint64_t>(k) * NT + lane;
+          const bool act = v < gend;
+          const bool inwin = need_profile && act && v * 16 < W;
+          uint32_t w[4] = {0, 0, 0, 0}, nb = act ? rv[k].nb : 0;
+          if (kFloat && !need_syms) {
+            if (act) minmax_vec<SRC>(rv[k], rg);
+            if (inwin) to_words<SRC>(p, rv[k], w, err);
+          } else if (act) {
+            to_words<SRC>(p, rv[k], w, err);
           }
-        }
-        if (need_full_hist) {
+          const uint32_t nwhole = nb >> 2;
+          if (need_maxzz && (!kFloat || need_syms)) {
 #pragma unroll
-          for (uint32_t j = 0; j < 16; ++j) {
-            const bool in = act && j < nb;
-            const uint32_t key = in ? byte_of(w, j) : 256u + lane;
-            const uint32_t peers = __match_any_sync(FULL, key);
-            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_fhist[key], __popc(peers));
+            for (int q = 0; q < 4; ++q)
+              if (static_cast<uint32_t>(q) < nwhole) mz = max(mz, zigzag32(static_cast<int32_t>(w[q])));
           }
-        }
-        if (p1_hbits && act) {
+          if (need_profile && __any_sync(FULL, inwin)) {
 #pragma unroll
-          for (uint32_t j = 0; j < 16; ++j) {
-            if (j < nb) {
-              uint32_t l = static_cast<uint32_t>(s_enc[byte_of(w, j)] >> 32);
-              hb += l;
-              zero |= (l == 0);
+            for (int q = 0; q < 4; ++q)
+              if (inwin && v * 16 + 4 * q + 4 <= W) wmz = max(wmz, zigzag32(static_cast<int32_t>(w[q])));
+            // warp-aggregated shared-memory histogram of the profile window
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              const bool in = inwin && j < nb && v * 16 + j < W;
+              const uint32_t key = in ? byte_of(w, j) : 256u + lane;
+              const uint32_t peers = __match_any_sync(FULL, key);
+              if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[key], __popc(peers));
+            }
+          }
+          if (need_full_hist) {
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              const bool in = act && j < nb;
+              const uint32_t key = in ? byte_of(w, j) : 256u + lane;
+              const uint32_t peers = __match_any_sync(FULL, key);
+              if (in && lane == __ffs(peers) - 1) atomicAdd(&s_fhist[key], __popc(peers));
+            }
+          }
+          if (p1_hbits && act) {
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              if (j < nb) {
+                uint32_t l = static_cast<uint32_t>(s_enc[byte_of(w, j)] >> 32);
+                hb += l;
+                zero |= (l == 0);
+              }
             }
           }
         }
@@ -393,12 +248,22 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
       uint32_t r = block_reduce_max(mz, s_red32);
       uint32_t r2 = block_reduce_max(wmz, s_red32);
       uint32_t r3 = block_reduce_max(zero, s_red32);
+      if (SRC == SRC_F32) {
+        rg.bad = rg.absbits >= 0x7f800000u ? 1u : 0u;
+        rg.dmn = rg.fmn;  // exact widening of the two extremes
+        rg.dmx = rg.fmx;
+      }
+      uint32_t r5 = block_reduce_max(rg.bad, s_red32);
       unsigned long long r4 = block_reduce_sum(hb, s_red);
+      double mn = block_reduce_fmin(rg.dmn, s_redd), mx = block_reduce_fmax(rg.dmx, s_redd);
       if (tid == 0) {
         s_ctrl.maxzz = r;
         s_ctrl.wmaxzz = r2;
         s_ctrl.zero_len = r3;
         s_ctrl.bits = r4;
+        s_ctrl.bad = r5;
+        s_ctrl.fmin = mn;
+        s_ctrl.fmax = mx;
       }
     }
     cluster.sync();  // A: partials visible cluster-wide
@@ -420,13 +285,28 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
       uint32_t maxzz = 0, wmaxzz = 0, zl = 0;
       unsigned long long bits = 0;
       if (tid == 0) {
+        double gmn = __builtin_huge_val(), gmx = -__builtin_huge_val();
+        uint32_t gbad = 0;
         for (int r = 0; r < CL; ++r) {
           Ctrl* c = cluster.map_shared_rank(&s_ctrl, r);
           maxzz = max(maxzz, c->maxzz);
           wmaxzz = max(wmaxzz, c->wmaxzz);
           zl |= c->zero_len;
+          gbad |= c->bad;
+          gmn = fmin(gmn, c->fmin);
+          gmx = fmax(gmx, c->fmax);
           s_ctrl.slice_base[r] = bits;
           bits += c->bits;
+        }
+        s_ctrl.dirty = (kFloat && (!need_maxzz || need_syms || gbad)) ? 1u : 0u;
+        if (kFloat && !need_syms && need_maxzz && R >= 4) {
+          if (gbad) {
+            err |= ZC_DERR_NONFINITE;
+          } else {
+            const int32_t smax = quantize_one(gmx, p.scale, p.rcp, err);
+            const int32_t smin = quantize_one(gmn, p.scale, p.rcp, err);
+            maxzz = max(zigzag32(smax), zigzag32(smin));
+          }
         }
       }
       // sample statistics (rea.cpp:93-118)
@@ -618,34 +498,65 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
         }
       }
     } else if (codec == ZC_CODEC_FIXEDLEN) {
-      // warp-level bit packing: 128 symbols (32 vectors) -> 4*width words, LSB-first
-      uint32_t* zz = s_x.zz[warp];
-      const uint32_t w4 = 4 * width;
-      for (uint64_t c = v0 / 32 + warp; c * 32 < v1; c += NW) {
-        const uint64_t v = c * 32 + lane;
-        uint32_t w[4] = {0, 0, 0, 0}, nb = 0;
-        if (v < v1) load_vec<SRC, kCoh>(p, uoff, R, v, w, nb, err);
+      // Lane-centric bit packing.  A warp takes 1024 consecutive symbols: 8 coalesced 16-byte
+      // loads per lane (all in flight together), quantize + zig-zag, then a transpose through
+      // XOR-swizzled shared memory so that lane L holds symbols [32L, 32L+32).  32 symbols at width
+      // w are exactly w LSB-first words, so each lane packs its own words with compile-time shifts
+      // (pack_store<W>) and no merging across lanes.  Slices start on 64-vector boundaries, so
+      // every 1024-symbol chunk starts on a word boundary.
+      uint4* zz = s_x.zz[warp];
+      // full chunks of a finite unit at an aligned source take the branch-light path
+      const bool fast = aligned16(p.src) && (p.unit_bytes % 16) == 0 && !c0->dirty;
+      const uint64_t vfull = min(v1, R / 16);
+      for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 256; base < v1; base += static_cast<uint64_t>(NW) * 256) {
+        if (fast && base + 256 <= vfull) {
+          RawVec rv[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          zz[lane * 4 + k] = (static_cast<uint32_t>(k) < (nb >> 2)) ? zigzag32(static_cast<int32_t>(w[k])) : 0u;
-        if (lane == 0) zz[128] = 0;
-        __syncwarp();
-        for (uint32_t k = lane; k < w4; k += 32) {
-          const uint32_t bitpos = k * 32;
-          uint32_t i = bitpos / width;
-          const uint32_t o = bitpos - i * width;
-          unsigned long long acc = zz[i] >> o;
-          uint32_t filled = width - o;
-          ++i;
-          while (filled < 32 && i < 128) {
-            acc |= static_cast<unsigned long long>(zz[i]) << filled;
-            filled += width;
-            ++i;
+          for (int j = 0; j < 8; ++j) fetch_full<SRC, kCoh>(p, uoff, base + 32 * j + lane, rv[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t w[4];
+            words_full<SRC>(p, rv[j], w, err);
+            const uint32_t slot = 32 * j + lane;
+            zz[slot ^ ((slot >> 3) & 7)] =
+                make_uint4(zigzag32(static_cast<int32_t>(w[0])), zigzag32(static_cast<int32_t>(w[1])),
+                           zigzag32(static_cast<int32_t>(w[2])), zigzag32(static_cast<int32_t>(w[3])));
           }
-          const uint64_t gw = c * w4 + k;
-          if (gw * 4 < P) store_word_safe(payload, gw, static_cast<uint32_t>(acc), P);
+        } else {
+          RawVec rv[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint64_t v = base + 32 * j + lane;
+            rv[j].nb = 0;
+            if (v < v1) fetch<SRC, kCoh>(p, uoff, R, v, rv[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            if (rv[j].nb) to_words<SRC>(p, rv[j], w, err);
+            uint32_t z[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              z[q] = (static_cast<uint32_t>(q) < (rv[j].nb >> 2)) ? zigzag32(static_cast<int32_t>(w[q])) : 0u;
+            const uint32_t slot = 32 * j + lane;
+            zz[slot ^ ((slot >> 3) & 7)] = make_uint4(z[0], z[1], z[2], z[3]);
+          }
         }
         __syncwarp();
+        uint32_t z[32];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t slot = 8 * lane + m;
+          const uint4 q = zz[slot ^ ((slot >> 3) & 7)];
+          z[4 * m] = q.x;
+          z[4 * m + 1] = q.y;
+          z[4 * m + 2] = q.z;
+          z[4 * m + 3] = q.w;
+        }
+        __syncwarp();
+        // word offset of symbol 4*base + 32*lane is (4*base + 32*lane) * width / 32
+        const uint64_t wb = (base / 8 + lane) * width;
+        if ((base + 8 * lane) < v1) pack_store_w(width, z, payload, wb, P);
       }
     } else if (codec == ZC_CODEC_HUFFMAN) {
       const uint64_t cb = (embed || (bare && p.embed)) ? ZC_HUFF_CODEBOOK_BYTES : 0;
@@ -812,7 +723,7 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
         if (tid == 0) check_frame<true>(rx_stage, rlen, rR, nullptr, false, p.ctx, true, s_fc);
         __syncthreads();
         Sink sink{p.rx_store ? OUT_BYTES : OUT_ADD_I32, p.rx_dst, 1.0};
-        uint32_t f = decode_slice<true>(s_fc, rx_stage + kHeaderBytes, rR, r0, r1, sink, uoff,
+        uint32_t f = decode_slice<true, 2>(s_fc, rx_stage + kHeaderBytes, rR, r0, r1, sink, uoff,
                                         reinterpret_cast<const uint32_t*>(rx_stage + p.L.idx_off), p.ctx, &s_x.dec.t,
                                         &s_flag, s_lens, s_x.dec.words, err);
         if (s_fc.codec == kFallback || f) err |= ZC_DERR_CORRUPT;
@@ -835,9 +746,18 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
 }
 
 int g_max_clusters = -1;
+constexpr size_t kDynSmem = sizeof(Scratch);
+
+// Opts a kernel into > 48 KB of dynamic shared memory (once per instantiation).
+template <typename K>
+void set_smem(K kern) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDynSmem));
+  cudaGetLastError();
+}
 
 template <typename K>
 int query_max_clusters(K kern) {
+  set_smem(kern);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -846,6 +766,7 @@ int query_max_clusters(K kern) {
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(NT);
   cfg.gridDim = dim3(CL * 64);
+  cfg.dynamicSmemBytes = kDynSmem;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
@@ -865,6 +786,7 @@ cudaError_t launch_cluster(K kern, const P& p, uint32_t nunits, int cap, cudaStr
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = kDynSmem;
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -888,15 +810,7 @@ cudaError_t launch_t(const EncParams& p, cudaStream_t s) {
 // Forces module loading of every kernel here.  With lazy loading, the first launch of a kernel
 // can wait for the device to go idle — fatal when a peer-waiting ring kernel is running.
 void preload_encode_kernels() {
-  cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_BYTES, false>);
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_BYTES, true>);
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_F32, false>);
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_F32, true>);
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_F64, false>);
-  cudaFuncGetAttributes(&a, encode_kernel<SRC_F64, true>);
   encode_max_clusters();
-  cudaGetLastError();
 }
 
 // Persistent-grid size: the smaller of what fits co-resident and the L2 residency cap (in-flight
@@ -904,6 +818,12 @@ void preload_encode_kernels() {
 // overrides the cap for experiments.
 int encode_max_clusters() {
   if (g_max_clusters < 0) {
+    // every instantiation: opt into the dynamic shared memory and force its module load
+    set_smem(encode_kernel<SRC_BYTES, false>);
+    set_smem(encode_kernel<SRC_BYTES, true>);
+    set_smem(encode_kernel<SRC_F32, true>);
+    set_smem(encode_kernel<SRC_F64, false>);
+    set_smem(encode_kernel<SRC_F64, true>);
     int n = std::min(query_max_clusters(encode_kernel<SRC_F32, false>), query_max_clusters(encode_kernel<SRC_BYTES, true>));
     const char* env = std::getenv("ZC_ENCODE_CLUSTERS");
     int cap = env ? std::atoi(env) : 16;

@@ -104,6 +104,11 @@ struct DecParams {
 };
 
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
+// Batched send-mode encode (no ring, no embedded codebook) as a persistent task kernel;
+// `scratch` holds task_scratch_bytes(nunits) bytes of device memory (zeroed by the launcher).
+cudaError_t launch_encode_tasks(const EncParams& p, void* scratch, cudaStream_t s);
+size_t task_scratch_bytes(uint32_t nunits);
+void preload_task_kernels();
 int encode_max_clusters();
 // Force module loading of every kernel (lazy loading may otherwise stall a launch behind a
 // running peer-waiting kernel).
