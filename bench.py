@@ -156,6 +156,7 @@ def codec_bench(args):
             clk.__enter__()
             time.sleep(0.3)
         torch.cuda.synchronize()
+        n0 = zcomm.launch_count()
         start.record(stream)
         for i in range(steps):
             ev[i][0].record(stream)
@@ -164,6 +165,7 @@ def codec_bench(args):
             decode(out)
             ev[i][2].record(stream)
         end.record(stream)
+        launches = zcomm.launch_count() - n0
         torch.cuda.synchronize()
         if with_clocks:
             clk.__exit__()
@@ -179,7 +181,7 @@ def codec_bench(args):
         if e:
             raise RuntimeError(f"device error word 0x{e:x}")
         return {"ms": total, "enc_ms": enc, "dec_ms": dec, "payload": payload, "frames": frames,
-                "clocks": clk.summary() if with_clocks else None}
+                "clocks": clk.summary() if with_clocks else None, "launches": launches}
 
     auto = run(abi.PIN_AUTO, args.steps, args.warmup, with_clocks=True)
     # correctness guard on the measured output: the eb bound plus the one fp32 rounding of the output
@@ -263,7 +265,7 @@ def codec_bench(args):
         },
         "e2e": {"value": round(gbs(e2e_ms), 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": 4 * count, "d2h_bytes_per_step": 4 * count},
-        "gpu_launches": args.steps * 3,
+        "gpu_launches": auto["launches"],
         "clocks": auto["clocks"],
     }
     if not args.no_cpu_baseline:
@@ -335,16 +337,32 @@ def reference_arm(args):
 
 
 # ---------------------------------------------------------------------------------------- N > 1
-def allreduce_bench(args):
+def max_over_ranks(v: float) -> float:
+    """Max of a per-rank scalar over the job (torch.distributed must be initialised)."""
     import torch
     import torch.distributed as dist
-    from paper_2605_12396_b200 import abi, zcomm
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_bench(args):
+    """Compressed ring AllReduce (allreduce_eb: quantize -> fused compressed RS -> AG -> dequantize),
+    one process per GPU; device-timed with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_12396_b200 import zcomm
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    dev_index = local % torch.cuda.device_count()
+    ndev = torch.cuda.device_count()
+    dev_index = local % ndev
     torch.cuda.set_device(dev_index)
-    dist.init_process_group("gloo")
+    use_nccl = ndev >= world and os.environ.get("ZC_BENCH_GLOO") is None
+    dist.init_process_group("nccl" if use_nccl else "gloo",
+                            **({"device_id": torch.device("cuda", dev_index)} if use_nccl else {}))
     dev = torch.device("cuda", dev_index)
     if world == 2:
         count, workload, rel_mode = 64 << 20, "BASELINE config 1: ring AllReduce, 256 MB Laplacian per rank, abs eb 1e-4", "abs"
@@ -352,6 +370,7 @@ def allreduce_bench(args):
         g.manual_seed(100 + rank)
         u = torch.rand(count, generator=g, device=dev, dtype=torch.float64) - 0.5
         x = (-1e-2 * torch.sign(u) * torch.log1p(-2 * u.abs())).float()
+        del u
     else:
         count, workload, rel_mode = 512 * 512 * 512, "BASELINE config 2: ring RS+AG, 512^3 smooth field per rank, rel eb 1e-3", "rel"
         i = torch.arange(512, device=dev, dtype=torch.float32)
@@ -364,44 +383,88 @@ def allreduce_bench(args):
         x = x[:count].contiguous()
     comm = zcomm.Communicator(rank, world, dev_index)
     if rel_mode == "abs":
-        gmax = torch.tensor([x.abs().max().item()], dtype=torch.float64)
-        dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
-        rel = ABS_EB / gmax.item()
+        rel = ABS_EB / max_over_ranks(x.abs().max().item())
     else:
         rel = 1e-3
     out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         comm.allreduce_eb(x, rel, out)
-    comm.wire_stats()
-    lib = zcomm.lib()
-    lib.zc_comm_reset_stats(comm._h)
+    torch.cuda.synchronize()
+    zcomm.lib().zc_comm_reset_stats(comm._h)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    n0 = zcomm.launch_count()
     clk = Clocks(dev_index)
     with clk:
+        time.sleep(0.2)
+        t0.record(stream)
         for _ in range(args.steps):
             comm.allreduce_eb(x, rel, out)
+        t1.record(stream)
         torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / args.steps
-    t = torch.tensor([dt], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = t.item()
+    launches = zcomm.launch_count() - n0
+    dist.barrier()
+    dt = max_over_ranks(t0.elapsed_time(t1) / 1e3 / args.steps)
     w = comm.wire_stats()
+
+    # e2e through the public API: pinned host input -> device -> allreduce_eb -> pinned host output
+    hx = torch.empty(count, dtype=torch.float32, pin_memory=True)
+    hx.copy_(x.cpu())
+    hy = torch.empty(count, dtype=torch.float32, pin_memory=True)
+    dx = torch.empty_like(x)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        dx.copy_(hx, non_blocking=True)
+        comm.allreduce_eb(dx, rel, out)
+        hy.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dt_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+
+    # context: plain uncompressed NCCL AllReduce of the same fp32 buffer
+    nccl_algbw = None
+    if use_nccl:
+        y = x.clone()
+        for _ in range(3):
+            dist.all_reduce(y)
+        torch.cuda.synchronize()
+        dist.barrier()
+        n0e, n1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0e.record(stream)
+        for _ in range(args.steps):
+            dist.all_reduce(y)
+        n1e.record(stream)
+        torch.cuda.synchronize()
+        nccl_algbw = round(4 * count / max_over_ranks(n0e.elapsed_time(n1e) / 1e3 / args.steps) / 1e9, 2)
+        del y
+
     line = None
     if rank == 0:
         S = 4 * count
         cr = w.raw_bytes / max(w.payload_bytes, 1)
         algbw = S / dt / 1e9
+        per_gpu_sent = w.total_bytes / max(args.steps, 1)  # this rank's frames (wire stats are per rank)
         line = {
             "metric": "compressed AllReduce algbw GB/s", "value": round(algbw, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32->int32", "data": "synthetic",
-            "config": {"workload": workload, "count_per_rank": count, "pin": "auto", "hint_beta_bytes_per_sec": BETA},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32->int32 symbols (int32 sum)",
+            "data": "synthetic (generated on device)",
+            "config": {"workload": workload, "count_per_rank": count, "pin": "auto",
+                       "hint_beta_bytes_per_sec": BETA, "parallelism": f"ring{world}",
+                       "l2": "per-rank input exceeds L2"},
             "compression_ratio": round(cr, 4), "busbw": round(algbw * 2 * (world - 1) / world, 2),
-            "aggregate_gbs": round(world * S / dt / 1e9, 2),
-            "frames_by_codec": list(w.frames_by_codec), "clocks": clk.summary(),
-            "e2e": None, "gpu_launches": None,
+            "frames_by_codec": list(w.frames_by_codec),
+            "roofline": {"bound": "nvlink", "achieved": round(per_gpu_sent / dt / 1e9, 2), "peak": 900.0,
+                         "unit": "GB/s", "frac": round(per_gpu_sent / dt / 1e9 / 900.0, 4), "traffic": None},
+            "nccl_uncompressed_algbw": nccl_algbw,
+            "e2e": {"value": round(S / dt_e2e / 1e9, 2), "unit": "GB/s", "ms_per_step": round(dt_e2e * 1e3, 3),
+                    "h2d_bytes_per_step": S, "d2h_bytes_per_step": S},
+            "gpu_launches": launches, "clocks": clk.summary(),
         }
     comm.close()
     dist.destroy_process_group()

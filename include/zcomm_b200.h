@@ -175,6 +175,8 @@ typedef struct zc_comm zc_comm;         /* one rank of a Communicator (collectiv
 /* ---- library ---- */
 const char* zc_last_error(void);
 const char* zc_version(void);
+/* Kernels this library has launched in this process (all devices and streams). */
+uint64_t zc_launch_count(void);
 int zc_device_count(int* h_count);
 /* Reference defaults: ArbitrationConfig{} (rea.hpp:64-79), TransportHint{} (rea.hpp:33-36),
  * CollectiveConfig{} (collectives.hpp:24-34). */

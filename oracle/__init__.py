@@ -123,6 +123,38 @@ class Port:
                                C.byref(r))
         return r, stage[: r.total_bytes].copy()
 
+    def encode_best(self, raw, hint=None, ctx=None, cfg=None, cap=abi.STAGE_BANK_BYTES):
+        raw = np.ascontiguousarray(raw).view(np.uint8).ravel()
+        stage = np.zeros(max(cap, 1), np.uint8)
+        r = abi.EncodeResult()
+        self.lib.zo_encode_best(raw, len(raw), stage, cap, C.byref(hint or abi.make_hint()),
+                                C.byref(ctx) if ctx is not None else None, C.byref(cfg or abi.default_arb_config()),
+                                C.byref(r))
+        return r, stage[: r.total_bytes].copy()
+
+    def fixedlen_encode(self, sym, cap=None):
+        sym = np.ascontiguousarray(sym, np.int32)
+        out = np.zeros(cap if cap is not None else len(sym) * 4 + 8, np.uint8)
+        w = C.c_uint32()
+        p = self.lib.zo_fixedlen_encode(sym, len(sym), out, len(out), C.byref(w))
+        return out[:p].copy(), w.value
+
+    def huffman_encode(self, raw, ctx, embed=False, cap=None):
+        raw = np.ascontiguousarray(raw, np.uint8)
+        out = np.zeros(cap if cap is not None else len(raw) * 4 + 512, np.uint8)
+        p = self.lib.zo_huffman_encode(raw, len(raw), C.byref(ctx), out, len(out), 1 if embed else 0)
+        return out[:p].copy()
+
+    def ring_allgather(self, blocks, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None):
+        blocks = np.ascontiguousarray(blocks, np.int32)
+        n, block = blocks.shape
+        out = np.zeros((n, n * block), np.int32)  # every rank's gathered copy
+        w = abi.WireStats()
+        rc = self.lib.zo_ring_allgather(n, blocks.ravel(), block, pin, C.byref(hint or abi.make_hint()),
+                                        C.byref(ctx) if ctx is not None else None,
+                                        C.byref(cfg or abi.default_arb_config()), out.ravel(), C.byref(w))
+        return rc, out, w
+
     def encode_batches(self, raw, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None):
         """Frame every 4 MiB batch of a message exactly as send_encoded does (collectives.cpp:350-356)."""
         raw = np.ascontiguousarray(raw).view(np.uint8).ravel()

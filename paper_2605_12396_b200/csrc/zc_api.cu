@@ -3,6 +3,7 @@
 // Host C++ that validates arguments the way the reference does, prepares kernel parameters and
 // launches the sm_100a kernels.  Never computes on the CPU: every data-touching entry point
 // launches device work and returns ZC_ERR_CUDA when no device is usable.
+#include <atomic>
 #include <cctype>
 #include <cmath>
 #include <cstdlib>
@@ -26,6 +27,12 @@ struct zc_huff_ctx {
 namespace zc {
 
 thread_local std::string g_err;
+
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> n{0};
+  return n;
+}
+void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
 int set_err(int code, const std::string& msg) {
   g_err = msg;
@@ -144,6 +151,7 @@ extern "C" {
 
 const char* zc_last_error(void) { return g_err.c_str(); }
 const char* zc_version(void) { return "zcomm-b200 0.1 (sm_100a)"; }
+uint64_t zc_launch_count(void) { return zc::launch_counter().load(std::memory_order_relaxed); }
 
 int zc_device_count(int* n) {
   cudaError_t e = cudaGetDeviceCount(n);

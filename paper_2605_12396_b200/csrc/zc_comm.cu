@@ -360,6 +360,7 @@ int launch_mail(zc_comm* c, int op, const uint32_t rec[8], int from_absmax, doub
   a.rec_scale_from_scal = scale_from_scal;
   a.rel = rel;
   a.scal = c->scal();
+  note_launch();
   mailbox_kernel<<<1, 32, 0, c->stream>>>(a);
   return cuda_err(cudaGetLastError(), "mailbox");
 }
@@ -450,8 +451,10 @@ int enqueue_meta(zc_comm* c, uint64_t count, int mode, double scale, uint32_t le
 
 int enqueue_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int mode, double scale, uint32_t levels) {
   if (c->nranks == 1 || count == 0) return ZC_OK;
-  if (int rc = enqueue_meta(c, count, mode, scale, levels)) return rc;
+  if (int rc = enqueue_meta(c, count, mode, scale, levels)) return rc; {
+  note_launch();
   requant_kernel<<<sm_count(c->device) * 4, 256, 0, c->stream>>>(d_sym, count, c->scal());
+}
   if (int rc = cuda_err(cudaGetLastError(), "requant")) return rc;
   return enqueue_ring(c, d_sym, count, true);
 }
@@ -475,9 +478,11 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
     count_ctrl_frames(c, 8);
     if (int rc = launch_mail(c, MAIL_EB_SCALE, nullptr, 1, rel)) return rc;
   } else {
+    note_launch();
     set_scale_kernel<<<1, 1, 0, c->stream>>>(s, rel, 1);
   }
   const int g = sm_count(c->device) * 4;
+  note_launch();
   quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
   if (c->nranks > 1 && count > 0) {
     // allreduce(q) with the shared scale: the meta ring still runs (and checks the counts)
@@ -489,6 +494,7 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
     if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
     if (int rc = enqueue_ring(c, c->sym, count, true)) return rc;
   }
+  note_launch();
   dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym, count, s, d_out, out_f64);
   return cuda_err(cudaGetLastError(), "dequantize");
 }

@@ -159,10 +159,13 @@ cudaError_t launch_decode(const DecParams& p, cudaStream_t s) {
   const uint64_t nvec = (maxR + 15) / 16;
   const uint32_t slices = static_cast<uint32_t>((nvec + SLICE_VEC - 1) / SLICE_VEC);
   dim3 grid(slices > 0 ? slices : 1, p.nunits);
+  note_launch();
   decode_kernel<<<grid, DT, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return e; {
+  note_launch();
   fixup_kernel<<<p.nunits, DT, 0, s>>>(p);
+}
   return cudaGetLastError();
 }
 

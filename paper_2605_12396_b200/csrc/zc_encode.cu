@@ -793,6 +793,7 @@ cudaError_t launch_cluster(K kern, const P& p, uint32_t nunits, int cap, cudaStr
   const int mc = encode_max_clusters();
   int ncl = std::min<int>(static_cast<int>(nunits), cap > 0 ? std::min(cap, mc) : mc);
   cfg.gridDim = dim3(CL * std::max(1, ncl));
+  note_launch();
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 

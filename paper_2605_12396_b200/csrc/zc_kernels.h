@@ -103,6 +103,10 @@ struct DecParams {
   int32_t* ok_out;         // bare decode result
 };
 
+// Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
+// can state how many of OUR kernels a region launched.
+void note_launch();
+
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
 // Batched send-mode encode (no ring, no embedded codebook) as a persistent task kernel;
 // `scratch` holds task_scratch_bytes(nunits) bytes of device memory (zeroed by the launcher).

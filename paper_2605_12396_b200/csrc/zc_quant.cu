@@ -181,10 +181,13 @@ cudaError_t launch_absmax(const void* x, int src_kind, uint64_t n, double* out, 
   cudaMemsetAsync(out, 0, sizeof(double), s);
   if (n == 0) return cudaGetLastError();
   unsigned long long* o = reinterpret_cast<unsigned long long*>(out);
-  if (src_kind == SRC_F64)
+  if (src_kind == SRC_F64) {
+    note_launch();
     absmax_kernel<double><<<grid_for(n / 2), QT, 0, s>>>(static_cast<const double*>(x), n, o, err);
-  else
+  } else {
+    note_launch();
     absmax_kernel<float><<<grid_for(n / 4), QT, 0, s>>>(static_cast<const float*>(x), n, o, err);
+  }
   return cudaGetLastError();
 }
 
@@ -192,30 +195,38 @@ cudaError_t launch_quantize(const void* x, int src_kind, uint64_t n, double scal
                             cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const double rcp = 1.0 / scale;
-  if (src_kind == SRC_F64)
+  if (src_kind == SRC_F64) {
+    note_launch();
     quantize_kernel<double><<<grid_for(n / 4), QT, 0, s>>>(static_cast<const double*>(x), n, scale, rcp, sym, err);
-  else
+  } else {
+    note_launch();
     quantize_kernel<float><<<grid_for(n / 4), QT, 0, s>>>(static_cast<const float*>(x), n, scale, rcp, sym, err);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_dequantize(const int32_t* sym, uint64_t n, double k, int prequant, void* out, int out_f64,
                               cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
+  if (n == 0) return cudaSuccess; {
+  note_launch();
   dequantize_kernel<<<grid_for(n / 4), QT, 0, s>>>(sym, n, prequant ? 1.0 : k, out, out_f64);
+}
   return cudaGetLastError();
 }
 
 cudaError_t launch_commit_raw(const uint8_t* raw, uint64_t n, uint8_t* region, uint64_t cap, uint64_t* total,
                               cudaStream_t s) {
+  note_launch();
   commit_raw_kernel<<<grid_for(n / 16 + 1), QT, 0, s>>>(raw, n, region, cap, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_hist(const uint8_t* d, uint64_t n, uint64_t* hist, cudaStream_t s) {
   cudaMemsetAsync(hist, 0, 256 * sizeof(uint64_t), s);
-  if (n == 0) return cudaGetLastError();
+  if (n == 0) return cudaGetLastError(); {
+  note_launch();
   hist_kernel<<<grid_for(n / 4), QT, 0, s>>>(d, n, reinterpret_cast<unsigned long long*>(hist));
+}
   return cudaGetLastError();
 }
 

@@ -693,6 +693,7 @@ cudaError_t launch_tasks_t(const EncParams& p, void* scratch, cudaStream_t s) {
   TaskHdr* th = static_cast<TaskHdr*>(scratch);
   UnitState* us = reinterpret_cast<UnitState*>(static_cast<uint8_t*>(scratch) + 256);
   const uint32_t ctas = std::min<uint64_t>(static_cast<uint64_t>(sms), static_cast<uint64_t>(p.nunits) * S);
+  note_launch();
   task_kernel<SRC><<<ctas, NT, sizeof(Scratch), s>>>(p, us, th);
   return cudaGetLastError();
 }

@@ -68,6 +68,7 @@ def lib():
     u64, i32, u32, dbl = C.c_uint64, C.c_int32, C.c_uint32, C.c_double
     _sig(L, "zc_last_error", C.c_char_p)
     _sig(L, "zc_version", C.c_char_p)
+    _sig(L, "zc_launch_count", C.c_uint64)
     _sig(L, "zc_device_count", C.c_int, P(C.c_int))
     _sig(L, "zc_default_arb_config", None, P(abi.ArbConfig))
     _sig(L, "zc_default_transport_hint", None, P(abi.TransportHint))
@@ -136,6 +137,11 @@ def lib():
     _sig(L, "zc_group_allreduce_max", C.c_int, P(vp), C.c_int, P(dbl), P(dbl))
     _lib = L
     return L
+
+
+def launch_count() -> int:
+    """Kernels this library has launched so far in this process."""
+    return int(lib().zc_launch_count())
 
 
 def check(rc: int) -> None:
@@ -637,13 +643,15 @@ class Communicator:
                  exchange=None):
         self.rank, self.nranks, self.device = rank, nranks, device
         self.cfg = cfg or collective_config()
+        exchange = exchange or _dist_allgather_bytes
+        check_consistent_config(self.cfg, rank, exchange)
         h = vp()
         check(lib().zc_comm_create(rank, nranks, device, C.byref(self.cfg), C.byref(h)))
         self._h = h
         n = lib().zc_comm_export_size()
         blob = (C.c_uint8 * n)()
         check(lib().zc_comm_export(h, C.cast(blob, vp)))
-        blobs = (exchange or _dist_allgather_bytes)(bytes(blob))
+        blobs = exchange(bytes(blob))
         allb = (C.c_uint8 * (n * nranks)).from_buffer_copy(b"".join(blobs))
         check(lib().zc_comm_connect(h, C.cast(allb, vp)))
 
@@ -682,6 +690,21 @@ class Communicator:
         if getattr(self, "_h", None) is not None and _lib is not None:
             _lib.zc_comm_destroy(self._h)
             self._h = None
+
+
+def check_consistent_config(cfg: abi.CollectiveConfig, rank: int, exchange) -> None:
+    """Every rank must run the same CollectiveConfig.  Frames are self-describing, so a hint or
+    cost-model mismatch would still decode, but ranks would pick different codecs than the
+    reference's single config does; a pin or fused_codec_min_msg_bytes mismatch would make ranks
+    run different step schedules over the same banks (a hang until the timeout).  The reference
+    gets this for free (one Communicator object, collectives.cpp:137-152); across processes it is
+    checked once at rendezvous, like the stream-meta check (collectives.cpp:428-452), and raises
+    ValueError (std::invalid_argument) on every rank."""
+    mine = bytes(cfg)
+    allc = exchange(mine)
+    bad = [r for r, b in enumerate(allc) if bytes(b) != mine]
+    if bad:
+        raise ValueError(f"rank {rank}: CollectiveConfig differs on rank(s) {bad}")
 
 
 def _dist_allgather_bytes(b: bytes):
