@@ -108,7 +108,11 @@ int encode_common(EncParams& p, cudaStream_t s) {
   // The batched send path (many frames, shared or no Huffman context) runs on the persistent
   // task kernel; single frames, bare codecs, profiling and embedded codebooks on the cluster one.
   if (p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook && std::getenv("ZC_NO_TASKS") == nullptr) {
-    const size_t need = task_scratch_bytes(p.nunits);
+    const char* which = std::getenv("ZC_ENCODER");  // developer switch: batch (default) | stream | tasks
+    const int kind = which == nullptr ? 0 : (std::strcmp(which, "stream") == 0 ? 1 : std::strcmp(which, "tasks") == 0 ? 2 : 0);
+    const bool stream = kind == 1 && stream_encoder_ok(p);
+    const size_t need = kind == 0 ? batch_scratch_bytes(p.nunits)
+                                  : (stream ? stream_scratch_bytes(p.nunits) : task_scratch_bytes(p.nunits));
     if (sc->task_bytes < need) {
       cudaStreamSynchronize(s);
       if (sc->task) cudaFree(sc->task);
@@ -117,7 +121,8 @@ int encode_common(EncParams& p, cudaStream_t s) {
       if (int rc = cuda_err(cudaMalloc(&sc->task, need), "task scratch")) return rc;
       sc->task_bytes = need;
     }
-    return cuda_err(launch_encode_tasks(p, sc->task, s), "encode");
+    if (kind == 0) return cuda_err(launch_encode_batch(p, sc->task, s), "encode");
+    return cuda_err(stream ? launch_encode_stream(p, sc->task, s) : launch_encode_tasks(p, sc->task, s), "encode");
   }
   return cuda_err(launch_encode(p, s), "encode");
 }

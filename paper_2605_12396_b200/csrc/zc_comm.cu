@@ -221,12 +221,12 @@ __global__ void quantize_dev_kernel(const float* __restrict__ x, uint64_t n, con
   uint32_t e = 0;
   const uint64_t nv = n / 4, stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv; v += stride) {
-    float4 f = __ldg(reinterpret_cast<const float4*>(x) + v);
+    const uint4 f = __ldg(reinterpret_cast<const uint4*>(x) + v);
     int4 o;
-    o.x = quantize_one(f.x, scale, rcp, e);
-    o.y = quantize_one(f.y, scale, rcp, e);
-    o.z = quantize_one(f.z, scale, rcp, e);
-    o.w = quantize_one(f.w, scale, rcp, e);
+    o.x = quantize_f32bits(f.x, scale, rcp, e);
+    o.y = quantize_f32bits(f.y, scale, rcp, e);
+    o.z = quantize_f32bits(f.z, scale, rcp, e);
+    o.w = quantize_f32bits(f.w, scale, rcp, e);
     reinterpret_cast<int4*>(sym)[v] = o;
   }
   for (uint64_t i = nv * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
@@ -238,10 +238,23 @@ __global__ void quantize_dev_kernel(const float* __restrict__ x, uint64_t n, con
 __global__ void dequantize_dev_kernel(const int32_t* __restrict__ sym, uint64_t n, const Scal* s, void* out, int f64) {
   const double k = s->scale;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-    double d = __dmul_rn(k, static_cast<double>(sym[i]));
+  const bool al = ((reinterpret_cast<uintptr_t>(sym) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const uint64_t nv = al ? n / 4 : 0;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nv; v += stride) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(sym) + v);
+    const double d0 = __dmul_rn(k, i2d_magic(q.x)), d1 = __dmul_rn(k, i2d_magic(q.y));
+    const double d2 = __dmul_rn(k, i2d_magic(q.z)), d3 = __dmul_rn(k, i2d_magic(q.w));
+    if (f64) {
+      reinterpret_cast<double2*>(out)[2 * v] = make_double2(d0, d1);
+      reinterpret_cast<double2*>(out)[2 * v + 1] = make_double2(d2, d3);
+    } else {
+      reinterpret_cast<float4*>(out)[v] = make_float4(d2f_rn(d0), d2f_rn(d1), d2f_rn(d2), d2f_rn(d3));
+    }
+  }
+  for (uint64_t i = nv * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const double d = __dmul_rn(k, i2d_magic(static_cast<uint32_t>(sym[i])));
     if (f64) static_cast<double*>(out)[i] = d;
-    else static_cast<float*>(out)[i] = __double2float_rn(d);
+    else static_cast<float*>(out)[i] = d2f_rn(d);
   }
 }
 
@@ -541,6 +554,8 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     preload_decode_kernels();
     preload_quant_kernels();
     preload_task_kernels();
+    preload_stream_kernels();
+    preload_batch_kernels();
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, mailbox_kernel);
     cudaFuncGetAttributes(&fa, requant_kernel);

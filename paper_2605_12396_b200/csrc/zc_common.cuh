@@ -170,6 +170,36 @@ __device__ __forceinline__ int32_t quantize_one(double x, double scale, double r
   return static_cast<int32_t>(llround(qe));
 }
 
+// fp32 -> fp64 and fp64 -> fp32 (round to nearest even) with integer ops: the F2F conversion
+// instructions issue at a fraction of the ALU rate on sm_100 and dominated the codec loops.
+// Normal numbers and zeros take the integer path; the rest sets `slow` / falls back.
+__device__ __forceinline__ double f2d_bits(uint32_t u, bool& slow) {
+  const uint32_t ex = (u >> 23) & 0xffu;
+  uint32_t hi, lo;
+  if (ex - 1u < 254u) {
+    hi = (u & 0x80000000u) | ((ex + 896u) << 20) | ((u >> 3) & 0xfffffu);
+    lo = u << 29;
+  } else {
+    hi = u & 0x80000000u;
+    lo = 0;
+    slow |= (u & 0x7fffffffu) != 0;  // denormal, Inf, NaN
+  }
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+}
+
+__device__ __forceinline__ float d2f_rn(double d) {
+  const uint32_t hi = static_cast<uint32_t>(__double2hiint(d)), lo = static_cast<uint32_t>(__double2loint(d));
+  const uint32_t ex = (hi >> 20) & 0x7ffu;
+  if (ex - 897u < 254u) {
+    uint32_t f = (hi & 0x80000000u) | ((ex - 896u) << 23) | ((hi & 0xfffffu) << 3) | (lo >> 29);
+    const uint32_t rb = lo & 0x1fffffffu;
+    f += (rb > 0x10000000u || (rb == 0x10000000u && (f & 1u))) ? 1u : 0u;
+    return __uint_as_float(f);
+  }
+  if ((hi & 0x7fffffffu) == 0 && lo == 0) return __uint_as_float(hi & 0x80000000u);
+  return __double2float_rn(d);
+}
+
 // Branch-free fast path of quantize_one for finite inputs: returns the symbol and sets `slow` when
 // this input must instead go through quantize_one (near a tie or |q| >= 2^30).
 __device__ __forceinline__ int32_t quantize_fast(double x, double rcp, bool& slow) {
@@ -181,6 +211,20 @@ __device__ __forceinline__ int32_t quantize_fast(double x, double rcp, bool& slo
   const uint32_t rhi = static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu;
   slow |= !(qhi < 0x41D00000u && rhi < 0x3FDFFFF0u);
   return static_cast<int32_t>(__double2loint(t));
+}
+
+// quantize_one for an fp32 input given as bits: integer widening + branch-free fast path, exact
+// fallback only near a tie or for non-normal inputs.
+__device__ __forceinline__ int32_t quantize_f32bits(uint32_t u, double scale, double rcp, uint32_t& err) {
+  bool slow = false;
+  const int32_t r = quantize_fast(f2d_bits(u, slow), rcp, slow);
+  if (!slow) return r;
+  return quantize_one(static_cast<double>(__uint_as_float(u)), scale, rcp, err);
+}
+
+// int32 -> double exactly, without the I2F conversion pipe (magic-number subtraction).
+__device__ __forceinline__ double i2d_magic(uint32_t s) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(s ^ 0x80000000u)), 4503601774854144.0);
 }
 
 // ------------------------------------------------------------------ selector (rea.cpp:22-176)

@@ -70,7 +70,7 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
       float* o = static_cast<float*>(k.out) + ob / 4;
       float f[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) f[i] = __double2float_rn(__dmul_rn(k.scale, i2d(w[i])));
+      for (int i = 0; i < 4; ++i) f[i] = d2f_rn(__dmul_rn(k.scale, i2d(w[i])));
       if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
         *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
       } else {

@@ -241,18 +241,40 @@ __device__ __forceinline__ void to_words(const EncParams& p, const RawVec& rv, u
   }
 }
 
+// L2 eviction-priority hints for a read that will be re-read soon (kPolKeep: the scan pass of the
+// task kernel) and for its last read (kPolDrop: the encode pass), so the slices in flight between
+// the two passes stay resident in L2 instead of competing with the stream.
+enum : int { kPolNone = 0, kPolKeep = 1, kPolDrop = 2 };
+template <int kPol>
+__device__ __forceinline__ uint4 ld128_pol(const uint4* p) {
+  if (kPol == kPolNone) return __ldg(p);
+  uint64_t pol;
+  if (kPol == kPolKeep)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 // Full 16-byte vector at an aligned source (no tail / alignment checks).
-template <int SRC, bool kCoh>
+template <int SRC, bool kCoh, int kPol = kPolNone>
 __device__ __forceinline__ void fetch_full(const EncParams& p, uint64_t uoff, uint64_t v, RawVec& rv) {
   rv.nb = 16;
   if (SRC == SRC_BYTES) {
-    rv.a = ld128<kCoh>(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.src) + uoff) + v);
+    if (kCoh)
+      rv.a = ld128<kCoh>(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.src) + uoff) + v);
+    else
+      rv.a = ld128_pol<kPol>(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.src) + uoff) + v);
   } else if (SRC == SRC_F32) {
-    rv.a = __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(p.src) + uoff / 4) + v);
+    rv.a = ld128_pol<kPol>(reinterpret_cast<const uint4*>(static_cast<const float*>(p.src) + uoff / 4) + v);
   } else {
     const uint4* s = reinterpret_cast<const uint4*>(static_cast<const double*>(p.src) + uoff / 4) + 2 * v;
-    rv.a = __ldg(s);
-    rv.b = __ldg(s + 1);
+    rv.a = ld128_pol<kPol>(s);
+    rv.b = ld128_pol<kPol>(s + 1);
   }
 }
 

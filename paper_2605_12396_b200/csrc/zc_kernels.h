@@ -112,6 +112,16 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
 // `scratch` holds task_scratch_bytes(nunits) bytes of device memory (zeroed by the launcher).
 cudaError_t launch_encode_tasks(const EncParams& p, void* scratch, cudaStream_t s);
 size_t task_scratch_bytes(uint32_t nunits);
+// The default batched send path: profile -> scan -> emit streaming kernels (zc_batch.cu).
+cudaError_t launch_encode_batch(const EncParams& p, void* scratch, cudaStream_t s);
+size_t batch_scratch_bytes(uint32_t nunits);
+void preload_batch_kernels();
+// The same path with 64 KiB slices staged in shared memory by bulk copies (input read once);
+// used when the source is fp32 or symbol bytes, 16-byte aligned, with 64 KiB-multiple units.
+bool stream_encoder_ok(const EncParams& p);
+cudaError_t launch_encode_stream(const EncParams& p, void* scratch, cudaStream_t s);
+size_t stream_scratch_bytes(uint32_t nunits);
+void preload_stream_kernels();
 void preload_task_kernels();
 int encode_max_clusters();
 // Force module loading of every kernel (lazy loading may otherwise stall a launch behind a

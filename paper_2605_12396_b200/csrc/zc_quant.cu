@@ -75,11 +75,14 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const T* __restrict__ x, u
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(QT) + threadIdx.x; v < nvec; v += stride) {
     double a[4];
     if (sizeof(T) == 4) {
-      float4 f = __ldg(reinterpret_cast<const float4*>(x) + v);
-      a[0] = f.x;
-      a[1] = f.y;
-      a[2] = f.z;
-      a[3] = f.w;
+      const uint4 f = __ldg(reinterpret_cast<const uint4*>(x) + v);
+      int4 o;
+      o.x = quantize_f32bits(f.x, scale, rcp, e);
+      o.y = quantize_f32bits(f.y, scale, rcp, e);
+      o.z = quantize_f32bits(f.z, scale, rcp, e);
+      o.w = quantize_f32bits(f.w, scale, rcp, e);
+      reinterpret_cast<int4*>(sym)[v] = o;
+      continue;
     } else {
       double2 d0 = __ldg(reinterpret_cast<const double2*>(x) + 2 * v);
       double2 d1 = __ldg(reinterpret_cast<const double2*>(x) + 2 * v + 1);
@@ -107,15 +110,15 @@ __global__ void __launch_bounds__(QT) dequantize_kernel(const int32_t* __restric
   const uint64_t nvec = al ? n / 4 : 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * QT;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(QT) + threadIdx.x; v < nvec; v += stride) {
-    int4 s = __ldg(reinterpret_cast<const int4*>(sym) + v);
-    double d0 = __dmul_rn(k, static_cast<double>(s.x)), d1 = __dmul_rn(k, static_cast<double>(s.y));
-    double d2 = __dmul_rn(k, static_cast<double>(s.z)), d3 = __dmul_rn(k, static_cast<double>(s.w));
+    uint4 s = __ldg(reinterpret_cast<const uint4*>(sym) + v);
+    double d0 = __dmul_rn(k, i2d_magic(s.x)), d1 = __dmul_rn(k, i2d_magic(s.y));
+    double d2 = __dmul_rn(k, i2d_magic(s.z)), d3 = __dmul_rn(k, i2d_magic(s.w));
     if (out_f64) {
       reinterpret_cast<double2*>(out)[2 * v] = make_double2(d0, d1);
       reinterpret_cast<double2*>(out)[2 * v + 1] = make_double2(d2, d3);
     } else {
       reinterpret_cast<float4*>(out)[v] =
-          make_float4(__double2float_rn(d0), __double2float_rn(d1), __double2float_rn(d2), __double2float_rn(d3));
+          make_float4(d2f_rn(d0), d2f_rn(d1), d2f_rn(d2), d2f_rn(d3));
     }
   }
   for (uint64_t i = nvec * 4 + blockIdx.x * static_cast<uint64_t>(QT) + threadIdx.x; i < n; i += stride) {
