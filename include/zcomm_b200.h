@@ -303,6 +303,18 @@ int zc_decode_batches_f32(const uint8_t* d_stages, uint64_t stage_stride, uint64
 int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stage_stride, uint64_t stage_len,
                               const zc_encode_result* d_sent, uint64_t raw_bytes, const zc_huff_ctx* ctx,
                               const uint32_t* d_index, int32_t* d_acc, uint32_t* d_err, void* stream);
+/* Host-buffer codec round trip: the reference's per-batch send_encoded -> recv_decoded over a message
+ * (collectives.cpp:201-348 with quantize / dequantize, quant.cpp:43-62 and 107-127), the call that
+ * RankCtx::send_encoded + recv_decoded make on host spans.  h_x (host fp32; pinned for overlap) -> H2D ->
+ * fused quantize+encode (frames land in d_stages / d_results / d_index exactly as zc_encode_batches_f32
+ * writes them) -> decode+dequantize -> D2H -> h_y.  Pipelined in groups of `group_batches` 4 MiB batches
+ * (0 = 2) over internal streams so H2D, kernels and D2H overlap; ordered after earlier work on `stream`,
+ * and later work on `stream` waits for it.  d_work: count floats of device scratch (16-byte aligned). */
+int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, double scale, float* d_work, uint8_t* d_stages,
+                                uint64_t stage_stride, uint64_t stage_len, int32_t pin,
+                                const zc_transport_hint* h_hint, const zc_huff_ctx* ctx, const zc_arb_config* h_cfg,
+                                zc_encode_result* d_results, uint32_t* d_index, uint32_t* d_err, float* h_y,
+                                uint32_t group_batches, void* stream);
 
 /* ---- L6 collectives (collectives.hpp:48-153) ----
  * One zc_comm per rank.  Multi-process: each rank calls zc_comm_create, exchanges the opaque

@@ -69,7 +69,7 @@ struct Scratch {
   uint32_t* flags = nullptr;
   uint64_t nflags = 0;
   uint32_t* sink = nullptr;
-  void* task = nullptr;  // task-kernel unit states
+  void* task = nullptr;  // batched-encoder unit states
   size_t task_bytes = 0;
 };
 static std::mutex g_scratch_mu;
@@ -105,24 +105,20 @@ int encode_common(EncParams& p, cudaStream_t s) {
   Scratch* sc = scratch_for(s, 1);
   if (!sc) return set_err(ZC_ERR_CUDA, "cannot allocate scratch (no CUDA device?)");
   if (p.err == nullptr) p.err = sc->sink;
-  // The batched send path (many frames, shared or no Huffman context) runs on the persistent
-  // task kernel; single frames, bare codecs, profiling and embedded codebooks on the cluster one.
-  if (p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook && std::getenv("ZC_NO_TASKS") == nullptr) {
-    const char* which = std::getenv("ZC_ENCODER");  // developer switch: batch (default) | stream | tasks
-    const int kind = which == nullptr ? 0 : (std::strcmp(which, "stream") == 0 ? 1 : std::strcmp(which, "tasks") == 0 ? 2 : 0);
-    const bool stream = kind == 1 && stream_encoder_ok(p);
-    const size_t need = kind == 0 ? batch_scratch_bytes(p.nunits)
-                                  : (stream ? stream_scratch_bytes(p.nunits) : task_scratch_bytes(p.nunits));
+  // The batched send path (many frames, shared or no Huffman context) runs on the streaming
+  // profile / range / emit kernels (zc_batch.cu, zc_fixed.cu); single frames, bare codecs,
+  // profiling and embedded codebooks on the cluster kernels (zc_encode.cu).
+  if (p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook) {
+    const size_t need = batch_scratch_bytes(p.nunits);
     if (sc->task_bytes < need) {
       cudaStreamSynchronize(s);
       if (sc->task) cudaFree(sc->task);
       sc->task = nullptr;
       sc->task_bytes = 0;
-      if (int rc = cuda_err(cudaMalloc(&sc->task, need), "task scratch")) return rc;
+      if (int rc = cuda_err(cudaMalloc(&sc->task, need), "encoder scratch")) return rc;
       sc->task_bytes = need;
     }
-    if (kind == 0) return cuda_err(launch_encode_batch(p, sc->task, s), "encode");
-    return cuda_err(stream ? launch_encode_stream(p, sc->task, s) : launch_encode_tasks(p, sc->task, s), "encode");
+    return cuda_err(launch_encode_batch(p, sc->task, s), "encode");
   }
   return cuda_err(launch_encode(p, s), "encode");
 }
@@ -694,3 +690,78 @@ int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stride, uint64_t
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ host-buffer pipelines
+// Internal copy/compute streams per device: group g of a host-buffer call runs on stream g % kPipe,
+// so H2D of one group, the kernels of another and D2H of a third overlap (separate copy engines,
+// PCIe full duplex).  Each internal stream has its own encode/decode scratch (scratch_for).
+namespace {
+constexpr int kPipe = 3;
+struct Pipe {
+  cudaStream_t s[kPipe] = {};
+  cudaEvent_t done[kPipe] = {};
+  cudaEvent_t start = nullptr;
+  bool ok = false;
+};
+std::mutex g_pipe_mu;
+std::map<int, Pipe> g_pipes;
+
+Pipe* pipe_for_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(g_pipe_mu);
+  Pipe& pp = g_pipes[dev];
+  if (!pp.ok) {
+    for (int i = 0; i < kPipe; ++i) {
+      if (cudaStreamCreateWithFlags(&pp.s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&pp.done[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&pp.start, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    pp.ok = true;
+  }
+  return &pp;
+}
+}  // namespace
+
+extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, double scale, float* d_work,
+                                           uint8_t* d_stages, uint64_t stride, uint64_t stage_len, int32_t pin,
+                                           const zc_transport_hint* hint, const zc_huff_ctx* ctx,
+                                           const zc_arb_config* cfg, zc_encode_result* d_results, uint32_t* d_index,
+                                           uint32_t* d_err, float* h_y, uint32_t group_batches, void* stream) {
+  if (count == 0) return ZC_OK;
+  if (h_x == nullptr || h_y == nullptr || d_work == nullptr) return set_err(ZC_ERR_INVALID_ARGUMENT, "null buffer");
+  if (int rc = check_scale(scale, "eb_quantize_chunk")) return rc;
+  if (!aligned16(d_work)) return set_err(ZC_ERR_INVALID_ARGUMENT, "work buffer must be 16-byte aligned");
+  Pipe* pp = pipe_for_device();
+  if (pp == nullptr) return set_err(ZC_ERR_CUDA, "cannot create pipeline streams (no CUDA device?)");
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  const uint64_t per = ZC_BATCH_RAW_BYTES / 4;  // elements per batch
+  const uint64_t nb = (count + per - 1) / per;
+  const uint64_t gb = group_batches ? group_batches : 2;
+  const uint64_t ngroups = (nb + gb - 1) / gb;
+  if (int rc = cuda_err(cudaEventRecord(pp->start, caller), "pipeline start")) return rc;
+  for (int i = 0; i < kPipe; ++i)
+    if (int rc = cuda_err(cudaStreamWaitEvent(pp->s[i], pp->start, 0), "pipeline wait")) return rc;
+  for (uint64_t g = 0; g < ngroups; ++g) {
+    const cudaStream_t s = pp->s[g % kPipe];
+    const uint64_t b0 = g * gb;
+    const uint64_t e0 = b0 * per;
+    const uint64_t n = (count - e0) < gb * per ? (count - e0) : gb * per;
+    if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, s), "H2D")) return rc;
+    if (int rc = encode_batches(d_work + e0, SRC_F32, n * 4, scale, d_stages + b0 * stride, stride, stage_len, pin, hint,
+                                ctx, cfg, d_results + b0, d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr,
+                                d_err, s))
+      return rc;
+    // decoded in place: the group's encode has consumed its input (stream order)
+    if (int rc = decode_batches(d_stages + b0 * stride, stride, stage_len, d_results + b0, n * 4, ctx,
+                                d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr, OUT_F32, d_work + e0, scale,
+                                nullptr, d_err, s))
+      return rc;
+    if (int rc = cuda_err(cudaMemcpyAsync(h_y + e0, d_work + e0, n * 4, cudaMemcpyDeviceToHost, s), "D2H")) return rc;
+  }
+  for (int i = 0; i < kPipe; ++i) {
+    if (int rc = cuda_err(cudaEventRecord(pp->done[i], pp->s[i]), "pipeline done")) return rc;
+    if (int rc = cuda_err(cudaStreamWaitEvent(caller, pp->done[i], 0), "pipeline join")) return rc;
+  }
+  return ZC_OK;
+}

@@ -22,70 +22,11 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "zc_encode_common.cuh"
+#include "zc_batch.cuh"
 #include "zc_huff_device.cuh"
 
 namespace zc {
 namespace {
-
-constexpr uint32_t BS = 65536;                      // slice: raw symbol bytes
-constexpr uint32_t BV = BS / 16;                    // vectors per slice
-constexpr uint32_t BMAX = ZC_BATCH_RAW_BYTES / BS;  // slices per full 4 MiB unit
-
-struct BPart {  // per slice (pass 2)
-  float fmn, fmx;
-  double dmn, dmx;
-  uint32_t maxzz, bad, zero, _p;
-  unsigned long long bits;
-};
-
-struct BUnit {  // per unit, zeroed before every launch
-  uint32_t plan;  // selector choice (Auto)
-  uint32_t codec, width, scan_done;
-  unsigned long long payload;
-  uint32_t edone, pdone;
-  uint32_t whist[256];  // window histogram (pass 1, merged from PC CTAs)
-  uint32_t wmz;         // window max zig-zag
-  uint32_t maxzz, bad, _q;
-  uint32_t fmin_c, fmax_k;           // fp32 range as order-preserving keys (min complemented)
-  unsigned long long dmin_c, dmax_k;  // fp64 range, same encoding
-  BPart part[BMAX];
-  unsigned long long hbase[BMAX];
-  unsigned long long head_idx[BMAX], tail_idx[BMAX];
-  uint32_t head_val[BMAX], tail_val[BMAX], has_head[BMAX], has_tail[BMAX];
-};
-
-struct BGeom {
-  uint32_t s_full;  // slices per full unit
-  uint64_t total;   // slices in the message
-  __device__ __forceinline__ void unit_of(uint64_t t, uint32_t nunits, uint32_t& u, uint32_t& s) const {
-    const uint64_t head = static_cast<uint64_t>(nunits - 1) * s_full;
-    if (t < head) {
-      u = static_cast<uint32_t>(t / s_full);
-      s = static_cast<uint32_t>(t - static_cast<uint64_t>(u) * s_full);
-    } else {
-      u = nunits - 1;
-      s = static_cast<uint32_t>(t - head);
-    }
-  }
-};
-
-__device__ __forceinline__ uint64_t unit_R(const EncParams& p, uint32_t u) {
-  const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
-  return (p.total_bytes - uoff) < p.unit_bytes ? (p.total_bytes - uoff) : p.unit_bytes;
-}
-__device__ __forceinline__ uint32_t unit_slices(const EncParams& p, uint32_t u) {
-  return static_cast<uint32_t>((unit_R(p, u) + BS - 1) / BS);
-}
-
-// The codec pass 2/3 work towards for a unit: Auto -> the plan; pins -> the pin (RAW when the
-// pinned codec cannot apply).
-__device__ __forceinline__ uint32_t target_codec(const EncParams& p, const BUnit& U, bool ctx_ok) {
-  if (p.pin == ZC_PIN_AUTO) return U.plan;
-  if (p.pin == ZC_PIN_FIXEDLEN) return ZC_CODEC_FIXEDLEN;
-  if (p.pin == ZC_PIN_HUFFMAN) return ctx_ok ? ZC_CODEC_HUFFMAN : ZC_CODEC_RAW;
-  return ZC_CODEC_RAW;
-}
 
 // ------------------------------------------------------------------ pass 1: window profile + plan
 constexpr uint32_t PC = 16;            // CTAs per unit window (64 KiB / 16 = 4 KiB each)
@@ -183,6 +124,7 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
         o->self_code_len_valid = 0u;
       }
       U.plan = arbitrate_plan(R, pcap, st, p.hint, ctx_ok, p.cfg).choice;
+      if (U.plan == ZC_CODEC_HUFFMAN) atomicAdd(&bglobal(us, p.nunits)->n_huff, 1u);
     }
   }
   err = __reduce_or_sync(FULL, err);
@@ -190,76 +132,6 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
 }
 
 // ------------------------------------------------------------------ pass 2: ranges / bit counts, decision
-// Order-preserving u32/u64 keys of fp32/fp64 values, so the unit range merges with atomicMax
-// (the minimum is kept as the complement of its key: zero-initialised state works for both).
-__device__ __forceinline__ uint32_t fkey(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float fkey_inv(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
-__device__ __forceinline__ unsigned long long dkey(double d) {
-  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d));
-  return (u >> 63) ? ~u : (u | (1ull << 63));
-}
-__device__ __forceinline__ double dkey_inv(unsigned long long k) {
-  return __longlong_as_double(static_cast<long long>((k >> 63) ? (k & ~(1ull << 63)) : ~k));
-}
-
-// The unit's final decision once every slice has reported (tid 0 of the CTA that completed it):
-// encode_best post-checks (rea.cpp:189-236) or the pinned send_batch fallbacks (collectives.cpp:223-275).
-template <int SRC>
-__device__ void decide_unit(const EncParams& p, BUnit& U, uint32_t u, bool want_range, bool fast_ok, uint32_t& err) {
-  constexpr bool kFloat = SRC != SRC_BYTES;
-  const uint64_t R = unit_R(p, u);
-  const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
-  const uint32_t ns = unit_slices(p, u);
-  uint32_t codec = ZC_CODEC_RAW, width = 0;
-  unsigned long long pay_b = R;
-  const bool gate = p.pin == ZC_PIN_AUTO;  // Auto applies gain_ok; pins do not
-  if (want_range) {
-    uint32_t maxzz = __ldcg(&U.maxzz);
-    if (kFloat && fast_ok) {
-      if (__ldcg(&U.bad)) {
-        err |= ZC_DERR_NONFINITE;
-      } else if (R >= 4) {
-        double mn, mx;
-        if (SRC == SRC_F32) {
-          mn = static_cast<double>(fkey_inv(~__ldcg(&U.fmin_c)));
-          mx = static_cast<double>(fkey_inv(__ldcg(&U.fmax_k)));
-        } else {
-          mn = dkey_inv(~__ldcg(&U.dmin_c));
-          mx = dkey_inv(__ldcg(&U.dmax_k));
-        }
-        maxzz = max(zigzag32(quantize_one(mx, p.scale, p.rcp, err)), zigzag32(quantize_one(mn, p.scale, p.rcp, err)));
-      }
-    }
-    if (R >= 4 && R % 4 == 0) {
-      width = width_from_maxzz(maxzz);
-      const unsigned long long pay = packed_bytes(R / 4, width);
-      if (pay > 0 && pay <= pcap && (!gate || gain_ok(R, pay, p.cfg.min_gain_permil))) {
-        codec = ZC_CODEC_FIXEDLEN;
-        pay_b = pay;
-      }
-    }
-  } else {
-    uint32_t zl = 0;
-    unsigned long long bits = 0;
-    for (uint32_t r = 0; r < ns; ++r) {
-      zl |= __ldcg(&U.part[r].zero);
-      U.hbase[r] = bits;
-      bits += __ldcg(&U.part[r].bits);
-    }
-    const unsigned long long pay = (bits + 7) / 8;
-    if (!zl && pay > 0 && pay <= pcap && (!gate || gain_ok(R, pay, p.cfg.min_gain_permil))) {
-      codec = ZC_CODEC_HUFFMAN;
-      pay_b = pay;
-    }
-  }
-  U.codec = codec;
-  U.width = width;
-  U.payload = pay_b;
-}
-
 // Each CTA streams a CONTIGUOUS range of slices (mostly inside one unit), keeps the value range in
 // registers across the slices of a unit and merges it into the unit once per unit (one block
 // reduction + atomics), so the pass is a plain HBM stream; Huffman units reduce per slice (the
@@ -274,6 +146,7 @@ __global__ void __launch_bounds__(NT, 1) scan_kernel(const EncParams p, BUnit* u
   constexpr bool kFloat = SRC != SRC_BYTES;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
+  if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<volatile uint32_t*>(&bglobal(us, p.nunits)->n_huff) == 0) return;
   for (int i = tid; i < 256; i += NT) s_clens[i] = ctx_ok ? p.ctx->len[i] : 0;
   __syncthreads();
   uint32_t err = 0;
@@ -345,6 +218,7 @@ __global__ void __launch_bounds__(NT, 1) scan_kernel(const EncParams p, BUnit* u
     BUnit& U = us[u];
     const uint32_t target = target_codec(p, U, ctx_ok);
     if (target != ZC_CODEC_FIXEDLEN && target != ZC_CODEC_HUFFMAN) continue;  // RAW: decided in pass 3
+    if (g.fast && target == ZC_CODEC_FIXEDLEN) continue;                      // zc_fixed.cu's range pass
     const uint64_t R = unit_R(p, u);
     const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
     const uint64_t v0 = static_cast<uint64_t>(s) * BV;
@@ -469,6 +343,7 @@ __global__ void __launch_bounds__(NT, 1) emit_kernel(const EncParams p, BUnit* u
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
   const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
+  if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<const volatile uint32_t*>(&bglobal(us, p.nunits)->n_huff) == 0) return;
   for (int i = tid; i < 256; i += NT) s_enc[i] = ctx_ok ? p.ctx->enc[i] : 0ull;
   __syncthreads();
   uint32_t err = 0;
@@ -498,6 +373,7 @@ __global__ void __launch_bounds__(NT, 1) emit_kernel(const EncParams p, BUnit* u
       P = U.payload;
       if (codec == ZC_CODEC_RAW && R > pcap) codec = CODEC_NONE;
     }
+    if (g.fast && codec != ZC_CODEC_HUFFMAN) continue;  // zc_fixed.cu's emit owns RAW / FixedLen / failures
     if (codec == CODEC_NONE) {
       if (s == 0) err |= ZC_DERR_CAPACITY;
     } else if (codec == ZC_CODEC_RAW) {
@@ -727,30 +603,46 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaMemsetAsync(scratch, 0, sizeof(BUnit) * p.nunits, s);
+  cudaMemsetAsync(scratch, 0, sizeof(BUnit) * p.nunits + sizeof(BGlobal), s);
   BUnit* us = static_cast<BUnit*>(scratch);
   BGeom g;
   g.s_full = static_cast<uint32_t>((p.unit_bytes + BS - 1) / BS);
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
+  g.fast = (SRC == SRC_F32 && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
   if (p.pin == ZC_PIN_AUTO) {
     note_launch();
     profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
   }
   const bool ctx_ok_host = p.ctx != nullptr;  // validity is checked on the device
+  const bool huff_possible = (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_HUFFMAN) && ctx_ok_host;
+  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms)));
+  if (g.fast) {
+    if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN)
+      if (cudaError_t e = launch_fixed_range(p, scratch, g.total, g.s_full, sms, s)) return e;
+    if (huff_possible) {
+      note_launch();
+      scan_kernel<SRC><<<grid, NT, 0, s>>>(p, us, g);
+    }
+    if (cudaError_t e = launch_fixed_emit(p, scratch, g.total, g.s_full, sms, s)) return e;
+    if (huff_possible) {
+      note_launch();
+      emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
+    }
+    return cudaGetLastError();
+  }
   if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN || (p.pin == ZC_PIN_HUFFMAN && ctx_ok_host)) {
     note_launch();
-    scan_kernel<SRC><<<static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms))), NT, 0, s>>>(p, us, g);
+    scan_kernel<SRC><<<grid, NT, 0, s>>>(p, us, g);
   }
   note_launch();
-  emit_kernel<SRC><<<static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms))), NT,
-                     sizeof(Scratch), s>>>(p, us, g);
+  emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t batch_scratch_bytes(uint32_t nunits) { return sizeof(BUnit) * (nunits ? nunits : 1); }
+size_t batch_scratch_bytes(uint32_t nunits) { return sizeof(BUnit) * (nunits ? nunits : 1) + sizeof(BGlobal); }
 
 void preload_batch_kernels() {
   cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));

@@ -553,9 +553,8 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     preload_encode_kernels();
     preload_decode_kernels();
     preload_quant_kernels();
-    preload_task_kernels();
-    preload_stream_kernels();
     preload_batch_kernels();
+    preload_fixed_kernels();
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, mailbox_kernel);
     cudaFuncGetAttributes(&fa, requant_kernel);

@@ -11,6 +11,8 @@
 // companion bit-offset index; a grain that does not end exactly where the next one starts (an
 // index that does not belong to the payload) sends the unit to the sequential decoder, which is
 // also the path for frames that come without an index (e.g. produced by the CPU reference).
+#include <cstdlib>
+
 #include "zc_decode.cuh"
 
 namespace zc {
@@ -54,11 +56,13 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
     check_frame<false>(stage, unit_region(p, u), R, p.bare ? &p.hdr : nullptr, p.bare != 0, p.ctx, p.index != nullptr, fc);
   __syncthreads();
   if (blockIdx.x == 0 && tid == 0) {
-    if (p.codec_out && !p.bare) p.codec_out[u] = fc.codec;
+    if (p.codec_out && !p.bare && !(p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)))
+      p.codec_out[u] = fc.codec;
     if (p.bare && p.ok_out) *p.ok_out = fc.codec == kFallback ? 0 : 1;
     if (fc.need_seq) atomicOr(&p.flags[u], 1u);
   }
   if (fc.codec == kFallback && p.bare) return;
+  if (p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)) return;  // zc_fixed.cu decoded it
   Sink sink{p.out_kind, p.out, p.scale};
   const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
   uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
@@ -153,8 +157,14 @@ void preload_decode_kernels() {
   cudaGetLastError();
 }
 
-cudaError_t launch_decode(const DecParams& p, cudaStream_t s) {
-  if (p.nunits == 0) return cudaSuccess;
+cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
+  if (p0.nunits == 0) return cudaSuccess;
+  DecParams p = p0;
+  p.fast = 0;
+  if (fixed_decode_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) {
+    if (cudaError_t e = launch_fixed_decode(p, s)) return e;
+    p.fast = 1;
+  }
   const uint64_t maxR = p.bare ? p.hdr.raw_bytes : (p.unit_bytes < p.total_bytes ? p.unit_bytes : p.total_bytes);
   const uint64_t nvec = (maxR + 15) / 16;
   const uint32_t slices = static_cast<uint32_t>((nvec + SLICE_VEC - 1) / SLICE_VEC);

@@ -1,0 +1,695 @@
+// zc_fixed.cu — the fp32 hot path of the batched send encoder (send_encoded over a message,
+// collectives.cpp:201-302 for every 4 MiB batch) for units that end up FixedLen or RAW:
+//
+//   range    one HBM stream over the FixedLen-target units: fp32 min / max (NaN-propagating), so
+//            the unit's width is width(max(zz(q(min)), zz(q(max)))) — quantization is monotone —
+//            without quantizing anything; the unit's last slice runs decide_unit (the post-checks
+//            of encode_best, rea.cpp:189-236, or the pinned send_batch fallbacks,
+//            collectives.cpp:223-275).
+//   emit     quantize (quant.cpp:22-27) + zig-zag + LSB-first pack (fixedlen.cpp:15-37) or the raw
+//            symbol copy, streamed through TMA: each warp owns a ring of 4 KiB tiles (32 rows x 32
+//            fp32, 128-byte swizzle) filled by cp.async.bulk.tensor and signalled on mbarriers, so
+//            HBM reads run ahead of the arithmetic.  Lane L owns the 32 consecutive symbols of row
+//            L, whose packed bits are exactly W whole words (W = width): the pack is compile-time
+//            shifts in registers and the words go out as 16/8/4-byte stores.
+//
+// Huffman units (and every non-fp32 / unaligned source) stay on zc_batch.cu's kernels, which skip
+// the units handled here.  Frames are byte-identical to the reference's.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "zc_batch.cuh"
+#include "zc_tma.cuh"
+
+namespace zc {
+namespace {
+
+constexpr int RT = 512;                  // range kernel threads
+constexpr int ET_WARPS = 16;             // emit kernel warps per CTA
+constexpr int ET = ET_WARPS * 32;
+constexpr int STAGES = 3;                // tiles in flight per warp
+constexpr uint32_t TILE_ELEMS = 1024;    // 32 x 32 fp32
+constexpr uint32_t TILE_BYTES = TILE_ELEMS * 4;
+constexpr uint32_t UNIT_TILES = ZC_BATCH_RAW_BYTES / TILE_BYTES;  // 1024
+constexpr size_t EMIT_SMEM = static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES + 1024 + ET_WARPS * STAGES * 8;
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// ------------------------------------------------------------------ range
+__global__ void __launch_bounds__(RT, 2) range_kernel(const EncParams p, BUnit* us, BGeom g) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float s_mn[RT / 32], s_mx[RT / 32];
+  const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
+  uint32_t err = 0;
+  const uint64_t t0 = g.total * blockIdx.x / gridDim.x, t1 = g.total * (blockIdx.x + 1) / gridDim.x;
+  float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+  uint32_t run_u = 0xffffffffu, run_n = 0;
+  auto flush = [&]() {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin_nan(mn, __shfl_xor_sync(FULL, mn, o));
+      mx = fmax_nan(mx, __shfl_xor_sync(FULL, mx, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+      s_mn[warp] = mn;
+      s_mx[warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 1; i < RT / 32; ++i) {
+        mn = fmin_nan(mn, s_mn[i]);
+        mx = fmax_nan(mx, s_mx[i]);
+      }
+      BUnit& U = us[run_u];
+      const bool bad = !(fabsf(mn) <= 3.402823466e38f) || !(fabsf(mx) <= 3.402823466e38f);  // NaN / Inf
+      if (bad) atomicOr(&U.bad, 1u);
+      atomicMax(&U.fmin_c, ~fkey(mn));
+      atomicMax(&U.fmax_k, fkey(mx));
+      __threadfence();
+      if (atomicAdd(&U.scan_done, run_n) + run_n == unit_slices(p, run_u)) {
+        __threadfence();
+        decide_unit<SRC_F32>(p, U, run_u, true, true, err);
+      }
+    }
+    mn = __int_as_float(0x7f800000);
+    mx = -__int_as_float(0x7f800000);
+    run_n = 0;
+  };
+  for (uint64_t t = t0; t < t1; ++t) {
+    uint32_t u, s;
+    g.unit_of(t, p.nunits, u, s);
+    if (target_codec(p, us[u], ctx_ok) != ZC_CODEC_FIXEDLEN) continue;
+    if (run_n && run_u != u) flush();
+    run_u = u;
+    ++run_n;
+    const uint64_t R = unit_R(p, u);
+    const uint64_t nf = R / 16;  // whole 16-byte vectors of the unit
+    const uint64_t v0 = static_cast<uint64_t>(s) * BV;
+    const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
+    if (v0 + BV <= nf) {
+      const float4* q = src + v0 + tid;
+      float4 a[BV / RT];
+#pragma unroll
+      for (int k = 0; k < static_cast<int>(BV / RT); ++k) a[k] = __ldg(q + k * RT);
+#pragma unroll
+      for (int k = 0; k < static_cast<int>(BV / RT); ++k) {
+        mn = fmin_nan(mn, fmin_nan(fmin_nan(a[k].x, a[k].y), fmin_nan(a[k].z, a[k].w)));
+        mx = fmax_nan(mx, fmax_nan(fmax_nan(a[k].x, a[k].y), fmax_nan(a[k].z, a[k].w)));
+      }
+    } else {
+      const uint64_t v1 = min(v0 + BV, nf);
+      for (uint64_t v = v0 + tid; v < v1; v += RT) {
+        const float4 a = __ldg(src + v);
+        mn = fmin_nan(mn, fmin_nan(fmin_nan(a.x, a.y), fmin_nan(a.z, a.w)));
+        mx = fmax_nan(mx, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+      }
+      if (tid == 0 && v0 * 16 + BS >= R) {  // the unit's last 0..3 elements
+        const float* f = reinterpret_cast<const float*>(src);
+        for (uint64_t e = nf * 4; e < R / 4; ++e) {
+          mn = fmin_nan(mn, __ldg(f + e));
+          mx = fmax_nan(mx, __ldg(f + e));
+        }
+      }
+    }
+  }
+  if (run_n) flush();
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
+}
+
+// ------------------------------------------------------------------ emit
+// Quantizes the 32 fp32 values of a row; exact division (quantize_one) for any lane whose row
+// holds a value near a rounding tie.  `big` = the unit may hold |q| >= 2^30 (then every value
+// takes quantize_one).
+// quantize_one out of line: the rare exact path (near a tie, |q| >= 2^30, non-finite) must not
+// force the callers' per-row arrays into local memory.
+__device__ __noinline__ uint32_t quantize_exact(float x, double scale, double rcp, uint32_t* err) {
+  uint32_t e = 0;
+  const uint32_t r = static_cast<uint32_t>(quantize_one(static_cast<double>(x), scale, rcp, e));
+  *err |= e;
+  return r;
+}
+
+__device__ __forceinline__ void quantize_row(const float (&x)[32], double scale, double rcp, bool big, uint32_t (&s)[32],
+                                             uint32_t& err) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  uint32_t rm = 0;  // max over the row of the high word of |r|, r = q - round(q)
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const double q = __dmul_rn(static_cast<double>(x[i]), rcp);
+    const double t = __dadd_rn(q, kMagic);
+    const double r = __dsub_rn(q, __dsub_rn(t, kMagic));
+    rm = max(rm, static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu);
+    s[i] = static_cast<uint32_t>(__double2loint(t));
+  }
+  // a value within 2^-18 of a rounding tie (|r| >= 0.5 - 2^-18, high word >= 0x3FDFFFF0), or a
+  // unit that may leave the fast range: exact path for the row
+  if (big || rm >= 0x3FDFFFF0u) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s[i] = quantize_exact(x[i], scale, rcp, &err);
+  }
+}
+
+// Packs 32 zig-zag symbols of width W into W words and stores them at word `wb` of the payload
+// (no bound: the row lies wholly inside the payload).
+template <int W>
+__device__ __forceinline__ void pack_store_full(const uint32_t (&z)[32], uint32_t* dst) {
+  uint32_t o[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) o[k] = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {  // fields are disjoint: + is | (one IMAD per symbol)
+    const int bit = i * W, k = bit >> 5, sh = bit & 31;
+    o[k] += z[i] << sh;
+    if (sh + W > 32) o[k + 1] += z[i] >> (32 - sh);
+  }
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j) reinterpret_cast<uint4*>(dst)[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) reinterpret_cast<uint2*>(dst)[j] = make_uint2(o[2 * j], o[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) dst[j] = o[j];
+  }
+}
+
+__device__ __forceinline__ void store_row(uint32_t codec, uint32_t width, const uint32_t (&s)[32], uint8_t* payload,
+                                          uint64_t row_sym) {
+  uint32_t* base = reinterpret_cast<uint32_t*>(payload);
+  if (codec == ZC_CODEC_RAW) {
+    uint4* d = reinterpret_cast<uint4*>(base + row_sym);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = make_uint4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
+    return;
+  }
+  uint32_t z[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) z[i] = zigzag32(static_cast<int32_t>(s[i]));
+  uint32_t* d = base + (row_sym / 32) * width;
+  switch (width) {
+#define ZC_PS(W)                   \
+  case W:                          \
+    pack_store_full<W>(z, d);      \
+    break;
+    ZC_PS(1) ZC_PS(2) ZC_PS(3) ZC_PS(4) ZC_PS(5) ZC_PS(6) ZC_PS(7) ZC_PS(8) ZC_PS(9) ZC_PS(10) ZC_PS(11)
+    ZC_PS(12) ZC_PS(13) ZC_PS(14) ZC_PS(15) ZC_PS(16) ZC_PS(17) ZC_PS(18) ZC_PS(19) ZC_PS(20) ZC_PS(21)
+    ZC_PS(22) ZC_PS(23) ZC_PS(24) ZC_PS(25) ZC_PS(26) ZC_PS(27) ZC_PS(28) ZC_PS(29) ZC_PS(30) ZC_PS(31)
+    ZC_PS(32)
+#undef ZC_PS
+    default:
+      break;
+  }
+}
+
+// Warp tile order: warp gw owns chunks gw, gw + tw, ... of CHUNK consecutive tiles (chunks never
+// straddle a unit), so consecutive tiles of a warp share the unit's state and payload rows.
+constexpr uint64_t CHUNK = 4;
+__device__ __forceinline__ uint64_t tile_adv(uint64_t c, uint64_t tw) {
+  return ((c + 1) % CHUNK) != 0 ? c + 1 : c + 1 + (tw - 1) * CHUNK;
+}
+// The warp's first tile at or past tile `ue` (a unit boundary), given its current tile c.
+__device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64_t tw) {
+  const uint64_t j = c / CHUNK, je = ue / CHUNK;
+  return (j + ((je - j + tw - 1) / tw) * tw) * CHUNK;
+}
+
+struct UnitView {
+  uint32_t codec, width;
+  uint64_t P;
+  bool big;
+};
+
+// Per-unit view for the emit kernel: owned (RAW / FixedLen) or not, and whether the fast
+// quantizer applies (max |q| < 2^30 over the unit, from the range pass).
+__device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* us, uint32_t u, bool ctx_ok) {
+  UnitView v;
+  final_codec(p, us[u], u, ctx_ok, v.codec, v.width, v.P);
+  v.big = true;
+  if (v.codec == ZC_CODEC_FIXEDLEN) {
+    // the width is < 31 iff max zz < 2^30, i.e. every |q| < 2^29
+    v.big = v.width >= 31;
+  }
+  return v;
+}
+
+__device__ __forceinline__ bool owned(uint32_t codec) { return codec == ZC_CODEC_RAW || codec == ZC_CODEC_FIXEDLEN; }
+
+__global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ EncParams p, const BUnit* us, BGeom g,
+                                                     const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
+                                                     uint64_t nfull) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* s_tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* my = s_tiles + static_cast<size_t>(warp) * STAGES * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES) + warp * STAGES;
+  const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
+  uint32_t err = 0;
+
+  // headers / results of every owned unit, and the capacity failures (send_batch throws)
+  for (uint32_t u = blockIdx.x * ET + tid; u < p.nunits; u += gridDim.x * ET) {
+    const UnitView v = unit_view(p, us, u, ctx_ok);
+    if (owned(v.codec) || v.codec == CODEC_NONE) write_frame_header(p, u, v.codec, v.width, v.P);
+    if (v.codec == CODEC_NONE) err |= ZC_DERR_CAPACITY;
+  }
+
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) tma::mbar_init(&bars[i], 1);
+    tma::fence_barrier_init();
+  }
+  __syncwarp();
+
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * ET_WARPS + warp, tw = static_cast<uint64_t>(gridDim.x) * ET_WARPS;
+  // The warp's tile sequence: tiles gw, gw+tw, ... of owned units, full tiles only.
+  uint32_t iss_u = 0xffffffffu;
+  bool iss_owned = false;
+  auto next_tile = [&](uint64_t c) -> uint64_t {
+    while (c < nfull) {
+      const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+      if (u != iss_u) {
+        iss_u = u;
+        iss_owned = owned(unit_view(p, us, u, ctx_ok).codec);
+      }
+      if (iss_owned) return c;
+      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
+    }
+    return nfull;
+  };
+  uint64_t c_issue = next_tile(gw * CHUNK);
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      if (c_issue < nfull) {
+        tma::mbar_arrive_expect_tx(&bars[i], TILE_BYTES);
+        tma::load_2d(my + i * TILE_BYTES, &tmap, &bars[i], 0, static_cast<int32_t>(c_issue * 32));
+      }
+      c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
+    }
+  } else {
+    for (int i = 0; i < STAGES; ++i) c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
+  }
+  uint32_t k = 0, cur_u = 0xffffffffu;
+  UnitView v;
+  uint8_t* payload = nullptr;
+  const double scale = p.scale, rcp = p.rcp;
+  uint64_t c_first = gw;
+  {  // the processing sequence restarts from the first tile (its own unit cache)
+    iss_u = 0xffffffffu;
+    c_first = next_tile(gw * CHUNK);
+    iss_u = 0xffffffffu;
+  }
+  for (uint64_t c = c_first; c < nfull; c = next_tile(tile_adv(c, tw)), ++k) {
+    const uint32_t st = k % STAGES;
+    tma::mbar_wait(&bars[st], (k / STAGES) & 1u);
+    const uint8_t* tile = my + st * TILE_BYTES;
+    float x[32];
+    const uint32_t row = tma::smem_u32(tile) + lane * 128;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x[4 * m]), "=f"(x[4 * m + 1]), "=f"(x[4 * m + 2]), "=f"(x[4 * m + 3])
+                   : "r"(row + ((m ^ (lane & 7)) << 4)));
+    }
+    __syncwarp();
+    if (lane == 0 && c_issue < nfull) {  // refill this stage
+      tma::mbar_arrive_expect_tx(&bars[st], TILE_BYTES);
+      tma::load_2d(my + st * TILE_BYTES, &tmap, &bars[st], 0, static_cast<int32_t>(c_issue * 32));
+    }
+    c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
+    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    if (u != cur_u) {
+      cur_u = u;
+      v = unit_view(p, us, u, ctx_ok);
+      payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+    }
+    uint32_t s[32];
+    quantize_row(x, scale, rcp, v.big, s, err);
+    store_row(v.codec, v.width, s, payload, (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
+  }
+
+  // the message's last, partial tile (direct guarded loads / byte-exact tail stores)
+  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
+    const uint64_t c = nfull;
+    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    v = unit_view(p, us, u, ctx_ok);
+    if (owned(v.codec)) {
+      const uint64_t R = unit_R(p, u);
+      const uint64_t n = R / 4;  // symbols of the unit
+      const uint64_t e0 = (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
+      const float* src = static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4);
+      uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+      uint32_t s[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[i] = e0 + i < n ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err) : 0u;
+      if (v.codec == ZC_CODEC_RAW) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (e0 + i < n) reinterpret_cast<uint32_t*>(payload)[e0 + i] = s[i];
+        // a raw unit of f32 source has R % 4 == 0: no partial word
+      } else {
+        uint32_t z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = zigzag32(static_cast<int32_t>(s[i]));
+        if (e0 < n) pack_store_w(v.width, z, payload, (e0 / 32) * v.width, v.P);
+      }
+    }
+  }
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
+}
+
+// ------------------------------------------------------------------ decode (FixedLen / RAW -> fp32)
+// recv_batch's decode dispatch (collectives.cpp:314-336) for valid FixedLen and RAW frames fused
+// with dequantize_into (quant.cpp:107-127) into fp32: lane L reads the W payload words of row L
+// (its 32 symbols) straight from HBM — the next row's words are in flight while this one is
+// unpacked with compile-time shifts — and writes its 32 floats into a 128-byte-swizzled 4 KiB
+// tile that one TMA tensor store (cp.async.bulk.tensor) moves to HBM.  Everything else (Huffman,
+// the raw-copy fallback, other sinks) stays on zc_decode.cu's kernels, which skip these units.
+constexpr int DT_WARPS = 16;
+constexpr int DT = DT_WARPS * 32;
+constexpr size_t DEC_SMEM = static_cast<size_t>(DT_WARPS) * 2 * TILE_BYTES + 1024;
+
+struct DecView {
+  uint32_t codec;  // ZC_CODEC_RAW / ZC_CODEC_FIXEDLEN when this kernel owns the unit, else kFallback
+  uint32_t width;  // FixedLen width; 0 for RAW
+};
+
+__device__ __forceinline__ DecView dec_view(const DecParams& p, uint32_t u) {
+  const uint64_t off = static_cast<uint64_t>(u) * p.unit_bytes;
+  const uint64_t R = (p.total_bytes - off) < p.unit_bytes ? (p.total_bytes - off) : p.unit_bytes;
+  FrameCheck fc;
+  check_frame<false>(p.stages + static_cast<uint64_t>(u) * p.stride, p.frame_len ? p.frame_len[u].total_bytes : p.region,
+                     R, nullptr, false, p.ctx, p.index != nullptr, fc);
+  DecView v;
+  v.codec = (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN) ? fc.codec : kFallback;
+  v.width = fc.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(fc.h.params) : 0u;
+  return v;
+}
+
+// W words of row `row` (W = 32 and kRaw: the symbols themselves).
+template <int W>
+__device__ __forceinline__ void load_row_words(const uint32_t* payload, uint64_t row, uint32_t (&a)[W]) {
+  const uint32_t* s = payload + row * W;
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(s) + j);
+      a[4 * j] = q.x;
+      a[4 * j + 1] = q.y;
+      a[4 * j + 2] = q.z;
+      a[4 * j + 3] = q.w;
+    }
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+      const uint2 q = __ldg(reinterpret_cast<const uint2*>(s) + j);
+      a[2 * j] = q.x;
+      a[2 * j + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) a[j] = __ldg(s + j);
+  }
+}
+
+// Symbol i (0..31) of a row packed at width W (fixedlen.cpp:49-63), un-zig-zagged.
+template <int W, bool kRaw>
+__device__ __forceinline__ int32_t row_symbol(const uint32_t (&a)[W], int i) {
+  if (kRaw) return static_cast<int32_t>(a[i]);
+  const int bit = i * W, k = bit >> 5, sh = bit & 31;
+  uint32_t z;
+  if (sh + W <= 32) {
+    z = a[k] >> sh;
+  } else {
+    z = __funnelshift_r(a[k], a[k + 1], sh);
+  }
+  constexpr uint32_t kMask = W < 32 ? (1u << (W & 31)) - 1u : 0xffffffffu;
+  z &= kMask;
+  return unzigzag32(z);
+}
+
+template <int W, bool kRaw>
+__device__ __forceinline__ void dequant_row_to_tile(const uint32_t (&a)[W], double scale, uint8_t* tile, int lane) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    float f[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t sym = row_symbol<W, kRaw>(a, 4 * m + q);
+      f[q] = __double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym))));
+    }
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(tma::smem_u32(tile) + lane * 128 + ((m ^ (lane & 7)) << 4)),
+                 "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3])
+                 : "memory");
+  }
+}
+
+struct DecSeq {  // the warp's tile sequence over owned units
+  const DecParams* p;
+  uint64_t nfull, tw;
+  uint32_t cu;
+  DecView cv;
+  __device__ __forceinline__ uint64_t next(uint64_t c) {
+    while (c < nfull) {
+      const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+      if (u != cu) {
+        cu = u;
+        cv = dec_view(*p, u);
+      }
+      if (cv.codec != kFallback) return c;
+      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
+    }
+    return nfull;
+  }
+};
+
+// Runs the warp's tiles c, tile_adv(c), ... while they stay below `end` (the unit's last full tile or
+// the message's); returns the first tile past them and the updated store counter.  Out of line
+// per width: the row arrays live in registers, and all arguments are scalars.
+struct DecStep {
+  uint64_t c;
+  uint32_t k;
+};
+template <int W, bool kRaw>
+__device__ __noinline__ DecStep decode_unit_tiles(const uint32_t* payload, uint64_t c, uint64_t end, uint64_t tw,
+                                                  double scale, const CUtensorMap* tmap, uint8_t* bufs, uint32_t k,
+                                                  int lane) {
+  uint32_t a[W], b[W];
+  load_row_words<W>(payload, (c % UNIT_TILES) * 32 + lane, a);
+  for (;;) {
+    const uint64_t cn = tile_adv(c, tw);
+    const bool more = cn < end;
+    if (more) load_row_words<W>(payload, (cn % UNIT_TILES) * 32 + lane, b);
+    uint8_t* tile = bufs + (k & 1) * TILE_BYTES;
+    if (lane == 0) tma::bulk_wait_read<1>();  // the store issued from this buffer two tiles ago
+    __syncwarp();
+    dequant_row_to_tile<W, kRaw>(a, scale, tile, lane);
+    tma::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma::store_2d(tmap, tile, 0, static_cast<int32_t>(c * 32));
+      tma::bulk_commit();
+    }
+    ++k;
+    if (!more) return DecStep{cn, k};
+    c = cn;
+#pragma unroll
+    for (int j = 0; j < W; ++j) a[j] = b[j];
+  }
+}
+
+__global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant__ DecParams p, const __grid_constant__ CUtensorMap tmap,
+                                                          uint64_t ntiles, uint64_t nfull) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* s_tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* bufs = s_tiles + static_cast<size_t>(warp) * 2 * TILE_BYTES;
+  uint32_t err = 0;
+  // decoded codec per owned unit (recv_batch's dispatch result)
+  for (uint32_t u = blockIdx.x * DT + tid; u < p.nunits; u += gridDim.x * DT) {
+    const DecView v = dec_view(p, u);
+    if (v.codec != kFallback && p.codec_out) p.codec_out[u] = v.codec;
+  }
+  DecSeq seq;
+  seq.p = &p;
+  seq.nfull = nfull;
+  seq.tw = static_cast<uint64_t>(gridDim.x) * DT_WARPS;
+  seq.cu = 0xffffffffu;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * DT_WARPS + warp;
+  uint32_t k = 0;
+  uint64_t c = seq.next(gw * CHUNK);
+  while (c < nfull) {
+    const DecView v = seq.cv;  // view of c's unit (seq.next just returned c)
+    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    const uint64_t ue = static_cast<uint64_t>(u + 1) * UNIT_TILES;
+    const uint64_t end = ue < nfull ? ue : nfull;
+    const uint32_t* payload = reinterpret_cast<const uint32_t*>(p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes);
+    DecStep st{nfull, k};
+    if (v.codec == ZC_CODEC_RAW) {
+      st = decode_unit_tiles<32, true>(payload, c, end, seq.tw, p.scale, &tmap, bufs, k, lane);
+    } else {
+      switch (v.width) {
+#define ZC_DC(W)                                                                                \
+  case W:                                                                                       \
+    st = decode_unit_tiles<W, false>(payload, c, end, seq.tw, p.scale, &tmap, bufs, k, lane); \
+    break;
+        ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
+        ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
+        ZC_DC(22) ZC_DC(23) ZC_DC(24) ZC_DC(25) ZC_DC(26) ZC_DC(27) ZC_DC(28) ZC_DC(29) ZC_DC(30) ZC_DC(31)
+        ZC_DC(32)
+#undef ZC_DC
+        default:
+          break;
+      }
+    }
+    k = st.k;
+    c = seq.next(st.c);
+  }
+  // the message's last, partial tile: symbol by symbol with byte-exact bounds
+  if (nfull < ntiles && gw == (nfull / CHUNK) % seq.tw) {
+    const uint32_t u = static_cast<uint32_t>(nfull / UNIT_TILES);
+    const DecView v = dec_view(p, u);
+    if (v.codec != kFallback) {
+      const uint64_t off = static_cast<uint64_t>(u) * p.unit_bytes;
+      const uint64_t n = ((p.total_bytes - off) < p.unit_bytes ? (p.total_bytes - off) : p.unit_bytes) / 4;
+      const uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+      const uint64_t P = v.codec == ZC_CODEC_RAW ? 4 * n : packed_bytes(n, v.width);
+      float* out = static_cast<float*>(p.out) + off / 4;
+      const uint64_t e0 = (nfull % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
+      for (uint64_t e = e0; e < e0 + 32 && e < n; ++e) {
+        int32_t sym;
+        if (v.codec == ZC_CODEC_RAW) {
+          sym = static_cast<int32_t>(stream_word<false>(payload, P, e));
+        } else {
+          const uint64_t bit = e * v.width;
+          const unsigned long long x = (static_cast<unsigned long long>(stream_word<false>(payload, P, bit / 32 + 1)) << 32) |
+                                       stream_word<false>(payload, P, bit / 32);
+          const uint32_t z = static_cast<uint32_t>((x >> (bit & 31)) & (v.width == 32 ? 0xffffffffull : ((1ull << v.width) - 1)));
+          sym = unzigzag32(z);
+        }
+        out[e] = __double2float_rn(__dmul_rn(p.scale, i2d(static_cast<uint32_t>(sym))));
+      }
+    }
+  }
+  if (lane == 0) tma::bulk_wait<0>();
+  __syncwarp();
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+// The fp32 source as a [rows][32] tensor of 4 KiB tiles (32 x 32, 128-byte swizzle).
+bool make_row_tensor_map(CUtensorMap* map, const void* base, uint64_t rows) {  // 4-byte elements
+  static EncodeTiled fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || f == nullptr)
+      return false;
+    fn = reinterpret_cast<EncodeTiled>(f);
+  }
+  const cuuint64_t dims[2] = {32, rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool fixed_path_ok(const EncParams& p) {
+  return p.src_kind == SRC_F32 && (reinterpret_cast<uintptr_t>(p.src) & 15u) == 0 && p.unit_bytes == ZC_BATCH_RAW_BYTES &&
+         p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook;
+}
+
+cudaError_t launch_fixed_range(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                               cudaStream_t s) {
+  BGeom g;
+  g.s_full = s_full;
+  g.total = total_slices;
+  note_launch();
+  range_kernel<<<static_cast<uint32_t>(std::min<uint64_t>(total_slices, 2ull * sms)), RT, 0, s>>>(
+      p, static_cast<BUnit*>(scratch), g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                              cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+    attr = true;
+  }
+  const uint64_t count = p.total_bytes / 4;
+  const uint64_t rows = count / 32;
+  // tiles of the message (the last unit's may be partial) and the full ones before it
+  const uint64_t last_n = (p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes) / 4;
+  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
+  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + last_n / TILE_ELEMS;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (rows > 0 && !make_row_tensor_map(&map, p.src, rows)) return cudaErrorInvalidValue;
+  BGeom g;
+  g.s_full = s_full;
+  g.total = total_slices;
+  const uint64_t want = (ntiles + ET_WARPS * CHUNK - 1) / (ET_WARPS * CHUNK);
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
+  note_launch();
+  emit_kernel<<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
+  return cudaGetLastError();
+}
+
+bool fixed_decode_ok(const DecParams& p) {
+  return !p.bare && p.out_kind == OUT_F32 && p.unit_bytes == ZC_BATCH_RAW_BYTES && (p.total_bytes % 4) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0 && (p.stride % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.stages) & 15u) == 0;
+}
+
+cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fl_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t count = p.total_bytes / 4;
+  const uint64_t rows = count / 32;
+  const uint64_t last_n = (p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes) / 4;
+  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
+  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + last_n / TILE_ELEMS;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (rows > 0 && !make_row_tensor_map(&map, p.out, rows)) return cudaErrorInvalidValue;
+  const uint64_t want = (ntiles + DT_WARPS * CHUNK - 1) / (DT_WARPS * CHUNK);
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
+  note_launch();
+  fl_decode_kernel<<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+  return cudaGetLastError();
+}
+
+void preload_fixed_kernels() {
+  cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, range_kernel);
+  cudaFuncSetAttribute(fl_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+  cudaGetLastError();
+}
+
+}  // namespace zc

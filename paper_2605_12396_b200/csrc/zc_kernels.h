@@ -101,6 +101,7 @@ struct DecParams {
   int bare;                // bare decode: `stages` is one payload and `hdr` describes it
   zc_frame_header hdr;
   int32_t* ok_out;         // bare decode result
+  int fast;                // zc_fixed.cu's decoder has handled the valid FixedLen / RAW units
 };
 
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
@@ -108,21 +109,19 @@ struct DecParams {
 void note_launch();
 
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
-// Batched send-mode encode (no ring, no embedded codebook) as a persistent task kernel;
-// `scratch` holds task_scratch_bytes(nunits) bytes of device memory (zeroed by the launcher).
-cudaError_t launch_encode_tasks(const EncParams& p, void* scratch, cudaStream_t s);
-size_t task_scratch_bytes(uint32_t nunits);
 // The default batched send path: profile -> scan -> emit streaming kernels (zc_batch.cu).
 cudaError_t launch_encode_batch(const EncParams& p, void* scratch, cudaStream_t s);
 size_t batch_scratch_bytes(uint32_t nunits);
 void preload_batch_kernels();
-// The same path with 64 KiB slices staged in shared memory by bulk copies (input read once);
-// used when the source is fp32 or symbol bytes, 16-byte aligned, with 64 KiB-multiple units.
-bool stream_encoder_ok(const EncParams& p);
-cudaError_t launch_encode_stream(const EncParams& p, void* scratch, cudaStream_t s);
-size_t stream_scratch_bytes(uint32_t nunits);
-void preload_stream_kernels();
-void preload_task_kernels();
+// zc_fixed.cu: the fp32 FixedLen / RAW units of the batched path (TMA-pipelined).
+bool fixed_path_ok(const EncParams& p);
+cudaError_t launch_fixed_range(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                               cudaStream_t s);
+cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                              cudaStream_t s);
+bool fixed_decode_ok(const DecParams& p);
+cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s);
+void preload_fixed_kernels();
 int encode_max_clusters();
 // Force module loading of every kernel (lazy loading may otherwise stall a launch behind a
 // running peer-waiting kernel).

@@ -112,6 +112,8 @@ def lib():
     _sig(L, "zc_decode_batches_sym", C.c_int, vp, u64, u64, vp, u64, vp, vp, vp, vp, vp)
     _sig(L, "zc_decode_batches_f32", C.c_int, vp, u64, u64, vp, u64, dbl, vp, vp, vp, vp, vp)
     _sig(L, "zc_decode_batches_add_sym", C.c_int, vp, u64, u64, vp, u64, vp, vp, vp, vp, vp)
+    _sig(L, "zc_codec_roundtrip_host_f32", C.c_int, vp, u64, dbl, vp, vp, u64, u64, i32, P(abi.TransportHint), vp,
+         P(abi.ArbConfig), vp, vp, vp, vp, u32, vp)
     _sig(L, "zc_comm_create", C.c_int, C.c_int, C.c_int, C.c_int, P(abi.CollectiveConfig), P(vp))
     _sig(L, "zc_comm_export_size", C.c_int)
     _sig(L, "zc_comm_export", C.c_int, vp, vp)

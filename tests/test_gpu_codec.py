@@ -384,3 +384,75 @@ def test_decode_fallback_on_corrupt_header(zc, port):
     assert cdc == -1 and int(codecs.item()) == -1
     have = len(frame) - 32  # min(dst, have) bytes are the payload region verbatim (collectives.cpp:330-336)
     assert np.array_equal(npy(out).view(np.uint8)[:have], exp[:have])
+
+
+# ------------------------------------------------------------------ fp32 fast path (zc_fixed.cu)
+@pytest.mark.parametrize("sigma,scale", [(0.0, 2e-4), (1e-4, 2e-4), (1.0, 2e-4), (3.0, 1e-3), (1.0, 1e-6),
+                                         (100.0, 1e-6), (150.0, 1e-6), (300.0, 1e-6)])
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_RAW])
+def test_fixed_path_widths_vs_oracle(zc, port, sigma, scale, pin):
+    """Every FixedLen width from 1 to 32 (and RAW) through the TMA emit / decode kernels, with
+    values placed on exact rounding ties and near the int32 limit, frames byte-compared with the
+    oracle and the decoded fp32 compared with dequantize_into."""
+    rng = np.random.default_rng(int(sigma * 7) + pin)
+    count = (6 << 20) // 4 + 1029  # one full unit, one ragged unit with a partial tile
+    x = (rng.normal(0, 1, count) * sigma).astype(np.float32)
+    k = rng.integers(-1000, 1000, 4096)
+    x[rng.integers(0, count, 4096)] = ((k + 0.5) * scale).astype(np.float32)  # ties (after fp32 rounding: near ties)
+    rc, sym = port.eb_quantize_f32(x, scale)
+    assert rc == 0
+    raw = sym.view(np.uint8)
+    hint = abi.make_hint()
+    fr = zc.encode_batches(t(x), pin, scale=scale, hint=hint)
+    exp = port.encode_batches(raw, pin, hint, None)
+    for b, (er, ef) in enumerate(exp):
+        r = fr.encode_results()[b]
+        assert (r.codec, r.payload_bytes, r.total_bytes) == (er.codec, er.payload_bytes, er.total_bytes)
+        assert np.array_equal(npy(fr.frame(b)), ef), f"frame {b}"
+    y = npy(zc.decode_batches(fr, None, scale=scale))
+    deq = np.zeros(count, np.float32)
+    port.lib.zo_dequantize_f32(sym, count, 0, scale, 0, deq)
+    assert np.array_equal(y, deq)
+    assert np.array_equal(npy(zc.decode_batches(fr, None)), sym)
+
+
+def test_fixed_path_matches_generic_kernels(zc, monkeypatch):
+    """The fast kernels and the generic batch kernels (ZC_NO_FIXED) produce identical frames."""
+    rng = np.random.default_rng(11)
+    x = rng.laplace(0, 1e-2, (9 << 20) // 4 + 5).astype(np.float32)
+    fast = zc.encode_batches(t(x), abi.PIN_AUTO, scale=2e-4)
+    monkeypatch.setenv("ZC_NO_FIXED", "1")
+    slow = zc.encode_batches(t(x), abi.PIN_AUTO, scale=2e-4)
+    ys = npy(zc.decode_batches(slow, None, scale=2e-4))
+    monkeypatch.delenv("ZC_NO_FIXED")
+    yf = npy(zc.decode_batches(fast, None, scale=2e-4))
+    for b in range(fast.nbatches):
+        assert np.array_equal(npy(fast.frame(b)), npy(slow.frame(b)))
+    assert np.array_equal(yf, ys)
+
+
+def test_codec_roundtrip_host_pipeline(zc):
+    """zc_codec_roundtrip_host_f32 (pinned host in -> frames -> pinned host out) equals the
+    device-resident encode + decode, frames included."""
+    import ctypes as C
+    L = zc.lib()
+    rng = np.random.default_rng(5)
+    count = (21 << 20) // 4 + 7
+    x = rng.normal(0, 1, count).astype(np.float32)
+    hx = torch.from_numpy(x).pin_memory()
+    hy = torch.empty(count, dtype=torch.float32).pin_memory()
+    work = torch.empty(count, dtype=torch.float32, device=DEV)
+    fr = zc.alloc_frames(count * 4, DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    hint, cfg = abi.make_hint(), zc.default_arb_config()
+    s = torch.cuda.current_stream()
+    zc.check(L.zc_codec_roundtrip_host_f32(hx.data_ptr(), count, 2e-4, zc._ptr(work), zc._ptr(fr.stages),
+                                           zc.STAGE_STRIDE, abi.STAGE_BANK_BYTES, abi.PIN_AUTO, C.byref(hint), None,
+                                           C.byref(cfg), zc._ptr(fr.results), zc._ptr(fr.index), zc._ptr(err),
+                                           hy.data_ptr(), 2, C.c_void_p(s.cuda_stream)))
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    ref = zc.encode_batches(t(x), abi.PIN_AUTO, scale=2e-4)
+    for b in range(ref.nbatches):
+        assert np.array_equal(npy(fr.frame(b)), npy(ref.frame(b)))
+    assert torch.equal(hy, zc.decode_batches(ref, None, scale=2e-4).cpu())

@@ -1,7 +1,7 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest.log
-for e in batch stream tasks; do ZC_ENCODER=$e timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$e.json 2> gpurun_out/bench_$e.err; done
+ZC_NO_FIXED=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_generic.json 2> gpurun_out/bench_generic.err
 timeout 300 python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_b.log 2>&1
 tail -3 gpurun_out/pytest.log
