@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(NT, 1) scan_kernel(const EncParams p, BUnit* u
     BUnit& U = us[u];
     const uint32_t target = target_codec(p, U, ctx_ok);
     if (target != ZC_CODEC_FIXEDLEN && target != ZC_CODEC_HUFFMAN) continue;  // RAW: decided in pass 3
-    if (g.fast && target == ZC_CODEC_FIXEDLEN) continue;                      // zc_fixed.cu's range pass
+    if (g.fast && target != ZC_CODEC_HUFFMAN) continue;                       // zc_fixed.cu's range pass
     const uint64_t R = unit_R(p, u);
     const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
     const uint64_t v0 = static_cast<uint64_t>(s) * BV;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(NT, 1) scan_kernel(const EncParams p, BUnit* u
       U.part[s].bits = hb;
       U.part[s].zero = zero;
       __threadfence();
-      if (atomicAdd(&U.scan_done, 1u) + 1 == unit_slices(p, u)) {
+      if (atomicAdd(g.fast ? &U.hdone : &U.scan_done, 1u) + 1 == unit_slices(p, u)) {
         __threadfence();
         decide_unit<SRC>(p, U, u, false, fast_ok, err);
       }
@@ -610,7 +610,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
   g.fast = (SRC == SRC_F32 && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
-  if (p.pin == ZC_PIN_AUTO) {
+  if (p.pin == ZC_PIN_AUTO && !g.fast) {
     note_launch();
     profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
   }
@@ -618,6 +618,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const bool huff_possible = (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_HUFFMAN) && ctx_ok_host;
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms)));
   if (g.fast) {
+    // the range kernel also profiles the window and plans (Auto): no separate profile launch
     if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN)
       if (cudaError_t e = launch_fixed_range(p, scratch, g.total, g.s_full, sms, s)) return e;
     if (huff_possible) {

@@ -25,7 +25,7 @@ struct BUnit {  // per unit, zeroed before every launch
   uint32_t edone, pdone;
   uint32_t whist[256];  // window histogram (pass 1, merged from PC CTAs)
   uint32_t wmz;         // window max zig-zag
-  uint32_t maxzz, bad, _q;
+  uint32_t maxzz, bad, hdone;  // hdone: Huffman bit-count slices (scan_kernel, fast mode)
   uint32_t fmin_c, fmax_k;           // fp32 range as order-preserving keys (min complemented)
   unsigned long long dmin_c, dmax_k;  // fp64 range, same encoding
   BPart part[BMAX];
@@ -36,7 +36,8 @@ struct BUnit {  // per unit, zeroed before every launch
 
 struct BGlobal {  // after the BUnit array in the scratch block (zeroed with it)
   uint32_t n_huff;  // units the selector planned as Huffman (Auto)
-  uint32_t pad[63];
+  uint32_t next_task;  // range kernel work counter (zc_fixed.cu)
+  uint32_t pad[62];
 };
 __device__ __forceinline__ BGlobal* bglobal(BUnit* us, uint32_t nunits) { return reinterpret_cast<BGlobal*>(us + nunits); }
 

@@ -46,15 +46,137 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   return r;
 }
 
-// ------------------------------------------------------------------ range
-__global__ void __launch_bounds__(RT, 2) range_kernel(const EncParams p, BUnit* us, BGeom g) {
+// ------------------------------------------------------------------ range (+ profile and plan)
+// Exact symbols of a 16-byte fp32 vector (fast path, exact division near a tie).
+__device__ __noinline__ uint32_t quantize_exact(float x, double scale, double rcp, uint32_t* err);
+__device__ __forceinline__ void quantize4(const float4& a, double scale, double rcp, uint32_t (&w)[4], uint32_t& err) {
+  const float f[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    bool slow = !(fabsf(f[k]) <= 3.402823466e38f);
+    const int32_t q = quantize_fast(static_cast<double>(f[k]), rcp, slow);
+    w[k] = slow ? quantize_exact(f[k], scale, rcp, &err) : static_cast<uint32_t>(q);
+  }
+}
+
+// profile_sample over the window (rea.cpp:93-118; the window is the unit's slice 0): byte
+// histogram in per-warp shared bins with warp-aggregated atomics (one atomic per distinct byte
+// value per warp instruction), max zig-zag over whole words; then the expected code length
+// under the shared context and arbitrate_plan (rea.cpp:145-176).  Whole CTA.
+struct ProfSmem {
+  uint32_t whist[RT / 32][256];
+  uint32_t hist[256];
+  uint8_t clens[256];
+  uint32_t wmz[RT / 32];
+};
+__device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uint32_t u, const float4* src, uint64_t R,
+                                               bool ctx_ok, ProfSmem& sm, uint32_t& err) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < (RT / 32) * 256; i += RT) (&sm.whist[0][0])[i] = 0;
+  for (int i = tid; i < 256; i += RT) sm.clens[i] = ctx_ok ? p.ctx->len[i] : 0;
+  __syncthreads();
+  const uint64_t W = R < kSampleWindow ? R : kSampleWindow;  // whole words: R % 4 == 0 for fp32
+  uint32_t wmz = 0;
+  for (uint64_t v0 = 0; v0 * 16 < W; v0 += RT) {
+    const uint64_t v = v0 + tid;
+    const bool in = v * 16 < W;
+    uint32_t w[4] = {0, 0, 0, 0};
+    uint32_t nb = 0;
+    if (in) {
+      nb = static_cast<uint32_t>(W - v * 16 < 16 ? W - v * 16 : 16);
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (nb == 16) {
+        a = __ldg(src + v);
+      } else {
+        const float* fs = reinterpret_cast<const float*>(src + v);
+        a.x = nb > 0 ? __ldg(fs) : 0.f;
+        a.y = nb > 4 ? __ldg(fs + 1) : 0.f;
+        a.z = nb > 8 ? __ldg(fs + 2) : 0.f;
+      }
+      quantize4(a, p.scale, p.rcp, w, err);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (static_cast<uint32_t>(k) < nb / 4) wmz = max(wmz, zigzag32(static_cast<int32_t>(w[k])));
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+      const bool act = in && j < nb;
+      const uint32_t byte = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+      const uint32_t key = act ? byte : 0x100u;  // inactive lanes group apart
+      const uint32_t peers = __match_any_sync(FULL, key);
+      if (act && (__ffs(peers) - 1) == lane) atomicAdd(&sm.whist[warp][byte], static_cast<uint32_t>(__popc(peers)));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) wmz = max(wmz, __shfl_xor_sync(FULL, wmz, o));
+  if (lane == 0) sm.wmz[warp] = wmz;
+  __syncthreads();
+  for (int i = tid; i < 256; i += RT) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < RT / 32; ++w2) c += sm.whist[w2][i];
+    sm.hist[i] = c;
+  }
+  __syncthreads();
+  double el = 0.0;
+  bool el_ok = false;
+  if (warp == 0) el_ok = ctx_ok && warp_mean_len(sm.hist, sm.clens, el);
+  if (p.stats != nullptr)
+    for (int i = tid; i < 256; i += RT) p.stats[u].hist[i] = sm.hist[i];
+  if (tid == 0) {
+    zc_sample_stats st;
+    st.sampled_bytes = W;
+    uint32_t m = 0;
+    for (int i = 0; i < RT / 32; ++i) m = max(m, sm.wmz[i]);
+    st.max_zigzag = m;
+    st.ctx_code_len_bits = el_ok ? el : 0.0;
+    st.ctx_code_len_valid = el_ok ? 1u : 0u;
+    st.self_code_len_bits = 0.0;
+    st.self_code_len_valid = 0u;  // only read with embedded codebooks (not on this path)
+    if (p.stats != nullptr) {
+      zc_sample_stats* o = p.stats + u;
+      o->sampled_bytes = st.sampled_bytes;
+      o->max_zigzag = st.max_zigzag;
+      o->ctx_code_len_bits = st.ctx_code_len_bits;
+      o->self_code_len_bits = 0.0;
+      o->ctx_code_len_valid = st.ctx_code_len_valid;
+      o->self_code_len_valid = 0u;
+    }
+    const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
+    U.plan = arbitrate_plan(R, pcap, st, p.hint, ctx_ok, p.cfg).choice;
+  }
+}
+
+// One HBM stream over the units that may end up FixedLen: fp32 min / max (NaN-propagating) per
+// unit.  Work is claimed dynamically: in Auto the first nunits tasks profile each unit's window
+// and store its plan (window_profile), the rest are runs of RCH consecutive 64 KiB slices.  A unit
+// is complete when its slices and (Auto) its profile have been counted; the task that completes
+// it decides FixedLen units (decide_unit).  Huffman-planned units are decided by scan_kernel's
+// bit counts, RAW ones by emit.
+constexpr uint32_t RCH = 8;
+
+__global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ EncParams p, BUnit* us, BGeom g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float s_mn[RT / 32], s_mx[RT / 32];
+  __shared__ ProfSmem s_prof;
+  __shared__ uint32_t s_task;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
+  const bool automode = p.pin == ZC_PIN_AUTO;
+  const uint32_t nprof = automode ? p.nunits : 0u;
+  const uint64_t nchunks = (g.total + RCH - 1) / RCH;
+  BGlobal* gl = bglobal(us, p.nunits);
   uint32_t err = 0;
-  const uint64_t t0 = g.total * blockIdx.x / gridDim.x, t1 = g.total * (blockIdx.x + 1) / gridDim.x;
   float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
   uint32_t run_u = 0xffffffffu, run_n = 0;
+  // counts `n` finished pieces of unit u (thread 0); the completing one decides
+  auto finish = [&](BUnit& U, uint32_t u, uint32_t n) {
+    __threadfence();
+    if (atomicAdd(&U.scan_done, n) + n == unit_slices(p, u) + (automode ? 1u : 0u)) {
+      __threadfence();
+      const uint32_t plan = *reinterpret_cast<volatile uint32_t*>(&U.plan);
+      if (plan == ZC_CODEC_HUFFMAN && automode) atomicAdd(&gl->n_huff, 1u);
+      if (target_codec(p, U, ctx_ok) == ZC_CODEC_FIXEDLEN) decide_unit<SRC_F32>(p, U, u, true, true, err);
+    }
+  };
   auto flush = [&]() {
     for (int o = 16; o > 0; o >>= 1) {
       mn = fmin_nan(mn, __shfl_xor_sync(FULL, mn, o));
@@ -76,54 +198,73 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const EncParams p, BUnit* 
       if (bad) atomicOr(&U.bad, 1u);
       atomicMax(&U.fmin_c, ~fkey(mn));
       atomicMax(&U.fmax_k, fkey(mx));
-      __threadfence();
-      if (atomicAdd(&U.scan_done, run_n) + run_n == unit_slices(p, run_u)) {
-        __threadfence();
-        decide_unit<SRC_F32>(p, U, run_u, true, true, err);
-      }
+      finish(U, run_u, run_n);
     }
     mn = __int_as_float(0x7f800000);
     mx = -__int_as_float(0x7f800000);
     run_n = 0;
   };
-  for (uint64_t t = t0; t < t1; ++t) {
-    uint32_t u, s;
-    g.unit_of(t, p.nunits, u, s);
-    if (target_codec(p, us[u], ctx_ok) != ZC_CODEC_FIXEDLEN) continue;
-    if (run_n && run_u != u) flush();
-    run_u = u;
-    ++run_n;
-    const uint64_t R = unit_R(p, u);
-    const uint64_t nf = R / 16;  // whole 16-byte vectors of the unit
-    const uint64_t v0 = static_cast<uint64_t>(s) * BV;
-    const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
-    if (v0 + BV <= nf) {
-      const float4* q = src + v0 + tid;
-      float4 a[BV / RT];
-#pragma unroll
-      for (int k = 0; k < static_cast<int>(BV / RT); ++k) a[k] = __ldg(q + k * RT);
-#pragma unroll
-      for (int k = 0; k < static_cast<int>(BV / RT); ++k) {
-        mn = fmin_nan(mn, fmin_nan(fmin_nan(a[k].x, a[k].y), fmin_nan(a[k].z, a[k].w)));
-        mx = fmax_nan(mx, fmax_nan(fmax_nan(a[k].x, a[k].y), fmax_nan(a[k].z, a[k].w)));
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_task = atomicAdd(&gl->next_task, 1u);
+    __syncthreads();
+    const uint32_t task = s_task;
+    if (task < nprof) {  // profile + plan of unit `task`
+      const uint32_t u = task;
+      const uint64_t R = unit_R(p, u);
+      if (R <= p.cfg.small_batch_threshold_bytes || p.stage_len <= kHeaderBytes) {
+        if (tid == 0) us[u].plan = ZC_CODEC_RAW;
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
+        window_profile(p, us[u], u, src, R, ctx_ok, s_prof, err);
       }
-    } else {
-      const uint64_t v1 = min(v0 + BV, nf);
-      for (uint64_t v = v0 + tid; v < v1; v += RT) {
-        const float4 a = __ldg(src + v);
-        mn = fmin_nan(mn, fmin_nan(fmin_nan(a.x, a.y), fmin_nan(a.z, a.w)));
-        mx = fmax_nan(mx, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
-      }
-      if (tid == 0 && v0 * 16 + BS >= R) {  // the unit's last 0..3 elements
-        const float* f = reinterpret_cast<const float*>(src);
-        for (uint64_t e = nf * 4; e < R / 4; ++e) {
-          mn = fmin_nan(mn, __ldg(f + e));
-          mx = fmax_nan(mx, __ldg(f + e));
+      __syncthreads();
+      if (tid == 0) finish(us[u], u, 1u);
+      continue;
+    }
+    const uint64_t ch = task - nprof;
+    if (ch >= nchunks) break;
+    const uint64_t te = min(g.total, (ch + 1) * RCH);
+    for (uint64_t t = ch * RCH; t < te; ++t) {
+      uint32_t u, s;
+      g.unit_of(t, p.nunits, u, s);
+      // Auto: every slice (the plan may not be known yet); FixedLen pin: FixedLen targets only
+      if (!automode && target_codec(p, us[u], ctx_ok) != ZC_CODEC_FIXEDLEN) continue;
+      if (run_n && run_u != u) flush();
+      run_u = u;
+      ++run_n;
+      const uint64_t R = unit_R(p, u);
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
+      const uint64_t nf = R / 16;  // whole 16-byte vectors of the unit
+      const uint64_t v0 = static_cast<uint64_t>(s) * BV;
+      if (v0 + BV <= nf) {
+        const float4* q = src + v0 + tid;
+        float4 a[BV / RT];
+#pragma unroll
+        for (int k = 0; k < static_cast<int>(BV / RT); ++k) a[k] = __ldg(q + k * RT);
+#pragma unroll
+        for (int k = 0; k < static_cast<int>(BV / RT); ++k) {
+          mn = fmin_nan(mn, fmin_nan(fmin_nan(a[k].x, a[k].y), fmin_nan(a[k].z, a[k].w)));
+          mx = fmax_nan(mx, fmax_nan(fmax_nan(a[k].x, a[k].y), fmax_nan(a[k].z, a[k].w)));
+        }
+      } else {
+        const uint64_t v1 = min(v0 + BV, nf);
+        for (uint64_t v = v0 + tid; v < v1; v += RT) {
+          const float4 a = __ldg(src + v);
+          mn = fmin_nan(mn, fmin_nan(fmin_nan(a.x, a.y), fmin_nan(a.z, a.w)));
+          mx = fmax_nan(mx, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+        }
+        if (tid == 0 && v0 * 16 + BS >= R) {  // the unit's last 0..3 elements
+          const float* fl = reinterpret_cast<const float*>(src);
+          for (uint64_t e = nf * 4; e < R / 4; ++e) {
+            mn = fmin_nan(mn, __ldg(fl + e));
+            mx = fmax_nan(mx, __ldg(fl + e));
+          }
         }
       }
     }
+    if (run_n) flush();  // a run never outlives its task: units are counted task by task
   }
-  if (run_n) flush();
   err = __reduce_or_sync(FULL, err);
   if (lane == 0 && err && p.err) atomicOr(p.err, err);
 }
@@ -371,18 +512,20 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
 
 // ------------------------------------------------------------------ decode (FixedLen / RAW -> fp32)
 // recv_batch's decode dispatch (collectives.cpp:314-336) for valid FixedLen and RAW frames fused
-// with dequantize_into (quant.cpp:107-127) into fp32: lane L reads the W payload words of row L
-// (its 32 symbols) straight from HBM — the next row's words are in flight while this one is
-// unpacked with compile-time shifts — and writes its 32 floats into a 128-byte-swizzled 4 KiB
-// tile that one TMA tensor store (cp.async.bulk.tensor) moves to HBM.  Everything else (Huffman,
-// the raw-copy fallback, other sinks) stays on zc_decode.cu's kernels, which skip these units.
+// with dequantize_into (quant.cpp:107-127) into fp32.  Per warp, a ring of STAGES 4 KiB shared
+// buffers: a 1-D bulk copy (TMA) brings a tile's packed rows (32 x W words) in, lane L reads the W
+// words of row L (its 32 symbols), unpacks them with compile-time shifts, writes its 32 floats
+// back into the same buffer in the 128-byte-swizzled layout, and one TMA tensor store moves the
+// 4 KiB tile to HBM.  Loads run STAGES-1 tiles ahead.  Everything else (Huffman, the raw-copy
+// fallback, other sinks) stays on zc_decode.cu's kernels, which skip these units.
 constexpr int DT_WARPS = 16;
 constexpr int DT = DT_WARPS * 32;
-constexpr size_t DEC_SMEM = static_cast<size_t>(DT_WARPS) * 2 * TILE_BYTES + 1024;
+constexpr int DSTAGES = 3;
+constexpr size_t DEC_SMEM = static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES + 1024 + DT_WARPS * DSTAGES * 8;
 
 struct DecView {
   uint32_t codec;  // ZC_CODEC_RAW / ZC_CODEC_FIXEDLEN when this kernel owns the unit, else kFallback
-  uint32_t width;  // FixedLen width; 0 for RAW
+  uint32_t width;  // FixedLen width; 32 for RAW (the row's words are the symbols)
 };
 
 __device__ __forceinline__ DecView dec_view(const DecParams& p, uint32_t u) {
@@ -393,34 +536,8 @@ __device__ __forceinline__ DecView dec_view(const DecParams& p, uint32_t u) {
                      R, nullptr, false, p.ctx, p.index != nullptr, fc);
   DecView v;
   v.codec = (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN) ? fc.codec : kFallback;
-  v.width = fc.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(fc.h.params) : 0u;
+  v.width = fc.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(fc.h.params) : 32u;
   return v;
-}
-
-// W words of row `row` (W = 32 and kRaw: the symbols themselves).
-template <int W>
-__device__ __forceinline__ void load_row_words(const uint32_t* payload, uint64_t row, uint32_t (&a)[W]) {
-  const uint32_t* s = payload + row * W;
-  if (W % 4 == 0) {
-#pragma unroll
-    for (int j = 0; j < W / 4; ++j) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(s) + j);
-      a[4 * j] = q.x;
-      a[4 * j + 1] = q.y;
-      a[4 * j + 2] = q.z;
-      a[4 * j + 3] = q.w;
-    }
-  } else if (W % 2 == 0) {
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-      const uint2 q = __ldg(reinterpret_cast<const uint2*>(s) + j);
-      a[2 * j] = q.x;
-      a[2 * j + 1] = q.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < W; ++j) a[j] = __ldg(s + j);
-  }
 }
 
 // Symbol i (0..31) of a row packed at width W (fixedlen.cpp:49-63), un-zig-zagged.
@@ -439,8 +556,26 @@ __device__ __forceinline__ int32_t row_symbol(const uint32_t (&a)[W], int i) {
   return unzigzag32(z);
 }
 
+// One tile in shared memory: packed rows in, swizzled fp32 tile out (same buffer).
 template <int W, bool kRaw>
-__device__ __forceinline__ void dequant_row_to_tile(const uint32_t (&a)[W], double scale, uint8_t* tile, int lane) {
+__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, int lane) {
+  uint32_t a[W];
+  const uint32_t row = buf + lane * W * 4;
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a[4 * j]), "=r"(a[4 * j + 1]), "=r"(a[4 * j + 2]), "=r"(a[4 * j + 3])
+                   : "r"(row + 16 * j));
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j)
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a[2 * j]), "=r"(a[2 * j + 1]) : "r"(row + 8 * j));
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[j]) : "r"(row + 4 * j));
+  }
+  __syncwarp();  // every lane holds its row before the floats overwrite the buffer
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     float f[4];
@@ -449,23 +584,42 @@ __device__ __forceinline__ void dequant_row_to_tile(const uint32_t (&a)[W], doub
       const int32_t sym = row_symbol<W, kRaw>(a, 4 * m + q);
       f[q] = __double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym))));
     }
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(tma::smem_u32(tile) + lane * 128 + ((m ^ (lane & 7)) << 4)),
-                 "f"(f[0]), "f"(f[1]), "f"(f[2]), "f"(f[3])
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)), "f"(f[0]),
+                 "f"(f[1]), "f"(f[2]), "f"(f[3])
                  : "memory");
   }
 }
 
-struct DecSeq {  // the warp's tile sequence over owned units
-  const DecParams* p;
+__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, int lane) {
+  if (v.codec == ZC_CODEC_RAW) {
+    decode_tile_smem<32, true>(buf, scale, lane);
+    return;
+  }
+  switch (v.width) {
+#define ZC_DC(W)                                  \
+  case W:                                         \
+    decode_tile_smem<W, false>(buf, scale, lane); \
+    break;
+    ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
+    ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
+    ZC_DC(22) ZC_DC(23) ZC_DC(24) ZC_DC(25) ZC_DC(26) ZC_DC(27) ZC_DC(28) ZC_DC(29) ZC_DC(30) ZC_DC(31)
+    ZC_DC(32)
+#undef ZC_DC
+    default:
+      break;
+  }
+}
+
+struct DecSeq {  // a warp's tile sequence over owned units, with the view of the current unit
   uint64_t nfull, tw;
   uint32_t cu;
   DecView cv;
-  __device__ __forceinline__ uint64_t next(uint64_t c) {
+  __device__ __forceinline__ uint64_t next(const DecParams& p, uint64_t c) {
     while (c < nfull) {
       const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
       if (u != cu) {
         cu = u;
-        cv = dec_view(*p, u);
+        cv = dec_view(p, u);
       }
       if (cv.codec != kFallback) return c;
       c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
@@ -474,90 +628,67 @@ struct DecSeq {  // the warp's tile sequence over owned units
   }
 };
 
-// Runs the warp's tiles c, tile_adv(c), ... while they stay below `end` (the unit's last full tile or
-// the message's); returns the first tile past them and the updated store counter.  Out of line
-// per width: the row arrays live in registers, and all arguments are scalars.
-struct DecStep {
-  uint64_t c;
-  uint32_t k;
-};
-template <int W, bool kRaw>
-__device__ __noinline__ DecStep decode_unit_tiles(const uint32_t* payload, uint64_t c, uint64_t end, uint64_t tw,
-                                                  double scale, const CUtensorMap* tmap, uint8_t* bufs, uint32_t k,
-                                                  int lane) {
-  uint32_t a[W], b[W];
-  load_row_words<W>(payload, (c % UNIT_TILES) * 32 + lane, a);
-  for (;;) {
-    const uint64_t cn = tile_adv(c, tw);
-    const bool more = cn < end;
-    if (more) load_row_words<W>(payload, (cn % UNIT_TILES) * 32 + lane, b);
-    uint8_t* tile = bufs + (k & 1) * TILE_BYTES;
-    if (lane == 0) tma::bulk_wait_read<1>();  // the store issued from this buffer two tiles ago
-    __syncwarp();
-    dequant_row_to_tile<W, kRaw>(a, scale, tile, lane);
-    tma::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma::store_2d(tmap, tile, 0, static_cast<int32_t>(c * 32));
-      tma::bulk_commit();
-    }
-    ++k;
-    if (!more) return DecStep{cn, k};
-    c = cn;
-#pragma unroll
-    for (int j = 0; j < W; ++j) a[j] = b[j];
-  }
-}
-
-__global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant__ DecParams p, const __grid_constant__ CUtensorMap tmap,
-                                                          uint64_t ntiles, uint64_t nfull) {
+__global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant__ DecParams p,
+                                                          const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
+                                                          uint64_t nfull) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
   uint8_t* s_tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint8_t* bufs = s_tiles + static_cast<size_t>(warp) * 2 * TILE_BYTES;
-  uint32_t err = 0;
+  uint8_t* my = s_tiles + static_cast<size_t>(warp) * DSTAGES * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES) + warp * DSTAGES;
+  const double scale = p.scale;
   // decoded codec per owned unit (recv_batch's dispatch result)
   for (uint32_t u = blockIdx.x * DT + tid; u < p.nunits; u += gridDim.x * DT) {
     const DecView v = dec_view(p, u);
     if (v.codec != kFallback && p.codec_out) p.codec_out[u] = v.codec;
   }
-  DecSeq seq;
-  seq.p = &p;
-  seq.nfull = nfull;
-  seq.tw = static_cast<uint64_t>(gridDim.x) * DT_WARPS;
-  seq.cu = 0xffffffffu;
+  if (lane == 0) {
+    for (int i = 0; i < DSTAGES; ++i) tma::mbar_init(&bars[i], 1);
+    tma::fence_barrier_init();
+  }
+  __syncwarp();
+  const uint64_t tw = static_cast<uint64_t>(gridDim.x) * DT_WARPS;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * DT_WARPS + warp;
-  uint32_t k = 0;
-  uint64_t c = seq.next(gw * CHUNK);
-  while (c < nfull) {
-    const DecView v = seq.cv;  // view of c's unit (seq.next just returned c)
+  DecSeq iss{nfull, tw, 0xffffffffu, {kFallback, 0}}, prc{nfull, tw, 0xffffffffu, {kFallback, 0}};
+  auto issue = [&](uint32_t st, uint64_t c) {  // lane 0: the packed rows of tile c into stage st
     const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
-    const uint64_t ue = static_cast<uint64_t>(u + 1) * UNIT_TILES;
-    const uint64_t end = ue < nfull ? ue : nfull;
-    const uint32_t* payload = reinterpret_cast<const uint32_t*>(p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes);
-    DecStep st{nfull, k};
-    if (v.codec == ZC_CODEC_RAW) {
-      st = decode_unit_tiles<32, true>(payload, c, end, seq.tw, p.scale, &tmap, bufs, k, lane);
-    } else {
-      switch (v.width) {
-#define ZC_DC(W)                                                                                \
-  case W:                                                                                       \
-    st = decode_unit_tiles<W, false>(payload, c, end, seq.tw, p.scale, &tmap, bufs, k, lane); \
-    break;
-        ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
-        ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
-        ZC_DC(22) ZC_DC(23) ZC_DC(24) ZC_DC(25) ZC_DC(26) ZC_DC(27) ZC_DC(28) ZC_DC(29) ZC_DC(30) ZC_DC(31)
-        ZC_DC(32)
-#undef ZC_DC
-        default:
-          break;
-      }
+    const uint32_t bytes = 128u * iss.cv.width;
+    const uint8_t* src = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes + (c % UNIT_TILES) * bytes;
+    tma::mbar_arrive_expect_tx(&bars[st], bytes);
+    tma::load_1d(my + st * TILE_BYTES, src, bytes, &bars[st]);
+  };
+  uint64_t c_issue = iss.next(p, gw * CHUNK);
+  for (int i = 0; i < DSTAGES - 1; ++i) {
+    if (c_issue < nfull) {
+      if (lane == 0) issue(i, c_issue);
+      c_issue = iss.next(p, tile_adv(c_issue, tw));
     }
-    k = st.k;
-    c = seq.next(st.c);
+  }
+  uint32_t k = 0;
+  for (uint64_t c = prc.next(p, gw * CHUNK); c < nfull; c = prc.next(p, tile_adv(c, tw)), ++k) {
+    const uint32_t st = k % DSTAGES;
+    // refill the stage that tile k-1 used once its store has read the buffer (the ring keeps
+    // DSTAGES-1 loads in flight while this tile is decoded)
+    if (c_issue < nfull) {
+      const uint32_t rs = (k + DSTAGES - 1) % DSTAGES;
+      if (lane == 0) {
+        tma::bulk_wait_read<0>();
+        issue(rs, c_issue);
+      }
+      c_issue = iss.next(p, tile_adv(c_issue, tw));
+    }
+    tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
+    const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
+    decode_tile_dispatch(prc.cv, buf, scale, lane);
+    tma::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma::store_2d(&tmap, my + st * TILE_BYTES, 0, static_cast<int32_t>(c * 32));
+      tma::bulk_commit();
+    }
   }
   // the message's last, partial tile: symbol by symbol with byte-exact bounds
-  if (nfull < ntiles && gw == (nfull / CHUNK) % seq.tw) {
+  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
     const uint32_t u = static_cast<uint32_t>(nfull / UNIT_TILES);
     const DecView v = dec_view(p, u);
     if (v.codec != kFallback) {
@@ -584,7 +715,6 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   }
   if (lane == 0) tma::bulk_wait<0>();
   __syncwarp();
-  if (lane == 0 && err && p.err) atomicOr(p.err, err);
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
