@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(NT, 1) emit_kernel(const EncParams p, BUnit* u
       P = U.payload;
       if (codec == ZC_CODEC_RAW && R > pcap) codec = CODEC_NONE;
     }
-    if (g.fast && codec != ZC_CODEC_HUFFMAN) continue;  // zc_fixed.cu's emit owns RAW / FixedLen / failures
+    if (g.fast && target != ZC_CODEC_HUFFMAN) continue;  // zc_fixed.cu owns the RAW / FixedLen targets
     if (codec == CODEC_NONE) {
       if (s == 0) err |= ZC_DERR_CAPACITY;
     } else if (codec == ZC_CODEC_RAW) {

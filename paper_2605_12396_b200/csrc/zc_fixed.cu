@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "zc_batch.cuh"
@@ -288,9 +289,11 @@ __device__ __forceinline__ void quantize_row(const float (&x)[32], double scale,
   uint32_t rm = 0;  // max over the row of the high word of |r|, r = q - round(q)
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    const double q = __dmul_rn(static_cast<double>(x[i]), rcp);
-    const double t = __dadd_rn(q, kMagic);
-    const double r = __dsub_rn(q, __dsub_rn(t, kMagic));
+    // t = RN(x*rcp + M): the nearest integer to x*rcp in its low word; r = RN(x*rcp - k) is the
+    // residual to that integer (one rounding), so |x/scale - k| <= |r| + 2^-22 for |q| < 2^30
+    const double xd = static_cast<double>(x[i]);
+    const double t = __fma_rn(xd, rcp, kMagic);
+    const double r = __fma_rn(xd, rcp, -__dsub_rn(t, kMagic));
     rm = max(rm, static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu);
     s[i] = static_cast<uint32_t>(__double2loint(t));
   }
@@ -813,6 +816,7 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
   fl_decode_kernel<<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
   return cudaGetLastError();
 }
+
 
 void preload_fixed_kernels() {
   cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
