@@ -204,7 +204,7 @@ def codec_bench(args):
         zcomm.check(L.zc_codec_roundtrip_host_f32(hx.data_ptr(), count, SCALE, P(work), P(fr.stages),
                                                   zcomm.STAGE_STRIDE, abi.STAGE_BANK_BYTES, abi.PIN_AUTO,
                                                   C.byref(hint), ctx.handle, C.byref(cfg), P(fr.results),
-                                                  P(fr.index), P(err), hy.data_ptr(), 2, s))
+                                                  P(fr.index), P(err), hy.data_ptr(), 8, s))
 
     for _ in range(args.warmup):
         e2e_step()

@@ -41,7 +41,7 @@ extern "C" {
 #define ZC_SLOTS_PER_CHANNEL 8u
 #define ZC_BATCH_RAW_BYTES (ZC_SLOT_BYTES * ZC_SLOTS_PER_CHANNEL)
 #define ZC_STAGE_BANK_BYTES (ZC_HEADER_BYTES + ZC_BATCH_RAW_BYTES)
-#define ZC_STAGE_BANKS 2u
+#define ZC_STAGE_BANKS 8u
 #define ZC_SAMPLE_WINDOW_BYTES 65536ull
 #define ZC_HUFF_MAX_CODE_LEN 32u
 #define ZC_HUFF_CODEBOOK_BYTES 256u
@@ -308,7 +308,7 @@ int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stage_stride, ui
  * RankCtx::send_encoded + recv_decoded make on host spans.  h_x (host fp32; pinned for overlap) -> H2D ->
  * fused quantize+encode (frames land in d_stages / d_results / d_index exactly as zc_encode_batches_f32
  * writes them) -> decode+dequantize -> D2H -> h_y.  Pipelined in groups of `group_batches` 4 MiB batches
- * (0 = 2) over internal streams so H2D, kernels and D2H overlap; ordered after earlier work on `stream`,
+ * (0 = 4) over internal H2D / kernel / D2H streams so both copy directions and the kernels overlap; ordered after earlier work on `stream`,
  * and later work on `stream` waits for it.  d_work: count floats of device scratch (16-byte aligned). */
 int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, double scale, float* d_work, uint8_t* d_stages,
                                 uint64_t stage_stride, uint64_t stage_len, int32_t pin,

@@ -692,15 +692,15 @@ int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stride, uint64_t
 }  // extern "C"
 
 // ------------------------------------------------------------------ host-buffer pipelines
-// Internal copy/compute streams per device: group g of a host-buffer call runs on stream g % kPipe,
-// so H2D of one group, the kernels of another and D2H of a third overlap (separate copy engines,
-// PCIe full duplex).  Each internal stream has its own encode/decode scratch (scratch_for).
+// Three internal streams per device — H2D copies, kernels, D2H copies — chained per group by
+// events, so the copy engines stream back to back in both directions (PCIe is full duplex) while
+// the kernels of group g run between H2D(g) and D2H(g).  Each stream has its own scratch.
 namespace {
-constexpr int kPipe = 3;
+constexpr int kEv = 4;
 struct Pipe {
-  cudaStream_t s[kPipe] = {};
-  cudaEvent_t done[kPipe] = {};
-  cudaEvent_t start = nullptr;
+  cudaStream_t h2d = nullptr, work = nullptr, d2h = nullptr;
+  cudaEvent_t in[kEv] = {}, done[kEv] = {};
+  cudaEvent_t start = nullptr, fin_work = nullptr, fin_d2h = nullptr;
   bool ok = false;
 };
 std::mutex g_pipe_mu;
@@ -712,11 +712,14 @@ Pipe* pipe_for_device() {
   std::lock_guard<std::mutex> g(g_pipe_mu);
   Pipe& pp = g_pipes[dev];
   if (!pp.ok) {
-    for (int i = 0; i < kPipe; ++i) {
-      if (cudaStreamCreateWithFlags(&pp.s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-      if (cudaEventCreateWithFlags(&pp.done[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    }
-    if (cudaEventCreateWithFlags(&pp.start, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    for (cudaStream_t* s : {&pp.h2d, &pp.work, &pp.d2h})
+      if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (int i = 0; i < kEv; ++i)
+      if (cudaEventCreateWithFlags(&pp.in[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pp.done[i], cudaEventDisableTiming) != cudaSuccess)
+        return nullptr;
+    for (cudaEvent_t* e : {&pp.start, &pp.fin_work, &pp.fin_d2h})
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
     pp.ok = true;
   }
   return &pp;
@@ -737,31 +740,34 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
   const cudaStream_t caller = static_cast<cudaStream_t>(stream);
   const uint64_t per = ZC_BATCH_RAW_BYTES / 4;  // elements per batch
   const uint64_t nb = (count + per - 1) / per;
-  const uint64_t gb = group_batches ? group_batches : 2;
+  const uint64_t gb = group_batches ? group_batches : 4;
   const uint64_t ngroups = (nb + gb - 1) / gb;
   if (int rc = cuda_err(cudaEventRecord(pp->start, caller), "pipeline start")) return rc;
-  for (int i = 0; i < kPipe; ++i)
-    if (int rc = cuda_err(cudaStreamWaitEvent(pp->s[i], pp->start, 0), "pipeline wait")) return rc;
+  for (cudaStream_t s : {pp->h2d, pp->work, pp->d2h})
+    if (int rc = cuda_err(cudaStreamWaitEvent(s, pp->start, 0), "pipeline wait")) return rc;
   for (uint64_t g = 0; g < ngroups; ++g) {
-    const cudaStream_t s = pp->s[g % kPipe];
     const uint64_t b0 = g * gb;
     const uint64_t e0 = b0 * per;
     const uint64_t n = (count - e0) < gb * per ? (count - e0) : gb * per;
-    if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, s), "H2D")) return rc;
+    cudaEvent_t in = pp->in[g % kEv], done = pp->done[g % kEv];
+    if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, pp->h2d), "H2D")) return rc;
+    if (int rc = cuda_err(cudaEventRecord(in, pp->h2d), "H2D event")) return rc;
+    if (int rc = cuda_err(cudaStreamWaitEvent(pp->work, in, 0), "H2D wait")) return rc;
     if (int rc = encode_batches(d_work + e0, SRC_F32, n * 4, scale, d_stages + b0 * stride, stride, stage_len, pin, hint,
                                 ctx, cfg, d_results + b0, d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr,
-                                d_err, s))
+                                d_err, pp->work))
       return rc;
     // decoded in place: the group's encode has consumed its input (stream order)
     if (int rc = decode_batches(d_stages + b0 * stride, stride, stage_len, d_results + b0, n * 4, ctx,
                                 d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr, OUT_F32, d_work + e0, scale,
-                                nullptr, d_err, s))
+                                nullptr, d_err, pp->work))
       return rc;
-    if (int rc = cuda_err(cudaMemcpyAsync(h_y + e0, d_work + e0, n * 4, cudaMemcpyDeviceToHost, s), "D2H")) return rc;
+    if (int rc = cuda_err(cudaEventRecord(done, pp->work), "kernel event")) return rc;
+    if (int rc = cuda_err(cudaStreamWaitEvent(pp->d2h, done, 0), "kernel wait")) return rc;
+    if (int rc = cuda_err(cudaMemcpyAsync(h_y + e0, d_work + e0, n * 4, cudaMemcpyDeviceToHost, pp->d2h), "D2H")) return rc;
   }
-  for (int i = 0; i < kPipe; ++i) {
-    if (int rc = cuda_err(cudaEventRecord(pp->done[i], pp->s[i]), "pipeline done")) return rc;
-    if (int rc = cuda_err(cudaStreamWaitEvent(caller, pp->done[i], 0), "pipeline join")) return rc;
-  }
-  return ZC_OK;
+  if (int rc = cuda_err(cudaEventRecord(pp->fin_work, pp->work), "pipeline done")) return rc;
+  if (int rc = cuda_err(cudaEventRecord(pp->fin_d2h, pp->d2h), "pipeline done")) return rc;
+  if (int rc = cuda_err(cudaStreamWaitEvent(caller, pp->fin_work, 0), "pipeline join")) return rc;
+  return cuda_err(cudaStreamWaitEvent(caller, pp->fin_d2h, 0), "pipeline join");
 }

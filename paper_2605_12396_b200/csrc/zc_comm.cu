@@ -280,6 +280,7 @@ struct zc_comm {
   int rank = 0, nranks = 1, device = 0;
   zc_collective_config cfg{};
   cudaStream_t stream = nullptr;
+  cudaEvent_t ev_in = nullptr;  // orders the collective after the caller's stream
   Layout lay{};
   uint8_t* block = nullptr;
   std::vector<uint8_t*> peer;      // every rank's block base, valid on this device
@@ -302,6 +303,15 @@ struct zc_comm {
 namespace {
 
 int dev_guard(zc_comm* c) { return cuda_err(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// The collective runs on the communicator's own stream, after all work already queued on the
+// caller's stream (NULL = the legacy default stream): inputs produced there are complete.
+int order_after(zc_comm* c, void* stream) {
+  if (c->ev_in == nullptr)
+    if (int rc = cuda_err(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming), "event")) return rc;
+  if (int rc = cuda_err(cudaEventRecord(c->ev_in, static_cast<cudaStream_t>(stream)), "event record")) return rc;
+  return cuda_err(cudaStreamWaitEvent(c->stream, c->ev_in, 0), "stream wait");
+}
 
 Link make_link(zc_comm* c) {
   Link L;
@@ -691,6 +701,7 @@ void zc_comm_destroy(zc_comm* c) {
   if (c->sym) cudaFree(c->sym);
   if (c->block) cudaFree(c->block);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->shared) zc_huff_ctx_destroy(c->shared);
   delete c;
 }
@@ -713,8 +724,8 @@ int zc_comm_set_shared_huffman(zc_comm* c, const zc_huff_ctx* ctx) {
 
 int zc_comm_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int32_t mode, double* h_scale, uint32_t levels,
                           void* stream) {
-  (void)stream;
   if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
   if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
   if (int rc = enqueue_allreduce_sym(c, d_sym, count, mode, *h_scale, levels)) return rc;
   int rc = finish(c);
@@ -724,32 +735,32 @@ int zc_comm_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int32_t mo
 
 int zc_comm_allreduce_eb_f32(zc_comm* c, const float* d_x, void* d_out, int32_t out_f64, uint64_t count, double rel,
                              void* stream) {
-  (void)stream;
   if (!(rel > 0.0) || rel > 1.0) return set_err(ZC_ERR_INVALID_ARGUMENT, "eb_quantize: rel must be in (0, 1]");
   if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
   if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
   if (int rc = enqueue_allreduce_eb(c, d_x, d_out, out_f64, count, rel)) return rc;
   return finish(c);
 }
 
 int zc_comm_reduce_scatter_sym(zc_comm* c, int32_t* d_sym, uint64_t count, void* stream) {
-  (void)stream;
   if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
   if (c->nranks == 1 || count == 0) return ZC_OK;
   if (int rc = enqueue_ring(c, d_sym, count, false)) return rc;
   return finish(c);
 }
 
 int zc_comm_allgather_sym(zc_comm* c, int32_t* d_all, uint64_t block, void* stream) {
-  (void)stream;
   if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
   if (c->nranks == 1 || block == 0) return ZC_OK;
   if (int rc = enqueue_allgather(c, d_all, block)) return rc;
   return finish(c);
 }
 
 int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
-  (void)stream;
+  (void)stream;  // host scalar in and out: nothing on the caller's stream to order after
   if (!std::isfinite(v)) return set_err(ZC_ERR_INVALID_ARGUMENT, "allreduce_max requires finite input");
   if (c->nranks == 1) {
     *out = v;
@@ -824,6 +835,7 @@ int zc_group_allreduce_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, ui
   int rc = ZC_OK;
   for (int r = 0; r < n && !rc; ++r) {
     if ((rc = dev_guard(cs[r]))) break;
+    if ((rc = order_after(cs[r], nullptr))) break;
     rc = enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels);
   }
   int first = rc;
@@ -854,6 +866,7 @@ int zc_group_allreduce_eb_f32(zc_comm* const* cs, int n, const float* const* d_x
   }
   for (int r = 0; r < n && !rc; ++r) {
     if ((rc = dev_guard(cs[r]))) break;
+    if ((rc = order_after(cs[r], nullptr))) break;
     rc = enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel);
   }
   int first = rc;
@@ -875,6 +888,7 @@ int zc_group_allgather_sym(zc_comm* const* cs, int n, int32_t* const* d_alls, ui
   int first = ZC_OK;
   for (int r = 0; r < n && !first; ++r) {
     if ((first = dev_guard(cs[r]))) break;
+    if ((first = order_after(cs[r], nullptr))) break;
     first = enqueue_allgather(cs[r], d_alls[r], block);
   }
   for (int r = 0; r < n; ++r) {
@@ -895,6 +909,7 @@ int zc_group_reduce_scatter_sym(zc_comm* const* cs, int n, int32_t* const* d_sym
   if (n > 1 && count > 0)
     for (int r = 0; r < n && !first; ++r) {
       if ((first = dev_guard(cs[r]))) break;
+      if ((first = order_after(cs[r], nullptr))) break;
       first = enqueue_ring(cs[r], d_syms[r], count, false);
     }
   for (int r = 0; r < n; ++r) {

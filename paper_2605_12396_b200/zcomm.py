@@ -662,20 +662,20 @@ class Communicator:
 
     def allreduce(self, sym: torch.Tensor, scale: float, mode: int = abi.QUANT_ERROR_BOUNDED, levels: int = 0) -> float:
         s = C.c_double(scale)
-        check(lib().zc_comm_allreduce_sym(self._h, _ptr(sym), sym.numel(), mode, C.byref(s), levels, None))
+        check(lib().zc_comm_allreduce_sym(self._h, _ptr(sym), sym.numel(), mode, C.byref(s), levels, _stream()))
         return s.value
 
     def allreduce_eb(self, x: torch.Tensor, rel: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         out = out if out is not None else torch.empty(x.numel(), dtype=torch.float32, device=x.device)
         check(lib().zc_comm_allreduce_eb_f32(self._h, _ptr(x), _ptr(out), 1 if out.dtype == torch.float64 else 0,
-                                             x.numel(), float(rel), None))
+                                             x.numel(), float(rel), _stream()))
         return out
 
     def reduce_scatter(self, sym: torch.Tensor):
-        check(lib().zc_comm_reduce_scatter_sym(self._h, _ptr(sym), sym.numel(), None))
+        check(lib().zc_comm_reduce_scatter_sym(self._h, _ptr(sym), sym.numel(), _stream()))
 
     def allgather(self, all_blocks: torch.Tensor, block: int):
-        check(lib().zc_comm_allgather_sym(self._h, _ptr(all_blocks), block, None))
+        check(lib().zc_comm_allgather_sym(self._h, _ptr(all_blocks), block, _stream()))
 
     def allreduce_max(self, v: float) -> float:
         o = C.c_double()

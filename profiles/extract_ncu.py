@@ -3,8 +3,10 @@
     python profiles/extract_ncu.py gpurun_out/prof_rNN_full.ncu-rep rNN
 
 Writes profiles/<tag>_ncu_full_summary.txt (key counters per kernel) and updates
-profiles/ncu_traffic.json: dram read+write bytes per launch, keyed the way bench.py looks them up
-("zc_encode_f32" for the batched encoder, "zc_decode" for the batched decoder).
+profiles/ncu_traffic.json: dram read+write bytes per CALL, keyed the way bench.py looks them up
+("zc_encode_f32": the kernels of one zc_encode_batches_f32 call — profile / range / scan / emit;
+"zc_decode": one zc_decode_batches_f32 call — fl_decode / decode / fixup).  Capture exactly one
+encode + decode call (e.g. --launch-skip / --launch-count over tools/codec_probe.py).
 """
 import csv
 import io
@@ -31,6 +33,7 @@ def main(rep, tag):
     lines = [f"# ncu --set full --clock-control none ({os.path.basename(rep)}); one launch per kernel, cold L2 (ncu replay)"]
     traffic_path = os.path.join(HERE, "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    sums = {}
     for v in data:
         name = v[hdr.index("Kernel Name")]
         lines.append(name)
@@ -44,11 +47,15 @@ def main(rep, tag):
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(k)
             b += float(v[i].replace(",", "")) * UNIT.get(units[i], 1.0)
-        key = "zc_encode_f32" if "task_kernel" in name or "encode_kernel" in name else (
-            "zc_decode" if "decode_kernel" in name else None)
+        enc = any(k in name for k in ("profile_kernel", "range_kernel", "scan_kernel", "emit_kernel"))
+        dec = any(k in name for k in ("decode_kernel", "fixup_kernel"))
+        key = "zc_encode_f32" if enc else ("zc_decode" if dec else None)
         if key:
-            traffic[key] = int(b)
-            traffic[key + "_source"] = f"{tag}: {os.path.basename(rep)}"
+            sums[key] = sums.get(key, 0) + int(b)
+    for key, b in sums.items():
+        traffic[key] = b
+        traffic[key + "_source"] = f"{tag}: {os.path.basename(rep)} (sum over the call's kernels)"
+        lines.append(f"{key}: dram read+write per call = {b} bytes")
     with open(os.path.join(HERE, f"{tag}_ncu_full_summary.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(traffic_path, "w") as f:
