@@ -609,7 +609,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   g.s_full = static_cast<uint32_t>((p.unit_bytes + BS - 1) / BS);
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
-  g.fast = (SRC == SRC_F32 && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
+  g.fast = ((SRC == SRC_F32 || SRC == SRC_BYTES) && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
   if (p.pin == ZC_PIN_AUTO && !g.fast) {
     note_launch();
     profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);

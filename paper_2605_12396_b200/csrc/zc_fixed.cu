@@ -70,13 +70,14 @@ struct ProfSmem {
   uint8_t clens[256];
   uint32_t wmz[RT / 32];
 };
+template <int SRC>
 __device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uint32_t u, const float4* src, uint64_t R,
                                                bool ctx_ok, ProfSmem& sm, uint32_t& err) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < (RT / 32) * 256; i += RT) (&sm.whist[0][0])[i] = 0;
   for (int i = tid; i < 256; i += RT) sm.clens[i] = ctx_ok ? p.ctx->len[i] : 0;
   __syncthreads();
-  const uint64_t W = R < kSampleWindow ? R : kSampleWindow;  // whole words: R % 4 == 0 for fp32
+  const uint64_t W = R < kSampleWindow ? R : kSampleWindow;  // whole words: R % 4 == 0 on this path
   uint32_t wmz = 0;
   for (uint64_t v0 = 0; v0 * 16 < W; v0 += RT) {
     const uint64_t v = v0 + tid;
@@ -94,7 +95,14 @@ __device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uin
         a.y = nb > 4 ? __ldg(fs + 1) : 0.f;
         a.z = nb > 8 ? __ldg(fs + 2) : 0.f;
       }
-      quantize4(a, p.scale, p.rcp, w, err);
+      if (SRC == SRC_F32) {
+        quantize4(a, p.scale, p.rcp, w, err);
+      } else {  // symbols already
+        w[0] = __float_as_uint(a.x);
+        w[1] = __float_as_uint(a.y);
+        w[2] = __float_as_uint(a.z);
+        w[3] = __float_as_uint(a.w);
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (static_cast<uint32_t>(k) < nb / 4) wmz = max(wmz, zigzag32(static_cast<int32_t>(w[k])));
@@ -155,9 +163,16 @@ __device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uin
 // bit counts, RAW ones by emit.
 constexpr uint32_t RCH = 8;
 
+__device__ __forceinline__ uint32_t zz4(const float4& a) {
+  return max(max(zigzag32(__float_as_int(a.x)), zigzag32(__float_as_int(a.y))),
+             max(zigzag32(__float_as_int(a.z)), zigzag32(__float_as_int(a.w))));
+}
+
+template <int SRC>
 __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ EncParams p, BUnit* us, BGeom g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float s_mn[RT / 32], s_mx[RT / 32];
+  __shared__ uint32_t s_mz[RT / 32];
   __shared__ ProfSmem s_prof;
   __shared__ uint32_t s_task;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
@@ -167,6 +182,7 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
   BGlobal* gl = bglobal(us, p.nunits);
   uint32_t err = 0;
   float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+  uint32_t mz = 0;  // symbol sources: max zig-zag
   uint32_t run_u = 0xffffffffu, run_n = 0;
   // counts `n` finished pieces of unit u (thread 0); the completing one decides
   auto finish = [&](BUnit& U, uint32_t u, uint32_t n) {
@@ -175,34 +191,42 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
       __threadfence();
       const uint32_t plan = *reinterpret_cast<volatile uint32_t*>(&U.plan);
       if (plan == ZC_CODEC_HUFFMAN && automode) atomicAdd(&gl->n_huff, 1u);
-      if (target_codec(p, U, ctx_ok) == ZC_CODEC_FIXEDLEN) decide_unit<SRC_F32>(p, U, u, true, true, err);
+      if (target_codec(p, U, ctx_ok) == ZC_CODEC_FIXEDLEN) decide_unit<SRC>(p, U, u, true, true, err);
     }
   };
   auto flush = [&]() {
     for (int o = 16; o > 0; o >>= 1) {
       mn = fmin_nan(mn, __shfl_xor_sync(FULL, mn, o));
       mx = fmax_nan(mx, __shfl_xor_sync(FULL, mx, o));
+      mz = max(mz, __shfl_xor_sync(FULL, mz, o));
     }
     __syncthreads();
     if (lane == 0) {
       s_mn[warp] = mn;
       s_mx[warp] = mx;
+      s_mz[warp] = mz;
     }
     __syncthreads();
     if (tid == 0) {
       for (int i = 1; i < RT / 32; ++i) {
         mn = fmin_nan(mn, s_mn[i]);
         mx = fmax_nan(mx, s_mx[i]);
+        mz = max(mz, s_mz[i]);
       }
       BUnit& U = us[run_u];
-      const bool bad = !(fabsf(mn) <= 3.402823466e38f) || !(fabsf(mx) <= 3.402823466e38f);  // NaN / Inf
-      if (bad) atomicOr(&U.bad, 1u);
-      atomicMax(&U.fmin_c, ~fkey(mn));
-      atomicMax(&U.fmax_k, fkey(mx));
+      if (SRC == SRC_F32) {
+        const bool bad = !(fabsf(mn) <= 3.402823466e38f) || !(fabsf(mx) <= 3.402823466e38f);  // NaN / Inf
+        if (bad) atomicOr(&U.bad, 1u);
+        atomicMax(&U.fmin_c, ~fkey(mn));
+        atomicMax(&U.fmax_k, fkey(mx));
+      } else {
+        atomicMax(&U.maxzz, mz);
+      }
       finish(U, run_u, run_n);
     }
     mn = __int_as_float(0x7f800000);
     mx = -__int_as_float(0x7f800000);
+    mz = 0;
     run_n = 0;
   };
   for (;;) {
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
         if (tid == 0) us[u].plan = ZC_CODEC_RAW;
       } else {
         const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
-        window_profile(p, us[u], u, src, R, ctx_ok, s_prof, err);
+        window_profile<SRC>(p, us[u], u, src, R, ctx_ok, s_prof, err);
       }
       __syncthreads();
       if (tid == 0) finish(us[u], u, 1u);
@@ -245,21 +269,34 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
         for (int k = 0; k < static_cast<int>(BV / RT); ++k) a[k] = __ldg(q + k * RT);
 #pragma unroll
         for (int k = 0; k < static_cast<int>(BV / RT); ++k) {
-          mn = fmin_nan(mn, fmin_nan(fmin_nan(a[k].x, a[k].y), fmin_nan(a[k].z, a[k].w)));
-          mx = fmax_nan(mx, fmax_nan(fmax_nan(a[k].x, a[k].y), fmax_nan(a[k].z, a[k].w)));
+          if (SRC == SRC_F32) {
+            mn = fmin_nan(mn, fmin_nan(fmin_nan(a[k].x, a[k].y), fmin_nan(a[k].z, a[k].w)));
+            mx = fmax_nan(mx, fmax_nan(fmax_nan(a[k].x, a[k].y), fmax_nan(a[k].z, a[k].w)));
+          } else {
+            mz = max(mz, zz4(a[k]));
+          }
         }
       } else {
         const uint64_t v1 = min(v0 + BV, nf);
         for (uint64_t v = v0 + tid; v < v1; v += RT) {
           const float4 a = __ldg(src + v);
-          mn = fmin_nan(mn, fmin_nan(fmin_nan(a.x, a.y), fmin_nan(a.z, a.w)));
-          mx = fmax_nan(mx, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+          if (SRC == SRC_F32) {
+            mn = fmin_nan(mn, fmin_nan(fmin_nan(a.x, a.y), fmin_nan(a.z, a.w)));
+            mx = fmax_nan(mx, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+          } else {
+            mz = max(mz, zz4(a));
+          }
         }
         if (tid == 0 && v0 * 16 + BS >= R) {  // the unit's last 0..3 elements
           const float* fl = reinterpret_cast<const float*>(src);
           for (uint64_t e = nf * 4; e < R / 4; ++e) {
-            mn = fmin_nan(mn, __ldg(fl + e));
-            mx = fmax_nan(mx, __ldg(fl + e));
+            const float v = __ldg(fl + e);
+            if (SRC == SRC_F32) {
+              mn = fmin_nan(mn, v);
+              mx = fmax_nan(mx, v);
+            } else {
+              mz = max(mz, zigzag32(__float_as_int(v)));
+            }
           }
         }
       }
@@ -391,6 +428,7 @@ __device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* u
 
 __device__ __forceinline__ bool owned(uint32_t codec) { return codec == ZC_CODEC_RAW || codec == ZC_CODEC_FIXEDLEN; }
 
+template <int SRC>
 __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ EncParams p, const BUnit* us, BGeom g,
                                                      const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
                                                      uint64_t nfull) {
@@ -478,7 +516,12 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
     }
     uint32_t s[32];
-    quantize_row(x, scale, rcp, v.big, s, err);
+    if (SRC == SRC_F32) {
+      quantize_row(x, scale, rcp, v.big, s, err);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[i] = __float_as_uint(x[i]);
+    }
     store_row(v.codec, v.width, s, payload, (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
   }
 
@@ -495,7 +538,10 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
       uint32_t s[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s[i] = e0 + i < n ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err) : 0u;
+      for (int i = 0; i < 32; ++i)
+        s[i] = e0 + i < n ? (SRC == SRC_F32 ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err)
+                                            : __float_as_uint(__ldg(src + e0 + i)))
+                          : 0u;
       if (v.codec == ZC_CODEC_RAW) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -560,8 +606,8 @@ __device__ __forceinline__ int32_t row_symbol(const uint32_t (&a)[W], int i) {
 }
 
 // One tile in shared memory: packed rows in, swizzled fp32 tile out (same buffer).
-template <int W, bool kRaw>
-__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, int lane) {
+template <int W, bool kRaw, int OUT>
+__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, const int32_t* acc, int lane, uint32_t& err) {
   uint32_t a[W];
   const uint32_t row = buf + lane * W * 4;
   if (W % 4 == 0) {
@@ -578,30 +624,43 @@ __device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, int
 #pragma unroll
     for (int j = 0; j < W; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[j]) : "r"(row + 4 * j));
   }
-  __syncwarp();  // every lane holds its row before the floats overwrite the buffer
+  __syncwarp();  // every lane holds its row before the output overwrites the buffer
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-    float f[4];
+    uint32_t o[4];
+    int4 add = make_int4(0, 0, 0, 0);
+    if (OUT == OUT_ADD_I32) add = __ldcg(reinterpret_cast<const int4*>(acc + lane * 32) + m);
+    const int32_t ad[4] = {add.x, add.y, add.z, add.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int32_t sym = row_symbol<W, kRaw>(a, 4 * m + q);
-      f[q] = __double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym))));
+      if (OUT == OUT_F32) {
+        o[q] = __float_as_uint(__double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym)))));
+      } else if (OUT == OUT_ADD_I32) {  // RS sink: int64 sum range-checked to int32 (collectives.cpp:480-491)
+        const long long sum = static_cast<long long>(ad[q]) + sym;
+        if (sum != static_cast<int32_t>(sum)) err |= ZC_DERR_OVERFLOW;
+        o[q] = static_cast<uint32_t>(static_cast<int32_t>(sum));
+      } else {
+        o[q] = static_cast<uint32_t>(sym);
+      }
     }
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)), "f"(f[0]),
-                 "f"(f[1]), "f"(f[2]), "f"(f[3])
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)), "r"(o[0]),
+                 "r"(o[1]), "r"(o[2]), "r"(o[3])
                  : "memory");
   }
 }
 
-__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, int lane) {
+template <int OUT>
+__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, const int32_t* acc,
+                                                     int lane, uint32_t& err) {
   if (v.codec == ZC_CODEC_RAW) {
-    decode_tile_smem<32, true>(buf, scale, lane);
+    decode_tile_smem<32, true, OUT>(buf, scale, acc, lane, err);
     return;
   }
   switch (v.width) {
-#define ZC_DC(W)                                  \
-  case W:                                         \
-    decode_tile_smem<W, false>(buf, scale, lane); \
+#define ZC_DC(W)                                                   \
+  case W:                                                          \
+    decode_tile_smem<W, false, OUT>(buf, scale, acc, lane, err); \
     break;
     ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
     ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
@@ -631,6 +690,7 @@ struct DecSeq {  // a warp's tile sequence over owned units, with the view of th
   }
 };
 
+template <int OUT>
 __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant__ DecParams p,
                                                           const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
                                                           uint64_t nfull) {
@@ -640,6 +700,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   uint8_t* my = s_tiles + static_cast<size_t>(warp) * DSTAGES * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES) + warp * DSTAGES;
   const double scale = p.scale;
+  uint32_t err = 0;
   // decoded codec per owned unit (recv_batch's dispatch result)
   for (uint32_t u = blockIdx.x * DT + tid; u < p.nunits; u += gridDim.x * DT) {
     const DecView v = dec_view(p, u);
@@ -682,7 +743,8 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     }
     tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
     const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
-    decode_tile_dispatch(prc.cv, buf, scale, lane);
+    const int32_t* acc = OUT == OUT_ADD_I32 ? static_cast<const int32_t*>(p.out) + c * TILE_ELEMS : nullptr;
+    decode_tile_dispatch<OUT>(prc.cv, buf, scale, acc, lane, err);
     tma::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -712,12 +774,23 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
           const uint32_t z = static_cast<uint32_t>((x >> (bit & 31)) & (v.width == 32 ? 0xffffffffull : ((1ull << v.width) - 1)));
           sym = unzigzag32(z);
         }
-        out[e] = __double2float_rn(__dmul_rn(p.scale, i2d(static_cast<uint32_t>(sym))));
+        if (OUT == OUT_F32) {
+          out[e] = __double2float_rn(__dmul_rn(p.scale, i2d(static_cast<uint32_t>(sym))));
+        } else if (OUT == OUT_ADD_I32) {
+          int32_t* o = reinterpret_cast<int32_t*>(out) + e;
+          const long long sum = static_cast<long long>(*o) + sym;
+          if (sum != static_cast<int32_t>(sum)) err |= ZC_DERR_OVERFLOW;
+          *o = static_cast<int32_t>(sum);
+        } else {
+          reinterpret_cast<int32_t*>(out)[e] = sym;
+        }
       }
     }
   }
   if (lane == 0) tma::bulk_wait<0>();
   __syncwarp();
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -746,7 +819,8 @@ bool make_row_tensor_map(CUtensorMap* map, const void* base, uint64_t rows) {  /
 }
 
 bool fixed_path_ok(const EncParams& p) {
-  return p.src_kind == SRC_F32 && (reinterpret_cast<uintptr_t>(p.src) & 15u) == 0 && p.unit_bytes == ZC_BATCH_RAW_BYTES &&
+  const bool src_ok = p.src_kind == SRC_F32 || (p.src_kind == SRC_BYTES && p.total_bytes % 4 == 0);
+  return src_ok && (reinterpret_cast<uintptr_t>(p.src) & 15u) == 0 && p.unit_bytes == ZC_BATCH_RAW_BYTES &&
          p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook;
 }
 
@@ -756,8 +830,11 @@ cudaError_t launch_fixed_range(const EncParams& p, void* scratch, uint64_t total
   g.s_full = s_full;
   g.total = total_slices;
   note_launch();
-  range_kernel<<<static_cast<uint32_t>(std::min<uint64_t>(total_slices, 2ull * sms)), RT, 0, s>>>(
-      p, static_cast<BUnit*>(scratch), g);
+  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(total_slices + p.nunits, 2ull * sms));
+  if (p.src_kind == SRC_F32)
+    range_kernel<SRC_F32><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
+  else
+    range_kernel<SRC_BYTES><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
   return cudaGetLastError();
 }
 
@@ -765,7 +842,8 @@ cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_
                               cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+    cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+    cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
     attr = true;
   }
   const uint64_t count = p.total_bytes / 4;
@@ -783,12 +861,16 @@ cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_
   const uint64_t want = (ntiles + ET_WARPS * CHUNK - 1) / (ET_WARPS * CHUNK);
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
   note_launch();
-  emit_kernel<<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
+  if (p.src_kind == SRC_F32)
+    emit_kernel<SRC_F32><<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
+  else
+    emit_kernel<SRC_BYTES><<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
   return cudaGetLastError();
 }
 
 bool fixed_decode_ok(const DecParams& p) {
-  return !p.bare && p.out_kind == OUT_F32 && p.unit_bytes == ZC_BATCH_RAW_BYTES && (p.total_bytes % 4) == 0 &&
+  return !p.bare && (p.out_kind == OUT_F32 || p.out_kind == OUT_ADD_I32 || p.out_kind == OUT_BYTES) &&
+         p.unit_bytes == ZC_BATCH_RAW_BYTES && (p.total_bytes % 4) == 0 &&
          (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0 && (p.stride % 16) == 0 &&
          (reinterpret_cast<uintptr_t>(p.stages) & 15u) == 0;
 }
@@ -796,7 +878,9 @@ bool fixed_decode_ok(const DecParams& p) {
 cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fl_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+    cudaFuncSetAttribute(fl_decode_kernel<OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+    cudaFuncSetAttribute(fl_decode_kernel<OUT_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+    cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
     attr = true;
   }
   int dev = 0, sms = 148;
@@ -813,16 +897,25 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
   const uint64_t want = (ntiles + DT_WARPS * CHUNK - 1) / (DT_WARPS * CHUNK);
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
   note_launch();
-  fl_decode_kernel<<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+  if (p.out_kind == OUT_F32)
+    fl_decode_kernel<OUT_F32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+  else if (p.out_kind == OUT_ADD_I32)
+    fl_decode_kernel<OUT_ADD_I32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+  else
+    fl_decode_kernel<OUT_BYTES><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
   return cudaGetLastError();
 }
 
 
 void preload_fixed_kernels() {
-  cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, range_kernel);
-  cudaFuncSetAttribute(fl_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+  cudaFuncGetAttributes(&a, range_kernel<SRC_F32>);
+  cudaFuncGetAttributes(&a, range_kernel<SRC_BYTES>);
+  cudaFuncSetAttribute(fl_decode_kernel<OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+  cudaFuncSetAttribute(fl_decode_kernel<OUT_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+  cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
   cudaGetLastError();
 }
 
