@@ -123,6 +123,24 @@ int encode_common(EncParams& p, cudaStream_t s) {
   return cuda_err(launch_encode(p, s), "encode");
 }
 
+// Pre-sizes the scratch of stream `s` for messages of up to `nunits` batches, so later calls on
+// it never allocate (cudaFree / cudaMalloc can wait for the whole device: a ring rank's spinning
+// wait kernel would then wait for work not yet enqueued).
+int reserve_scratch(cudaStream_t s, uint32_t nunits) {
+  Scratch* sc = scratch_for(s, nunits);
+  if (!sc) return set_err(ZC_ERR_CUDA, "cannot allocate scratch (no CUDA device?)");
+  const size_t need = batch_scratch_bytes(nunits);
+  if (sc->task_bytes < need) {
+    cudaStreamSynchronize(s);
+    if (sc->task) cudaFree(sc->task);
+    sc->task = nullptr;
+    sc->task_bytes = 0;
+    if (int rc = cuda_err(cudaMalloc(&sc->task, need), "encoder scratch")) return rc;
+    sc->task_bytes = need;
+  }
+  return ZC_OK;
+}
+
 int decode_common(DecParams& p, cudaStream_t s) {
   Scratch* sc = scratch_for(s, p.nunits);
   if (!sc) return set_err(ZC_ERR_CUDA, "cannot allocate scratch (no CUDA device?)");
@@ -598,7 +616,11 @@ int zc_encode_best(const uint8_t* d_raw, uint64_t raw_len, uint8_t* d_stage, uin
 }
 
 // ------------------------------------------------------------------ batched hot path
-static int encode_batches(const void* src, int kind, uint64_t total, double scale, uint8_t* d_stages, uint64_t stride,
+__attribute__((visibility("hidden"))) int zc_i_reserve_scratch(void* stream, uint32_t nunits) {
+  return reserve_scratch(static_cast<cudaStream_t>(stream), nunits);
+}
+
+__attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, int kind, uint64_t total, double scale, uint8_t* d_stages, uint64_t stride,
                           uint64_t stage_len, int32_t pin, const zc_transport_hint* hint, const zc_huff_ctx* ctx,
                           const zc_arb_config* cfg, zc_encode_result* d_results, uint32_t* d_index, uint32_t* d_err,
                           void* stream) {
@@ -629,7 +651,7 @@ int zc_encode_batches_sym(const int32_t* d_sym, uint64_t raw_bytes, uint8_t* d_s
                           uint64_t stage_len, int32_t pin, const zc_transport_hint* hint, const zc_huff_ctx* ctx,
                           const zc_arb_config* cfg, zc_encode_result* d_results, uint32_t* d_index, uint32_t* d_err,
                           void* stream) {
-  return encode_batches(d_sym, SRC_BYTES, raw_bytes, 1.0, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
+  return zc_i_encode_batches(d_sym, SRC_BYTES, raw_bytes, 1.0, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
                         d_index, d_err, stream);
 }
 
@@ -639,13 +661,13 @@ int zc_encode_batches_f32(const float* d_x, uint64_t count, double scale, uint8_
                           void* stream) {
   if (int rc = check_scale(scale, "eb_quantize_chunk")) return rc;
   if (!aligned16(d_x)) return set_err(ZC_ERR_INVALID_ARGUMENT, "input must be 16-byte aligned");
-  return encode_batches(d_x, SRC_F32, count * 4, scale, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
+  return zc_i_encode_batches(d_x, SRC_F32, count * 4, scale, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
                         d_index, d_err, stream);
 }
 
-static int decode_batches(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
+__attribute__((visibility("hidden"))) int zc_i_decode_batches(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t total, const zc_huff_ctx* ctx, const uint32_t* d_index, int out_kind, void* out,
-                          double scale, uint32_t* d_codec, uint32_t* d_err, void* stream) {
+                          double scale, uint32_t* d_codec, uint32_t* d_err, void* stream, int own_frames) {
   if (total == 0) return ZC_OK;
   if (!aligned16(d_stages) || (stride & 15)) return set_err(ZC_ERR_INVALID_ARGUMENT, "stages must be 16-byte aligned");
   DecParams p;
@@ -665,28 +687,29 @@ static int decode_batches(const uint8_t* d_stages, uint64_t stride, uint64_t sta
   p.index_stride = ZC_HUFF_INDEX_ENTRIES;
   p.codec_out = d_codec;
   p.err = d_err;
+  p.own_frames = own_frames;
   return decode_common(p, static_cast<cudaStream_t>(stream));
 }
 
 int zc_decode_batches_sym(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t raw_bytes, const zc_huff_ctx* ctx, const uint32_t* d_index, int32_t* d_sym,
                           uint32_t* d_codec_out, void* stream) {
-  return decode_batches(d_stages, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_BYTES, d_sym, 1.0, d_codec_out,
-                        nullptr, stream);
+  return zc_i_decode_batches(d_stages, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_BYTES, d_sym, 1.0, d_codec_out,
+                        nullptr, stream, 0);
 }
 
 int zc_decode_batches_f32(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t count, double scale, const zc_huff_ctx* ctx, const uint32_t* d_index, float* d_out,
                           uint32_t* d_codec_out, void* stream) {
-  return decode_batches(d_stages, stride, stage_len, d_sent, count * 4, ctx, d_index, OUT_F32, d_out, scale,
-                        d_codec_out, nullptr, stream);
+  return zc_i_decode_batches(d_stages, stride, stage_len, d_sent, count * 4, ctx, d_index, OUT_F32, d_out, scale,
+                        d_codec_out, nullptr, stream, 0);
 }
 
 int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len,
                               const zc_encode_result* d_sent, uint64_t raw_bytes, const zc_huff_ctx* ctx,
                               const uint32_t* d_index, int32_t* d_acc, uint32_t* d_err, void* stream) {
-  return decode_batches(d_stages, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_ADD_I32, d_acc, 1.0, nullptr,
-                        d_err, stream);
+  return zc_i_decode_batches(d_stages, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_ADD_I32, d_acc, 1.0, nullptr,
+                        d_err, stream, 0);
 }
 
 }  // extern "C"
@@ -742,6 +765,9 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
   const uint64_t nb = (count + per - 1) / per;
   const uint64_t gb = group_batches ? group_batches : 4;
   const uint64_t ngroups = (nb + gb - 1) / gb;
+  // frames of this call's own encoder: without a usable Huffman path every valid frame is
+  // FixedLen / RAW and the general decode kernels have nothing to do
+  const int own = (ctx == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN) ? 1 : 0;
   if (int rc = cuda_err(cudaEventRecord(pp->start, caller), "pipeline start")) return rc;
   for (cudaStream_t s : {pp->h2d, pp->work, pp->d2h})
     if (int rc = cuda_err(cudaStreamWaitEvent(s, pp->start, 0), "pipeline wait")) return rc;
@@ -753,14 +779,14 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
     if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, pp->h2d), "H2D")) return rc;
     if (int rc = cuda_err(cudaEventRecord(in, pp->h2d), "H2D event")) return rc;
     if (int rc = cuda_err(cudaStreamWaitEvent(pp->work, in, 0), "H2D wait")) return rc;
-    if (int rc = encode_batches(d_work + e0, SRC_F32, n * 4, scale, d_stages + b0 * stride, stride, stage_len, pin, hint,
+    if (int rc = zc_i_encode_batches(d_work + e0, SRC_F32, n * 4, scale, d_stages + b0 * stride, stride, stage_len, pin, hint,
                                 ctx, cfg, d_results + b0, d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr,
                                 d_err, pp->work))
       return rc;
     // decoded in place: the group's encode has consumed its input (stream order)
-    if (int rc = decode_batches(d_stages + b0 * stride, stride, stage_len, d_results + b0, n * 4, ctx,
+    if (int rc = zc_i_decode_batches(d_stages + b0 * stride, stride, stage_len, d_results + b0, n * 4, ctx,
                                 d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr, OUT_F32, d_work + e0, scale,
-                                nullptr, d_err, pp->work))
+                                nullptr, d_err, pp->work, own))
       return rc;
     if (int rc = cuda_err(cudaEventRecord(done, pp->work), "kernel event")) return rc;
     if (int rc = cuda_err(cudaStreamWaitEvent(pp->d2h, done, 0), "kernel wait")) return rc;

@@ -34,27 +34,44 @@ constexpr uint32_t kBlobMagic = 0x5A434231u;  // "ZCB1"
 
 uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
+// Piece regions (the staged ring path): NREG regions, each holding up to `runits` frames of one
+// piece (stage stride as in zcomm.py's Frames), their Huffman companion index and EncodeResults.
+constexpr uint32_t kRegions = 3;
+
 struct Layout {
-  uint32_t nbanks;
+  uint32_t nbanks, runits;
   uint64_t bank_stride, idx_off;
-  uint64_t off_banks, off_ready, off_len, off_credit, off_err, off_mbox, off_mflag, off_wire, off_errall, off_scal,
-      off_peers, total;
+  uint64_t reg_stride, reg_idx, reg_res;  // region size; index / results offsets inside a region
+  uint64_t off_banks, off_reg, off_ready, off_len, off_credit, off_sready, off_scredit, off_err, off_mbox, off_mflag,
+      off_wire, off_errall, off_scal, off_peers, total;
 };
 
-Layout make_layout(uint32_t nbanks) {
+constexpr uint64_t kStageStride = (ZC_STAGE_BANK_BYTES + 255) / 256 * 256;
+
+Layout make_layout(uint32_t nbanks, uint32_t runits) {
   Layout L;
   L.nbanks = nbanks;
+  L.runits = runits;
   L.idx_off = align_up(ZC_STAGE_BANK_BYTES, kAlign);
   L.bank_stride = L.idx_off + align_up(ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
+  L.reg_idx = runits * kStageStride;
+  L.reg_res = L.reg_idx + align_up(runits * ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
+  L.reg_stride = L.reg_res + align_up(runits * sizeof(zc_encode_result), kAlign);
   uint64_t o = 0;
   L.off_banks = o;
   o += nbanks * L.bank_stride;
+  L.off_reg = o;
+  o += kRegions * L.reg_stride;
   L.off_ready = o;
   o += align_up(8ull * nbanks, kAlign);
   L.off_len = o;
   o += align_up(8ull * nbanks, kAlign);
   L.off_credit = o;
   o += align_up(8ull * nbanks, kAlign);
+  L.off_sready = o;  // [kRegions] pieces received in region i (written by the predecessor)
+  o += kAlign;
+  L.off_scredit = o;  // [kRegions] pieces consumed from the successor's region i (written by it)
+  o += kAlign;
   L.off_err = o;
   o += kAlign;
   L.off_mbox = o;
@@ -92,6 +109,8 @@ struct Blob {
   int32_t device;
   int32_t pid;
   int32_t nbanks;
+  int32_t runits;
+  int32_t _pad;
   uint64_t bytes;
   cudaIpcMemHandle_t handle;
 };
@@ -265,6 +284,63 @@ __global__ void set_scale_kernel(Scal* s, double rel, int from_absmax) {
   }
 }
 
+// ---- staged ring path: flag waits / signals between the codec kernels of a piece
+// Spins (one thread) until *flag >= v; gives up on this rank's error word or the timeout, which
+// it raises on every rank (link poisoning, transport.cpp:90-95).
+__global__ void wait_geq_kernel(const unsigned long long* flag, unsigned long long v, uint8_t* const* peers,
+                                uint64_t off_err, int rank, int nranks, unsigned long long timeout_ns) {
+  const uint32_t* err_self = reinterpret_cast<const uint32_t*>(peers[rank] + off_err);
+  const unsigned long long t0 = gtimer();
+  while (ld_acq(flag) < v) {
+    if (*reinterpret_cast<const volatile uint32_t*>(err_self) != 0) return;
+    if (gtimer() - t0 > timeout_ns) {
+      for (int q = 0; q < nranks; ++q) atomicOr(reinterpret_cast<uint32_t*>(peers[q] + off_err), ZC_DERR_TIMEOUT);
+      return;
+    }
+    __nanosleep(128);
+  }
+}
+
+// After a piece's frames are in the successor's region: count them into this rank's WireStats
+// (send_batch's accounting, collectives.cpp:285-296) and publish the piece (system-scope release).
+__global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, uint64_t raw_total,
+                                  zc_wire_stats* wire, unsigned long long* remote_ready, unsigned long long v) {
+  unsigned long long f[3] = {0, 0, 0}, raw = 0, pay = 0, tot = 0, idx = 0;
+  for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
+    const zc_encode_result r = res[u];
+    if (r.total_bytes == 0) continue;  // capacity failure: reported through the error word
+    const uint64_t R = (raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES < ZC_BATCH_RAW_BYTES ? raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES : static_cast<uint64_t>(ZC_BATCH_RAW_BYTES));
+    f[r.codec < 3 ? r.codec : 0] += 1;
+    raw += R;
+    pay += r.payload_bytes;
+    tot += r.total_bytes;
+    if (r.codec == ZC_CODEC_HUFFMAN) idx += 4 * ((R + ZC_HUFF_INDEX_GRAIN - 1) / ZC_HUFF_INDEX_GRAIN);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    for (int i = 0; i < 3; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+    raw += __shfl_xor_sync(0xffffffffu, raw, o);
+    pay += __shfl_xor_sync(0xffffffffu, pay, o);
+    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    idx += __shfl_xor_sync(0xffffffffu, idx, o);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i)
+      if (f[i]) atomicAdd(reinterpret_cast<unsigned long long*>(&wire->frames_by_codec[i]), f[i]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&wire->raw_bytes), raw);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&wire->payload_bytes), pay);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&wire->total_bytes), tot);
+    if (idx) atomicAdd(reinterpret_cast<unsigned long long*>(&wire->index_bytes), idx);
+    __threadfence_system();
+    st_rel(remote_ready, v);
+  }
+}
+
+// The predecessor may reuse its target region: this rank has decoded the piece that was in it.
+__global__ void piece_done_kernel(unsigned long long* remote_credit, unsigned long long v) {
+  __threadfence_system();
+  st_rel(remote_credit, v);
+}
+
 int sm_count(int dev) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -288,6 +364,7 @@ struct zc_comm {
   uint8_t** d_peers = nullptr;     // device copy of `peer` (inside the block)
   zc_huff_ctx* shared = nullptr;   // installed shared Huffman context (owned)
   uint64_t tx_seq = 0, rx_seq = 0;
+  uint64_t ptx = 0, prx = 0;       // pieces sent to the successor / received from the predecessor
   unsigned long long epoch = 0;
   zc_wire_stats host_wire{};       // control frames (meta / max) counted on the host
   int share = 1;                   // ranks sharing this device (loopback groups)
@@ -414,6 +491,74 @@ int exchange_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx,
   return ZC_OK;
 }
 
+// ---- staged ring path (default): each ring step moves its chunk in pieces of up to `runits`
+// 4 MiB batches.  A piece is encoded by the batched fast kernels (zc_batch.cu / zc_fixed.cu)
+// straight into one of the successor's kRegions piece regions over NVLink (peer-mapped stores),
+// published with a system-scope release; the successor decodes it with the fused sink (int32
+// add for reduce-scatter, store for all-gather) and returns the region with a credit.  Sends run
+// one piece ahead of receives, so a rank's encode of piece k overlaps its peers' decode of k-1.
+void launch_wait(zc_comm* c, const unsigned long long* flag, unsigned long long v) {
+  note_launch();
+  wait_geq_kernel<<<1, 1, 0, c->stream>>>(flag, v, c->d_peers, c->lay.off_err, c->rank, c->nranks, c->timeout_ns);
+}
+
+int send_piece(zc_comm* c, const int32_t* src, uint64_t bytes, int pin) {
+  const Layout& y = c->lay;
+  const int next = (c->rank + 1) % c->nranks;
+  const uint64_t seq = c->ptx++;
+  const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
+  if (seq >= kRegions)  // the successor has consumed the piece that last used this region
+    launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_scredit) + reg, seq - kRegions + 1);
+  uint8_t* dst = c->peer[next] + y.off_reg + reg * y.reg_stride;
+  auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
+  if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, dst, kStageStride, ZC_STAGE_BANK_BYTES, pin, &c->cfg.hint,
+                                   c->shared, &c->cfg.arb, res, reinterpret_cast<uint32_t*>(dst + y.reg_idx),
+                                   c->err_word(), c->stream))
+    return rc;
+  note_launch();
+  piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(bytes)), bytes,
+                                             reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire),
+                                             reinterpret_cast<unsigned long long*>(c->peer[next] + y.off_sready) + reg,
+                                             seq + 1);
+  return cuda_err(cudaGetLastError(), "piece send");
+}
+
+int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
+  // frames of our own batched encoder: without a Huffman context (or with a FixedLen / RAW pin)
+  // all are FixedLen / RAW and the general decode kernels are skipped
+  const bool own = c->shared == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN;
+  const Layout& y = c->lay;
+  const int prev = (c->rank - 1 + c->nranks) % c->nranks;
+  const uint64_t seq = c->prx++;
+  const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
+  launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1);
+  const uint8_t* region = c->block + y.off_reg + reg * y.reg_stride;
+  if (int rc = zc_i_decode_batches(region, kStageStride, ZC_STAGE_BANK_BYTES,
+                                   reinterpret_cast<const zc_encode_result*>(region + y.reg_res), bytes, c->shared,
+                                   reinterpret_cast<const uint32_t*>(region + y.reg_idx), store ? OUT_BYTES : OUT_ADD_I32,
+                                   dst, 1.0, nullptr, c->err_word(), c->stream, own ? 1 : 0))
+    return rc;
+  note_launch();
+  piece_done_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(c->peer[prev] + y.off_scredit) + reg,
+                                            seq + 1);
+  return cuda_err(cudaGetLastError(), "piece recv");
+}
+
+int staged_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin, bool store) {
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * ZC_BATCH_RAW_BYTES;
+  const uint64_t ns = (tx_bytes + pb - 1) / pb, nr = (rx_bytes + pb - 1) / pb;
+  const uint64_t steps = std::max(ns, nr) + 1;
+  for (uint64_t k = 0; k < steps; ++k) {
+    if (k < ns)
+      if (int rc = send_piece(c, tx + k * (pb / 4), std::min(pb, tx_bytes - k * pb), pin)) return rc;
+    if (k >= 1 && k - 1 < nr)
+      if (int rc = recv_piece(c, rx + (k - 1) * (pb / 4), std::min(pb, rx_bytes - (k - 1) * pb), store, pin)) return rc;
+  }
+  return ZC_OK;
+}
+
+bool use_staged() { return std::getenv("ZC_RING_KERNEL") == nullptr; }
+
 // Reduce-scatter then (optionally) all-gather over the ring (collectives.cpp:460-502).  RS frames
 // use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.  An AG step re-encodes the
 // chunk it received in the previous step: frames are a pure function of the bytes, so every hop
@@ -433,13 +578,21 @@ int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
   for (int t = 0; t < n - 1; ++t) {
     chunk(r - t, &sb, &sby);
     chunk(r - t - 1, &rb, &rby);
-    if (int rc = exchange_step(c, sb, sby, rb, rby, fused_pin, false, "rs-step")) return rc;
+    if (use_staged()) {
+      if (int rc = staged_step(c, sb, sby, rb, rby, fused_pin, false)) return rc;
+    } else if (int rc = exchange_step(c, sb, sby, rb, rby, fused_pin, false, "rs-step")) {
+      return rc;
+    }
   }
   if (!allgather) return ZC_OK;
   for (int t = 0; t < n - 1; ++t) {
     chunk(r + 1 - t, &sb, &sby);
     chunk(r - t, &rb, &rby);
-    if (int rc = exchange_step(c, sb, sby, rb, rby, c->cfg.pin, true, "ag-step")) return rc;
+    if (use_staged()) {
+      if (int rc = staged_step(c, sb, sby, rb, rby, c->cfg.pin, true)) return rc;
+    } else if (int rc = exchange_step(c, sb, sby, rb, rby, c->cfg.pin, true, "ag-step")) {
+      return rc;
+    }
   }
   return ZC_OK;
 }
@@ -451,9 +604,13 @@ int enqueue_allgather(zc_comm* c, int32_t* d_all, uint64_t block) {
   const uint64_t by = block * 4;
   for (int t = 0; t < n - 1; ++t) {
     const int si = ((r - t) % n + n) % n, ri = ((r - t - 1) % n + n) % n;
-    if (int rc = exchange_step(c, d_all + static_cast<uint64_t>(si) * block, by,
-                               d_all + static_cast<uint64_t>(ri) * block, by, c->cfg.pin, true, "ag-step"))
+    int32_t* sb = d_all + static_cast<uint64_t>(si) * block;
+    int32_t* rb = d_all + static_cast<uint64_t>(ri) * block;
+    if (use_staged()) {
+      if (int rc = staged_step(c, sb, by, rb, by, c->cfg.pin, true)) return rc;
+    } else if (int rc = exchange_step(c, sb, by, rb, by, c->cfg.pin, true, "ag-step")) {
       return rc;
+    }
   }
   return ZC_OK;
 }
@@ -557,7 +714,9 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
   uint32_t nbanks = nb ? static_cast<uint32_t>(std::max(2, std::min(16, std::atoi(nb)))) : ZC_STAGE_BANKS;
   const char* to = std::getenv("ZC_COMM_TIMEOUT_MS");
   if (to) c->timeout_ns = static_cast<unsigned long long>(std::atoll(to)) * 1000000ull;
-  c->lay = make_layout(nbanks);
+  const char* ru = std::getenv("ZC_COMM_REGION_UNITS");
+  const uint32_t runits = ru ? static_cast<uint32_t>(std::max(1, std::min(256, std::atoi(ru)))) : 16u;
+  c->lay = make_layout(nbanks, runits);
   int rc = cuda_err(cudaSetDevice(device), "cudaSetDevice");
   if (!rc) {
     preload_encode_kernels();
@@ -571,11 +730,15 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     cudaFuncGetAttributes(&fa, quantize_dev_kernel);
     cudaFuncGetAttributes(&fa, dequantize_dev_kernel);
     cudaFuncGetAttributes(&fa, set_scale_kernel);
+    cudaFuncGetAttributes(&fa, wait_geq_kernel);
+    cudaFuncGetAttributes(&fa, piece_sent_kernel);
+    cudaFuncGetAttributes(&fa, piece_done_kernel);
     cudaGetLastError();
   }
   if (!rc) rc = cuda_err(cudaMalloc(&c->block, c->lay.total), "cudaMalloc block");
   if (!rc) rc = cuda_err(cudaMemset(c->block + c->lay.off_ready, 0, c->lay.total - c->lay.off_ready), "memset");
   if (!rc) rc = cuda_err(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  if (!rc) rc = zc_i_reserve_scratch(c->stream, runits);
   if (rc) {
     if (c->block) cudaFree(c->block);
     delete c;
@@ -606,6 +769,7 @@ int reset_state(zc_comm* c) {
   const Layout& y = c->lay;
   int rc = cuda_err(cudaMemset(c->block + y.off_ready, 0, y.off_wire - y.off_ready), "reset");
   c->tx_seq = c->rx_seq = 0;
+  c->ptx = c->prx = 0;
   c->epoch = 0;
   return rc;
 }
@@ -629,6 +793,7 @@ int zc_comm_export(zc_comm* c, uint8_t* blob) {
   b.device = c->device;
   b.pid = static_cast<int32_t>(getpid());
   b.nbanks = static_cast<int32_t>(c->lay.nbanks);
+  b.runits = static_cast<int32_t>(c->lay.runits);
   b.bytes = c->lay.total;
   if (int rc = dev_guard(c)) return rc;
   if (c->nranks > 1)
@@ -643,7 +808,7 @@ int zc_comm_connect(zc_comm* c, const uint8_t* blobs) {
   for (int r = 0; r < c->nranks; ++r) {
     Blob b;
     std::memcpy(&b, blobs + r * sizeof(Blob), sizeof(Blob));
-    if (b.magic != kBlobMagic || b.rank != r || b.nranks != c->nranks || b.nbanks != static_cast<int>(c->lay.nbanks) ||
+    if (b.magic != kBlobMagic || b.rank != r || b.nranks != c->nranks || b.nbanks != static_cast<int>(c->lay.nbanks) || b.runits != static_cast<int>(c->lay.runits) ||
         b.bytes != c->lay.total)
       return set_err(ZC_ERR_INVALID_ARGUMENT, "communicator blobs disagree (rank order, size or bank count)");
     if (b.device == c->device) ++same_dev;

@@ -164,6 +164,7 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   if (fixed_decode_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) {
     if (cudaError_t e = launch_fixed_decode(p, s)) return e;
     p.fast = 1;
+    if (p.own_frames) return cudaSuccess;
   }
   const uint64_t maxR = p.bare ? p.hdr.raw_bytes : (p.unit_bytes < p.total_bytes ? p.unit_bytes : p.total_bytes);
   const uint64_t nvec = (maxR + 15) / 16;

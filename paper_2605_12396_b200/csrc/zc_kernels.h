@@ -102,6 +102,8 @@ struct DecParams {
   zc_frame_header hdr;
   int32_t* ok_out;         // bare decode result
   int fast;                // zc_fixed.cu's decoder has handled the valid FixedLen / RAW units
+  int own_frames;          // the frames come from this library's batched encoder without a Huffman
+                           // context: all valid FixedLen / RAW, so the general kernels are skipped
 };
 
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
