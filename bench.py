@@ -221,6 +221,8 @@ def codec_bench(args):
     if not torch.equal(hy, y.cpu()):
         raise RuntimeError("e2e output differs from the device-resident run")
 
+    loop = loopback_allreduce(args) if not args.no_loopback else None
+
     peak, peak_kind = peaks()
     gbs = lambda ms: raw_bytes / (ms * 1e-3) / 1e9  # noqa: E731
     P_auto, F = auto["payload"], fr.nbatches
@@ -271,12 +273,56 @@ def codec_bench(args):
         "gpu_launches": auto["launches"],
         "clocks": auto["clocks"],
     }
+    if loop is not None:
+        line["collective_loopback"] = loop
     if not args.no_cpu_baseline:
         # the reference on all host cores over the SAME 64 Mi workload, repeated so the timed CPU work
         # is ~10+ core-seconds; value = mean throughput of the repetitions
         line["cpu_baseline"] = cpu_baseline(x[: args.cpu_sample].cpu().numpy(), prime.cpu().numpy(), 0,
                                             reps=args.cpu_reps)
     return line
+
+
+def loopback_allreduce(args):
+    """BASELINE config 1's compressed AllReduce (2 ranks x 64 Mi Laplacian fp32, abs eb 1e-4) as a
+    loopback group on this one GPU: both ranks' ring kernels share cuda:0, frames move through
+    device memory instead of NVLink.  Device-timed with CUDA events; context, not the headline."""
+    import torch
+    from paper_2605_12396_b200 import zcomm
+    n, count = 2, COUNT_C0
+    xs = []
+    for r in range(n):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(100 + r)
+        u = torch.rand(count, generator=g, device="cuda", dtype=torch.float64) - 0.5
+        xs.append((-1e-2 * torch.sign(u) * torch.log1p(-2 * u.abs())).float())
+        del u
+    grp = zcomm.Group(n)
+    rel = ABS_EB / max(float(x.abs().max().item()) for x in xs)
+    outs = [torch.empty_like(x) for x in xs]
+    for _ in range(args.warmup):
+        grp.allreduce_eb(xs, rel, outs=outs)
+    torch.cuda.synchronize()
+    grp.reset_stats()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, args.steps // 2)
+    a.record()
+    for _ in range(steps):
+        grp.allreduce_eb(xs, rel, outs=outs)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    exact = xs[0].double() + xs[1].double()
+    err = float((outs[0].double() - exact).abs().max().item())
+    bound = n * ABS_EB * (1 + 1e-9) + float(exact.abs().max().item()) * 2.0 ** -24
+    if not err <= bound:
+        raise RuntimeError(f"loopback allreduce exceeds the error bound: {err} > {bound}")
+    w = grp.wire_stats()
+    grp.close()
+    return {"workload": "BASELINE config 1 on one GPU: 2-rank loopback group, 64 Mi Laplacian fp32 per rank, abs eb 1e-4",
+            "ms_per_step": round(ms, 3), "algbw_gbs": round(4 * count / (ms * 1e-3) / 1e9, 2),
+            "compression_ratio": round(w.raw_bytes / max(w.payload_bytes, 1), 4), "max_abs_err": err,
+            "note": "both ranks share one B200's HBM and SMs; not an NVLink number"}
 
 
 # ------------------------------------------------------------------------- CPU baseline / reference
@@ -492,6 +538,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=COUNT_C0)
     ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-loopback", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -585,8 +585,10 @@ class Group:
         check(lib().zc_group_allreduce_sym(self._h, self.nranks, self._ptrs(syms), syms[0].numel(), mode, sc, levels))
         return list(sc)
 
-    def allreduce_eb(self, xs: Sequence[torch.Tensor], rel: float, out_dtype=torch.float32):
-        outs = [torch.empty(x.numel(), dtype=out_dtype, device=x.device) for x in xs]
+    def allreduce_eb(self, xs: Sequence[torch.Tensor], rel: float, out_dtype=torch.float32,
+                     outs: Optional[Sequence[torch.Tensor]] = None):
+        outs = outs if outs is not None else [torch.empty(x.numel(), dtype=out_dtype, device=x.device) for x in xs]
+        out_dtype = outs[0].dtype
         check(lib().zc_group_allreduce_eb_f32(self._h, self.nranks, self._ptrs(xs), self._ptrs(outs),
                                               1 if out_dtype == torch.float64 else 0, xs[0].numel(), float(rel)))
         return outs
