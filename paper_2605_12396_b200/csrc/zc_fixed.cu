@@ -407,6 +407,8 @@ __device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64
   return (j + ((je - j + tw - 1) / tw) * tw) * CHUNK;
 }
 
+constexpr uint32_t kForeign = 0xFEu;  // unit owned by the general kernels
+
 struct UnitView {
   uint32_t codec, width;
   uint64_t P;
@@ -418,6 +420,9 @@ struct UnitView {
 __device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* us, uint32_t u, bool ctx_ok) {
   UnitView v;
   final_codec(p, us[u], u, ctx_ok, v.codec, v.width, v.P);
+  // ownership is by TARGET: a Huffman-target unit (even one that fell back to RAW) belongs to
+  // zc_batch.cu's kernels
+  if (target_codec(p, us[u], ctx_ok) == ZC_CODEC_HUFFMAN) v.codec = kForeign;
   v.big = true;
   if (v.codec == ZC_CODEC_FIXEDLEN) {
     // the width is < 31 iff max zz < 2^30, i.e. every |q| < 2^29

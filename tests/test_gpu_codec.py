@@ -456,3 +456,27 @@ def test_codec_roundtrip_host_pipeline(zc):
     for b in range(ref.nbatches):
         assert np.array_equal(npy(fr.frame(b)), npy(ref.frame(b)))
     assert torch.equal(hy, zc.decode_batches(ref, None, scale=2e-4).cpu())
+
+
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_HUFFMAN])
+def test_embedded_codebook_batches_vs_oracle(zc, port, pin):
+    """cfg.embed_codebook end to end (rea.cpp:214-221, huffman.cpp:256-262): every
+    batch builds its own tree from its full histogram and ships the 256 code lengths in the frame;
+    frames byte-equal to the reference's send_batch, and recv_batch decodes them without a
+    shared context."""
+    cases = _stream_cases()
+    msg = np.concatenate([cases["geometric"].view(np.uint8), cases["adversarial"], cases["narrow"].view(np.uint8)])
+    cfg = abi.default_arb_config()
+    cfg.embed_codebook = 1
+    hint = abi.make_hint(1e9)
+    fr = zc.encode_batches(t(msg), pin, hint=hint, cfg=cfg)
+    exp = port.encode_batches(msg, pin, hint, None, cfg)
+    assert fr.nbatches == len(exp)
+    codecs = []
+    for b, (er, ef) in enumerate(exp):
+        r = fr.encode_results()[b]
+        assert (r.codec, r.payload_bytes, r.total_bytes) == (er.codec, er.payload_bytes, er.total_bytes), b
+        assert np.array_equal(npy(fr.frame(b)), ef), b
+        codecs.append(r.codec)
+    assert abi.CODEC_HUFFMAN in codecs
+    assert np.array_equal(npy(zc.decode_batches(fr, None)).view(np.uint8), msg)
