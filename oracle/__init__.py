@@ -238,8 +238,25 @@ class Ref:
         _sig(L, "zr_allgather_sym", C.c_int, C.c_int, P(abi.CollectiveConfig), i32p, C.c_uint64, vp, C.c_uint64,
              i32p, P(abi.WireStats))
         _sig(L, "zr_gen_data", C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, f64p)
+        _sig(L, "zr_emit_csv", C.c_int, f64p, C.c_int, C.c_char_p, C.c_uint64)
+        _sig(L, "zr_emit_markdown", C.c_int, f64p, C.c_int, C.c_char_p, C.c_uint64)
         _sig(L, "zr_codec_roundtrip_mt", C.c_int, f32p, C.c_uint64, C.c_double, C.c_int, vp, P(abi.ArbConfig),
              C.c_int, C.c_double, C.c_int, vp, P(C.c_uint64), u64p, P(C.c_double))
+
+    def _emit(self, fn, rows):
+        flat = np.ascontiguousarray([v for r in rows for v in r.flat()], np.float64)
+        buf = C.create_string_buffer(1 << 20)
+        n = fn(flat, len(rows), buf, len(buf))
+        assert n >= 0
+        return buf.value.decode()
+
+    def emit_csv(self, rows):
+        """bench.cpp:551-565 emit_csv over ReportRow records (report.ReportRow)."""
+        return self._emit(self.lib.zr_emit_csv, rows)
+
+    def emit_markdown(self, rows):
+        """bench.cpp:620-671 emit_markdown."""
+        return self._emit(self.lib.zr_emit_markdown, rows)
 
     def huff_from_hist(self, hist):
         return C.c_void_p(self.lib.zr_huff_ctx_new(np.ascontiguousarray(hist, np.uint64)))

@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <iostream>
+#include <sstream>
+#include <string>
 #include <cstring>
 #include <stdexcept>
 #include <thread>
@@ -508,4 +511,67 @@ int zr_codec_roundtrip_mt(const float* x, uint64_t count, double scale, int pin,
   }
 }
 
+}  // extern "C"
+
+// Report emitters (bench.cpp:551-565 emit_csv, :620-671 emit_markdown) over rows given as a flat
+// record array: the checker for paper_2605_12396_b200/report.py.  Per row, 26 doubles in the
+// ReportRow field order (enums and integers carried exactly as doubles).
+// The shim is linked with a static libstdc++ (this toolchain's g++ wrapper) and loaded with
+// dlopen: make sure the iostream / locale machinery the emitters use is initialised.
+static std::ios_base::Init g_zr_ios_init;
+
+static std::vector<ReportRow> rows_from_flat(const double* v, int nrows) {
+  std::vector<ReportRow> rows(static_cast<size_t>(nrows));
+  for (int i = 0; i < nrows; ++i) {
+    const double* f = v + 26 * i;
+    ReportRow& r = rows[static_cast<size_t>(i)];
+    r.collective = static_cast<CollOp>(static_cast<int>(f[0]));
+    r.ranks = static_cast<int>(f[1]);
+    r.msgBytes = static_cast<uint64_t>(f[2]);
+    r.codec = static_cast<CodecPin>(static_cast<int>(f[3]));
+    r.quant = static_cast<QuantKind>(static_cast<int>(f[4]));
+    r.dist = static_cast<DataDist>(static_cast<int>(f[5]));
+    r.seed = static_cast<uint64_t>(f[6]);
+    r.overlap = static_cast<OverlapMode>(static_cast<int>(f[7]));
+    r.regime = static_cast<Regime>(static_cast<int>(f[8]));
+    r.bwBytesPerSec = f[9];
+    r.latencySec = f[10];
+    r.simTimeSec = f[11];
+    r.wallTimeSec = f[12];
+    r.wireRawBytes = static_cast<uint64_t>(f[13]);
+    r.wirePayloadBytes = static_cast<uint64_t>(f[14]);
+    r.wireTotalBytes = static_cast<uint64_t>(f[15]);
+    r.framesRaw = static_cast<uint64_t>(f[16]);
+    r.framesFixed = static_cast<uint64_t>(f[17]);
+    r.framesHuffman = static_cast<uint64_t>(f[18]);
+    r.crQuant = f[19];
+    r.crFinal = f[20];
+    r.algBwBytesPerSec = f[21];
+    r.busBwBytesPerSec = f[22];
+    r.speedupVsRaw = f[23];
+    r.exposedCodecSimSec = f[24];
+    r.wallCodecSec = f[25];
+  }
+  return rows;
+}
+
+static int copy_out(const std::string& s, char* out, uint64_t cap) {
+  if (s.size() + 1 > cap) return -static_cast<int>(s.size() + 1);
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+extern "C" {
+int zr_emit_csv(const double* flat, int nrows, char* out, uint64_t cap) {
+  std::vector<ReportRow> rows = rows_from_flat(flat, nrows);
+  std::ostringstream os;
+  emit_csv(rows, os);
+  return copy_out(os.str(), out, cap);
+}
+int zr_emit_markdown(const double* flat, int nrows, char* out, uint64_t cap) {
+  std::vector<ReportRow> rows = rows_from_flat(flat, nrows);
+  std::ostringstream os;
+  emit_markdown(rows, os);
+  return copy_out(os.str(), out, cap);
+}
 }  // extern "C"
