@@ -276,6 +276,49 @@ __global__ void __launch_bounds__(NT, 1) scan_kernel(const EncParams p, BUnit* u
     uint32_t zero = 0;
     unsigned long long hb = 0;
     constexpr int UN = 4;
+    if (p.index != nullptr) {
+      // per 1 KiB grain (one warp, 32 bytes per lane): the grain's bit count goes to the
+      // companion index slot, which huff_emit_kernel turns into the grain's start bit
+      uint32_t* uindex = p.index + static_cast<uint64_t>(u) * p.index_stride;
+      // GU grains per warp iteration (2*GU x 16 bytes in flight per lane, as registers allow)
+      constexpr int GU = SRC == SRC_BYTES ? 4 : SRC == SRC_F32 ? 2 : 1;
+      for (uint64_t gv = v0 + static_cast<uint64_t>(warp) * 64; gv < v1; gv += NT * 2 * GU) {
+        RawVec rv[2 * GU];
+#pragma unroll
+        for (int k = 0; k < 2 * GU; ++k) {
+          const uint64_t v = gv + (k >> 1) * (NT * 2) + 2 * lane + (k & 1);
+          rv[k].nb = 0;
+          if (v < v1) fetch<SRC, false>(p, uoff, R, v, rv[k]);
+        }
+        uint32_t gb[GU];
+#pragma unroll
+        for (int h = 0; h < GU; ++h) gb[h] = 0;
+#pragma unroll
+        for (int k = 0; k < 2 * GU; ++k) {
+          if (rv[k].nb == 0) continue;
+          uint32_t w[4];
+          if (rv[k].nb == 16)
+            words_full<SRC>(p, rv[k], w, err);
+          else
+            to_words<SRC>(p, rv[k], w, err);
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            if (j < rv[k].nb) {
+              const uint32_t l = s_clens[byte_of(w, j)];
+              gb[k >> 1] += l;
+              zero |= (l == 0);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < GU; ++h) {
+          hb += gb[h];
+          const uint32_t t2 = __reduce_add_sync(FULL, gb[h]);
+          const uint64_t gh = gv + h * (NT * 2);
+          if (lane == 0 && gh < v1) uindex[gh / 64] = t2;
+        }
+      }
+    } else
     for (uint64_t base = v0 + static_cast<uint64_t>(warp) * 32; base < v1; base += NT * UN) {
       RawVec rv[UN];
 #pragma unroll
@@ -374,6 +417,7 @@ __global__ void __launch_bounds__(NT, 1) emit_kernel(const EncParams p, BUnit* u
       if (codec == ZC_CODEC_RAW && R > pcap) codec = CODEC_NONE;
     }
     if (g.fast && target != ZC_CODEC_HUFFMAN) continue;  // zc_fixed.cu owns the RAW / FixedLen targets
+    if (codec == ZC_CODEC_HUFFMAN && p.index != nullptr) continue;  // huff_emit_kernel
     if (codec == CODEC_NONE) {
       if (s == 0) err |= ZC_DERR_CAPACITY;
     } else if (codec == ZC_CODEC_RAW) {
@@ -593,6 +637,208 @@ __global__ void __launch_bounds__(NT, 1) emit_kernel(const EncParams p, BUnit* u
   if (lane == 0 && err && p.err) atomicOr(p.err, err);
 }
 
+// ------------------------------------------------------------------ pass 3b: Huffman frames, one warp per grain
+// huffman_encode (huffman.cpp:216-246) for every unit the decision made Huffman, when the companion
+// index exists.  scan_kernel left each 1 KiB grain's exact bit count in its index slot; per 64 KiB
+// slice the CTA turns the counts into start bits (the index proper).  A warp then encodes a grain
+// on its own: two 512-byte steps, lane = 16 bytes; a warp exclusive scan of the lanes' code
+// lengths gives each lane its bit offset and the lane packs its codes LSB-first into the warp's
+// shared-memory tile (ATOMS.OR only on words it may share with a neighbour).  Every payload word
+// has exactly one writer: the grain that starts in it.  The grain ORs in the tail bits of the
+// previous grain, recomputed from that grain's last 32 bytes (32 codes >= 32 bits always cover
+// the shared word), and leaves its own last partial word to the next grain (the unit's last grain
+// writes it, byte-exact at the payload end).  No zeroing pass, no global atomics, no seam merge.
+constexpr int HT = 1026;  // tile words per warp: a grain is <= 1024 codes x 32 bits, + shift
+
+template <int SRC, bool kFull>
+__device__ __forceinline__ void grain_codes(const EncParams& p, const RawVec& rv, const unsigned long long* s_enc,
+                                            unsigned long long ev[16], uint32_t& L, uint32_t& err) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  if (kFull || rv.nb == 16)
+    words_full<SRC>(p, rv, w, err);
+  else if (rv.nb)
+    to_words<SRC>(p, rv, w, err);
+  L = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) {
+    ev[j] = (kFull || j < rv.nb) ? s_enc[byte_of(w, j)] : 0ull;
+    L += static_cast<uint32_t>(ev[j] >> 32);
+  }
+}
+
+// Packs one lane's codes LSB-first at tile bit `pos`.  Codes are <= 32 bits, so each code flushes
+// at most one word; every flush is an ATOMS.OR (branch-free: the first and last words may be
+// shared with neighbouring lanes, the tile is zeroed).
+__device__ __forceinline__ void pack_codes(uint32_t* tile, uint32_t pos, const unsigned long long ev[16]) {
+  uint32_t wi = pos >> 5, nbit = pos & 31;
+  unsigned long long acc = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) {
+    acc |= (ev[j] & 0xffffffffull) << nbit;
+    nbit += static_cast<uint32_t>(ev[j] >> 32);
+    const bool f = nbit >= 32;
+    if (f) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+    acc = f ? (acc >> 32) : acc;
+    wi += f ? 1u : 0u;
+    nbit -= f ? 32u : 0u;
+  }
+  if (nbit > 0) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+}
+
+template <int SRC, bool kFull>
+__device__ __forceinline__ void grain_fetch(const EncParams& p, uint64_t uoff, uint64_t R, uint64_t nvec, uint64_t gv,
+                                            int lane, RawVec rv[2]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint64_t v = gv + 32 * k + lane;
+    if (kFull) {
+      fetch_full<SRC, false>(p, uoff, v, rv[k]);
+    } else {
+      rv[k].nb = 0;
+      if (v < nvec) fetch<SRC, false>(p, uoff, R, v, rv[k]);
+    }
+  }
+}
+
+// Encodes the two 512-byte steps of a grain into `tile` from bit sh0 on.
+template <int SRC, bool kFull>
+__device__ __forceinline__ void grain_pack(const EncParams& p, const RawVec rv[2], const unsigned long long* s_enc,
+                                           uint32_t* tile, uint32_t sh0, int lane, uint32_t& err) {
+  uint32_t run = sh0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    unsigned long long ev[16];
+    uint32_t L;
+    grain_codes<SRC, kFull>(p, rv[k], s_enc, ev, L, err);
+    uint32_t x = L;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    pack_codes(tile, run + x - L, ev);
+    run += __shfl_sync(FULL, x, 31);
+  }
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUnit* us, BGeom g) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ unsigned long long s_enc[256];
+  __shared__ uint32_t s_start[BS / kIndexGrain + 1];
+  extern __shared__ __align__(16) uint32_t s_tiles[];
+  uint32_t* tile = s_tiles + warp * HT;
+  const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
+  const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
+  if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<const volatile uint32_t*>(&bglobal(us, p.nunits)->n_huff) == 0) return;
+  if (!ctx_ok) return;
+  for (int i = tid; i < 256; i += NT) s_enc[i] = p.ctx->enc[i];
+  __syncthreads();
+  uint32_t err = 0;
+  for (uint64_t tt = blockIdx.x; tt < g.total; tt += gridDim.x) {
+    const uint64_t t = g.total - 1 - tt;  // reverse: pass 2 ended on the last units (L2-resident)
+    uint32_t u, s;
+    g.unit_of(t, p.nunits, u, s);
+    BUnit& U = us[u];
+    uint32_t codec, width;
+    uint64_t P;
+    final_codec(p, U, u, ctx_ok, codec, width, P);
+    if (codec != ZC_CODEC_HUFFMAN) continue;
+    const uint64_t R = unit_R(p, u);
+    const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
+    const uint64_t nvec = (R + 15) / 16;
+    const uint32_t ngr = static_cast<uint32_t>((R + kIndexGrain - 1) / kIndexGrain);
+    const uint32_t gs0 = s * (BS / kIndexGrain);
+    const uint32_t n = min(static_cast<uint32_t>(BS / kIndexGrain), ngr - gs0);
+    uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+    uint32_t* uindex = p.index + static_cast<uint64_t>(u) * p.index_stride;
+    if (warp == 0) {  // grain counts -> start bits (the companion index)
+      const uint32_t c0 = 2 * lane < n ? __ldcg(uindex + gs0 + 2 * lane) : 0u;
+      const uint32_t c1 = 2 * lane + 1 < n ? __ldcg(uindex + gs0 + 2 * lane + 1) : 0u;
+      uint32_t x = c0 + c1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t b0 = static_cast<uint32_t>(__ldcg(&U.hbase[s])) + x - c0 - c1;
+      s_start[2 * lane] = b0;
+      s_start[2 * lane + 1] = b0 + c0;
+      if (lane == 31) s_start[64] = b0 + c0 + c1;
+      __syncwarp();
+      if (2 * lane < n) uindex[gs0 + 2 * lane] = b0;
+      if (2 * lane + 1 < n) uindex[gs0 + 2 * lane + 1] = b0 + c0;
+    }
+    __syncthreads();
+    for (uint32_t gi = warp; gi < n; gi += NW) {
+      const uint32_t gidx = gs0 + gi;
+      const uint32_t B = s_start[gi], E = s_start[gi + 1];
+      const uint32_t sh0 = B & 31;
+      const uint32_t nw = (sh0 + (E - B) + 31) >> 5;  // tile words touched
+      const bool last = gidx + 1 == ngr;
+      const uint64_t gv = static_cast<uint64_t>(gidx) * 64;
+      const bool full = fast_ok && (gidx + 1) * static_cast<uint64_t>(kIndexGrain) <= R;
+      RawVec rv[2];
+      if (full) grain_fetch<SRC, true>(p, uoff, R, nvec, gv, lane, rv);
+      else grain_fetch<SRC, false>(p, uoff, R, nvec, gv, lane, rv);
+      // tail bits of the previous grain in this grain's first word
+      uint32_t prevtail = 0;
+      if (sh0 != 0 && gidx > 0) {
+        const uint64_t b = static_cast<uint64_t>(gidx) * kIndexGrain - 32 + lane;
+        RawVec pv;
+        fetch<SRC, false>(p, uoff, R, b / 16, pv);
+        uint32_t w[4];
+        if (pv.nb == 16)
+          words_full<SRC>(p, pv, w, err);
+        else
+          to_words<SRC>(p, pv, w, err);
+        const unsigned long long e = s_enc[byte_of(w, static_cast<uint32_t>(b & 15))];
+        const uint32_t l = static_cast<uint32_t>(e >> 32), c = static_cast<uint32_t>(e);
+        uint32_t x = l;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t T = __shfl_sync(FULL, x, 31);
+        // stream positions relative to W0 = B & ~31 (ints: the walk starts up to 1024 bits back)
+        const int end = static_cast<int>(sh0) - static_cast<int>(T - x);
+        const int start = end - static_cast<int>(l);
+        uint32_t part = 0;
+        if (end > 0 && l > 0) part = start >= 0 ? (c << start) : (c >> (-start));
+        prevtail = __reduce_or_sync(FULL, part);
+      }
+      for (uint32_t i = lane; i < nw; i += 32) tile[i] = 0;
+      __syncwarp();
+      if (full) grain_pack<SRC, true>(p, rv, s_enc, tile, sh0, lane, err);
+      else grain_pack<SRC, false>(p, rv, s_enc, tile, sh0, lane, err);
+      __syncwarp();
+      if (lane == 0 && prevtail) tile[0] |= prevtail;
+      __syncwarp();
+      const uint64_t wb = B >> 5;
+      const uint32_t nout = last ? nw : ((sh0 + (E - B)) >> 5);
+      for (uint32_t i = lane; i < nout; i += 32) store_word_safe(payload, wb + i, tile[i], P);
+      __syncwarp();
+    }
+    if (s == 0 && tid == 0) write_frame_header(p, u, codec, width, P);
+    __syncthreads();
+  }
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
+}
+
+constexpr size_t kHuffEmitSmem = sizeof(uint32_t) * NW * HT;
+
+template <int SRC>
+void launch_huff_emit(const EncParams& p, BUnit* us, const BGeom& g, int sms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(huff_emit_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+    attr = true;
+  }
+  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(2 * sms)));
+  note_launch();
+  huff_emit_kernel<SRC><<<grid, NT, kHuffEmitSmem, s>>>(p, us, g);
+}
+
 template <int SRC>
 cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   static bool attr = false;
@@ -626,10 +872,11 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
       scan_kernel<SRC><<<grid, NT, 0, s>>>(p, us, g);
     }
     if (cudaError_t e = launch_fixed_emit(p, scratch, g.total, g.s_full, sms, s)) return e;
-    if (huff_possible) {
+    if (huff_possible) {  // Huffman targets: frames without an index, and the RAW fallbacks
       note_launch();
       emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
     }
+    if (huff_possible && p.index != nullptr) launch_huff_emit<SRC>(p, us, g, sms, s);
     return cudaGetLastError();
   }
   if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN || (p.pin == ZC_PIN_HUFFMAN && ctx_ok_host)) {
@@ -638,6 +885,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   }
   note_launch();
   emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
+  if (huff_possible && p.index != nullptr) launch_huff_emit<SRC>(p, us, g, sms, s);
   return cudaGetLastError();
 }
 
@@ -649,6 +897,9 @@ void preload_batch_kernels() {
   cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
   cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
   cudaFuncSetAttribute(emit_kernel<SRC_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, profile_kernel<SRC_BYTES>);
   cudaFuncGetAttributes(&a, profile_kernel<SRC_F32>);

@@ -46,8 +46,12 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
   const int tid = threadIdx.x, lane = tid & 31;
 
   __shared__ FrameCheck fc;
-  __shared__ DevHuff s_t;
-  __shared__ uint32_t s_words[(DT / 32) * 136 * 4];
+  // a frame is one codec: the Huffman tables and the FixedLen staging words share the space, which
+  // leaves the L1 room for every thread's current 128-byte line of its Huffman grain
+  constexpr size_t kWordsBytes = sizeof(uint32_t) * (DT / 32) * 136 * 4;
+  __shared__ __align__(16) uint8_t s_pool[sizeof(DevHuff) > kWordsBytes ? sizeof(DevHuff) : kWordsBytes];
+  DevHuff& s_t = *reinterpret_cast<DevHuff*>(s_pool);
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pool);
   __shared__ uint8_t s_lens[256];
   __shared__ uint32_t s_flag;
   uint32_t err = 0;
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(DT) fixup_kernel(const DecParams p) {
 }  // namespace
 
 void preload_decode_kernels() {
+  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, decode_kernel);
   cudaFuncGetAttributes(&a, fixup_kernel);
@@ -170,6 +175,11 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   const uint64_t nvec = (maxR + 15) / 16;
   const uint32_t slices = static_cast<uint32_t>((nvec + SLICE_VEC - 1) / SLICE_VEC);
   dim3 grid(slices > 0 ? slices : 1, p.nunits);
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
+    carve = true;
+  }
   note_launch();
   decode_kernel<<<grid, DT, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();

@@ -235,6 +235,100 @@ __device__ __forceinline__ bool huff_run(const DevHuff* t, const uint8_t* s, uin
   return true;
 }
 
+// Over-root code (the root LUT escaped): the canonical walk of huffman.cpp:293-306 resumed at
+// length ROOT+1 — no code of length <= ROOT matches, or the LUT would have decoded it.  acc holds
+// >= 32 valid bits.  Returns the code length (0: undecodable) and the symbol.
+__device__ __forceinline__ uint32_t huff_long(const DevHuff* t, unsigned long long acc, uint32_t& sym) {
+  unsigned long long val = __brev(static_cast<uint32_t>(acc) & ((1u << ZC_HUFF_ROOT_BITS) - 1)) >> (32 - ZC_HUFF_ROOT_BITS);
+  for (uint32_t k = ZC_HUFF_ROOT_BITS + 1; k <= t->max_len; ++k) {
+    val = (val << 1) | ((acc >> (k - 1)) & 1ull);
+    const uint32_t c = t->count_at_len[k];
+    const unsigned long long fc = t->first_code[k];
+    if (c > 0 && val >= fc && val < fc + c) {
+      sym = t->sym_order[t->first_index[k] + static_cast<uint32_t>(val - fc)];
+      return k;
+    }
+  }
+  return 0;
+}
+
+// One index grain of a Huffman stream (huffman.cpp:281-314), the throughput path: n raw bytes from
+// bit `start`, 16 bytes at a time handed to emit16.  The bit reader keeps a 64-bit window topped
+// up to >= 32 bits before every code, from a prefetched next stream word (its load is issued one
+// top-up ahead, so no global load sits on the LUT -> shift chain).  The top-up is predicated, not
+// a branch: the 32 lanes of a warp refill at different symbols.  The root LUT is read through a
+// 32-bit shared-window address.  kChecked (grains near the frame end): stream bytes past the end
+// read as zero, as in the reference.  Codes past the stream end are caught by the final position
+// check: positions only grow, so any code crossing the end leaves *end > 8*slen.  Returns false
+// on an undecodable code or an overrun.  s must be 4-byte aligned.
+template <bool kCoherent, bool kChecked>
+__device__ __forceinline__ bool huff_grain(const DevHuff* t, const uint8_t* s, uint64_t slen, uint64_t start, uint32_t n,
+                                           const Sink& sink, uint64_t ob, uint64_t* end, uint32_t& err) {
+  const uint32_t* ws = reinterpret_cast<const uint32_t*>(s);
+  uint64_t wi = start >> 5;  // next word to prefetch
+  auto word = [&](uint64_t i) -> uint32_t {
+    if (kChecked) return stream_word<kCoherent>(s, slen, i);
+    if (kCoherent) return __ldcg(ws + i);
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::256B.u32 %0, [%1];" : "=r"(v) : "l"(ws + i));
+    return v;
+  };
+  if (!kChecked) {  // the grain's stream (~1 KiB at most for codes <= 8 bits) into L2 ahead of the reader
+    const uint8_t* g0 = s + ((start >> 3) & ~static_cast<uint64_t>(127));
+#pragma unroll
+    for (int k = 1; k < 8; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(g0 + 128 * k));
+  }
+  const uint32_t lut = static_cast<uint32_t>(__cvta_generic_to_shared(t->lut));
+  unsigned long long acc = word(wi++);
+  uint32_t nw = word(wi++);
+  acc >>= (start & 31);
+  uint32_t nb = 32 - static_cast<uint32_t>(start & 31);
+  bool ok = true;
+  auto sym1 = [&]() -> uint32_t {
+    if (nb < 32) {
+      acc |= static_cast<unsigned long long>(nw) << nb;
+      nb += 32;
+      nw = word(wi++);
+    }
+    uint32_t e;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut + 2u * static_cast<uint32_t>(acc & ((1u << ZC_HUFF_ROOT_BITS) - 1))));
+    uint32_t l = e >> 8, sym = e & 0xFFu;
+    if (l == 0) {
+      l = huff_long(t, acc, sym);
+      if (l == 0) {
+        ok = false;
+        l = 1;  // keep the reader moving; the grain is reported undecodable
+      }
+    }
+    acc >>= l;
+    nb -= l;
+    return sym;
+  };
+  const uint32_t ng = n / 16;
+  for (uint32_t gq = 0; gq < ng; ++gq) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t o = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o |= sym1() << (8 * k);
+      w[q] = o;
+    }
+    emit16(sink, ob + 16ull * gq, w, 16, err);
+  }
+  if (n & 15) {
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j)
+      if (j < (n & 15)) w[j >> 2] |= sym1() << (8 * (j & 3));
+    emit16(sink, ob + 16ull * ng, w, n & 15, err);
+  }
+  // words [start>>5, wi-1) have entered the window; nb of their bits are unconsumed
+  const uint64_t pos = (wi - 1) * 32 - nb;
+  *end = pos;
+  return ok && pos <= slen * 8;
+}
+
 // Decode tables for a Huffman frame into shared memory: the embedded codebook rebuilt (with the
 // reference's validation) or a copy of the shared context.  All threads call.
 template <bool kCoherent>
@@ -370,7 +464,14 @@ __device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* pay
         unsigned long long lo = 0, hi = 0;
         uint64_t endb = 0;
         const uint64_t start = ld32<kCoherent>(idx + g);
-        bool good = huff_run<kCoherent>(s_t, s, slen, start, n, &endb, [&](uint64_t j, uint32_t sym) {
+        bool good;
+        // unchecked 16-byte reads only where even a corrupt grain cannot leave the payload: a
+        // grain consumes <= 1024 codes x 32 bits, the reader runs <= 384 bits ahead
+        if ((reinterpret_cast<uintptr_t>(s) & 3) == 0 && start + 32768 + 1024 <= slen * 8)
+          good = huff_grain<kCoherent, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
+        else if ((reinterpret_cast<uintptr_t>(s) & 3) == 0)
+          good = huff_grain<kCoherent, true>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
+        else good = huff_run<kCoherent>(s_t, s, slen, start, n, &endb, [&](uint64_t j, uint32_t sym) {
           const uint32_t k = static_cast<uint32_t>(j & 15);
           if (k < 8) lo |= static_cast<unsigned long long>(sym) << (8 * k);
           else hi |= static_cast<unsigned long long>(sym) << (8 * (k - 8));
