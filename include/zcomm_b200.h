@@ -356,6 +356,31 @@ int zc_comm_reduce_scatter_sym(zc_comm* comm, int32_t* d_sym, uint64_t count, vo
 int zc_comm_allgather_sym(zc_comm* comm, int32_t* d_all, uint64_t block, void* stream);
 /* RankCtx::allreduce_max (collectives.cpp:398-421). */
 int zc_comm_allreduce_max(zc_comm* comm, double v, double* h_out, void* stream);
+/* RankCtx::alltoall (collectives.cpp:546-567): d_send / d_recv hold nranks*block symbols; block j of
+ * d_send goes to rank j, block j of d_recv comes from rank j (zc_comm_alltoall_sym copies the own
+ * block).  Frames use cfg.pin. */
+int zc_comm_alltoall_sym(zc_comm* comm, const int32_t* d_send, int32_t* d_recv, uint64_t block, void* stream);
+/* RankCtx::broadcast (collectives.cpp:569-591): root's d_data to every rank along the ring, in place;
+ * a root outside [0, nranks) is ZC_ERR_INVALID_ARGUMENT. */
+int zc_comm_broadcast_sym(zc_comm* comm, int32_t* d_data, uint64_t count, int32_t root, void* stream);
+/* CollectiveRequest / group_execute (collectives.hpp:94-105, collectives.cpp:593-616): requests run
+ * in order as one submission (one host wait at the end).  AllReduce: sym/count in place with
+ * mode/scale(in-out)/levels; AllGather: sym = this rank's block of `count`, recv = nranks*count;
+ * AllToAll: sym = nranks*count send symbols (count = block), recv = nranks*count; Broadcast:
+ * sym/count in place from root.  A request missing its buffer is ZC_ERR_INVALID_ARGUMENT (the reference's
+ * "request needs an output"). */
+enum { ZC_COLL_ALLREDUCE = 0, ZC_COLL_ALLGATHER = 1, ZC_COLL_ALLTOALL = 2, ZC_COLL_BROADCAST = 3 };
+typedef struct zc_coll_request {
+  int32_t op;
+  int32_t root;
+  int32_t mode;
+  uint32_t levels;
+  int32_t* sym;
+  int32_t* recv;
+  uint64_t count;
+  double scale;
+} zc_coll_request;
+int zc_comm_group_execute(zc_comm* comm, zc_coll_request* reqs, int32_t nreqs, void* stream);
 /* Waits for the rank's queued work, checks its device error word, and maps it to a status. */
 int zc_comm_sync(zc_comm* comm);
 /* Clean epoch after an aborted collective (Connection::reset_sim, transport.cpp:97-105). */
@@ -372,6 +397,11 @@ int zc_group_allreduce_eb_f32(zc_comm* const* comms, int nranks, const float* co
 int zc_group_reduce_scatter_sym(zc_comm* const* comms, int nranks, int32_t* const* d_syms, uint64_t count);
 int zc_group_allgather_sym(zc_comm* const* comms, int nranks, int32_t* const* d_alls, uint64_t block);
 int zc_group_allreduce_max(zc_comm* const* comms, int nranks, const double* h_vs, double* h_outs);
+int zc_group_alltoall_sym(zc_comm* const* comms, int nranks, const int32_t* const* d_sends, int32_t* const* d_recvs,
+                          uint64_t block);
+int zc_group_broadcast_sym(zc_comm* const* comms, int nranks, int32_t* const* d_datas, uint64_t count, int32_t root);
+/* group_execute on every rank (reqs[r] = rank r's request list, same ops in the same order). */
+int zc_group_execute(zc_comm* const* comms, int nranks, zc_coll_request* const* reqs, int32_t nreqs);
 
 #ifdef __cplusplus
 }

@@ -204,6 +204,17 @@ class Communicator {
   }
   void reduce_scatter(int32_t* d_sym, size_t count) { check(zc_comm_reduce_scatter_sym(h_.get(), d_sym, count, nullptr)); }
   void allgather(int32_t* d_all, size_t block) { check(zc_comm_allgather_sym(h_.get(), d_all, block, nullptr)); }
+  // RankCtx::alltoall / broadcast (collectives.cpp:546-591), device buffers.
+  void alltoall(const int32_t* d_send, int32_t* d_recv, size_t block) {
+    check(zc_comm_alltoall_sym(h_.get(), d_send, d_recv, block, nullptr));
+  }
+  void broadcast(int32_t* d_data, size_t count, int root) {
+    check(zc_comm_broadcast_sym(h_.get(), d_data, count, root, nullptr));
+  }
+  // group_execute (collectives.cpp:593-616): requests run in order as one submission.
+  void group_execute(std::vector<zc_coll_request>& reqs) {
+    check(zc_comm_group_execute(h_.get(), reqs.data(), static_cast<int32_t>(reqs.size()), nullptr));
+  }
   double allreduce_max(double v) {
     double o = 0;
     check(zc_comm_allreduce_max(h_.get(), v, &o, nullptr));

@@ -84,6 +84,14 @@ class WireStats(C.Structure):            # collectives.hpp:36-43
                 ("wall_codec_sec", C.c_double)]
 
 
+COLL_ALLREDUCE, COLL_ALLGATHER, COLL_ALLTOALL, COLL_BROADCAST = 0, 1, 2, 3  # CollOp, collectives.hpp:17
+
+
+class CollRequest(C.Structure):          # CollectiveRequest, collectives.hpp:94-101
+    _fields_ = [("op", C.c_int32), ("root", C.c_int32), ("mode", C.c_int32), ("levels", C.c_uint32),
+                ("sym", C.c_void_p), ("recv", C.c_void_p), ("count", C.c_uint64), ("scale", C.c_double)]
+
+
 class CollectiveConfig(C.Structure):     # collectives.hpp:24-34
     _fields_ = [("arb", ArbConfig), ("hint", TransportHint), ("pin", C.c_int32),
                 ("serialized", C.c_int32), ("fused_codec_min_msg_bytes", C.c_uint64)]

@@ -70,7 +70,7 @@ Layout make_layout(uint32_t nbanks, uint32_t runits) {
   o += align_up(8ull * nbanks, kAlign);
   L.off_sready = o;  // [kRegions] pieces received in region i (written by the predecessor)
   o += kAlign;
-  L.off_scredit = o;  // [kRegions] pieces consumed from the successor's region i (written by it)
+  L.off_scredit = o;  // [0]: pieces this rank has consumed from its regions (read by its senders)
   o += kAlign;
   L.off_err = o;
   o += kAlign;
@@ -130,7 +130,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-enum MailOp : int { MAIL_MAX = 0, MAIL_META = 1, MAIL_EB_SCALE = 2 };
+enum MailOp : int { MAIL_MAX = 0, MAIL_META = 1, MAIL_EB_SCALE = 2, MAIL_BARRIER = 3 };
 
 struct MailArgs {
   uint8_t* const* peers;  // device array: every rank's block base
@@ -185,6 +185,7 @@ __global__ void mailbox_kernel(MailArgs a) {
       __nanosleep(64);
     }
   }
+  if (a.op == MAIL_BARRIER) return;
   const uint8_t* mb = a.peers[a.rank] + a.off_mbox + par * kMaxRanks * 32;
   Scal* s = a.scal;
   if (a.op == MAIL_MAX || a.op == MAIL_EB_SCALE) {
@@ -502,14 +503,18 @@ void launch_wait(zc_comm* c, const unsigned long long* flag, unsigned long long 
   wait_geq_kernel<<<1, 1, 0, c->stream>>>(flag, v, c->d_peers, c->lay.off_err, c->rank, c->nranks, c->timeout_ns);
 }
 
-int send_piece(zc_comm* c, const int32_t* src, uint64_t bytes, int pin) {
+// Piece sequence numbers are the RECEIVER's: a sender's ptx equals its receiver's prx whenever the
+// two exchange (ring edges always do; the all-to-all resets every rank's counters first), so any
+// rank may send to any rank.  A region is reused once the receiver has consumed the piece that
+// last used it: the receiver publishes its consumed count in its own block (receiver-centric
+// credit), which stays correct when the sender into a rank changes from step to step.
+int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) {
   const Layout& y = c->lay;
-  const int next = (c->rank + 1) % c->nranks;
   const uint64_t seq = c->ptx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
-  if (seq >= kRegions)  // the successor has consumed the piece that last used this region
-    launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_scredit) + reg, seq - kRegions + 1);
-  uint8_t* dst = c->peer[next] + y.off_reg + reg * y.reg_stride;
+  if (seq >= kRegions)  // the receiver has consumed the piece that last used this region
+    launch_wait(c, reinterpret_cast<const unsigned long long*>(c->peer[to] + y.off_scredit), seq - kRegions + 1);
+  uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
   auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
   if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, dst, kStageStride, ZC_STAGE_BANK_BYTES, pin, &c->cfg.hint,
                                    c->shared, &c->cfg.arb, res, reinterpret_cast<uint32_t*>(dst + y.reg_idx),
@@ -518,7 +523,7 @@ int send_piece(zc_comm* c, const int32_t* src, uint64_t bytes, int pin) {
   note_launch();
   piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(bytes)), bytes,
                                              reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire),
-                                             reinterpret_cast<unsigned long long*>(c->peer[next] + y.off_sready) + reg,
+                                             reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg,
                                              seq + 1);
   return cuda_err(cudaGetLastError(), "piece send");
 }
@@ -528,7 +533,6 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
   // all are FixedLen / RAW and the general decode kernels are skipped
   const bool own = c->shared == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN;
   const Layout& y = c->lay;
-  const int prev = (c->rank - 1 + c->nranks) % c->nranks;
   const uint64_t seq = c->prx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
   launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1);
@@ -539,22 +543,28 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
                                    dst, 1.0, nullptr, c->err_word(), c->stream, own ? 1 : 0))
     return rc;
   note_launch();
-  piece_done_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(c->peer[prev] + y.off_scredit) + reg,
-                                            seq + 1);
+  piece_done_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(c->block + y.off_scredit), seq + 1);
   return cuda_err(cudaGetLastError(), "piece recv");
 }
 
-int staged_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin, bool store) {
+// One exchange (BatchIo::exchange, collectives.cpp:366-396): `tx` to rank `to`, `rx` from whoever
+// sends to this rank, in pieces; sends run one piece ahead of receives.
+int staged_xfer(zc_comm* c, int to, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin,
+                bool store) {
   const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * ZC_BATCH_RAW_BYTES;
   const uint64_t ns = (tx_bytes + pb - 1) / pb, nr = (rx_bytes + pb - 1) / pb;
   const uint64_t steps = std::max(ns, nr) + 1;
   for (uint64_t k = 0; k < steps; ++k) {
     if (k < ns)
-      if (int rc = send_piece(c, tx + k * (pb / 4), std::min(pb, tx_bytes - k * pb), pin)) return rc;
+      if (int rc = send_piece(c, to, tx + k * (pb / 4), std::min(pb, tx_bytes - k * pb), pin)) return rc;
     if (k >= 1 && k - 1 < nr)
       if (int rc = recv_piece(c, rx + (k - 1) * (pb / 4), std::min(pb, rx_bytes - (k - 1) * pb), store, pin)) return rc;
   }
   return ZC_OK;
+}
+
+int staged_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin, bool store) {
+  return staged_xfer(c, (c->rank + 1) % c->nranks, tx, tx_bytes, rx, rx_bytes, pin, store);
 }
 
 bool use_staged() { return std::getenv("ZC_RING_KERNEL") == nullptr; }
@@ -611,6 +621,61 @@ int enqueue_allgather(zc_comm* c, int32_t* d_all, uint64_t block) {
     } else if (int rc = exchange_step(c, sb, by, rb, by, c->cfg.pin, true, "ag-step")) {
       return rc;
     }
+  }
+  return ZC_OK;
+}
+
+// Every rank's piece counters back to zero (the all-to-all's precondition: any rank may send to any
+// rank, so senders' and receivers' counts must agree globally, which a broadcast does not keep).
+// barrier -> zero own piece flags -> barrier: between the barriers no rank touches any flag.
+int resync_pieces(zc_comm* c) {
+  if (int rc = launch_mail(c, MAIL_BARRIER, nullptr, 0, 0.0)) return rc;
+  const Layout& y = c->lay;
+  if (int rc = cuda_err(cudaMemsetAsync(c->block + y.off_sready, 0, y.off_err - y.off_sready, c->stream), "resync"))
+    return rc;
+  c->ptx = c->prx = 0;
+  return launch_mail(c, MAIL_BARRIER, nullptr, 0, 0.0);
+}
+
+// All-to-all of equal blocks (collectives.cpp:546-567): own block copied, then step r = 1..n-1
+// sends block (rank+r) to rank+r and receives block (rank-r) from rank-r, each an exchange of
+// compressed frames (cfg.pin) straight into the peer's regions.
+int enqueue_alltoall(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_t block) {
+  const int n = c->nranks, r = c->rank;
+  const uint64_t by = block * 4;
+  if (by)
+    if (int rc = cuda_err(cudaMemcpyAsync(d_recv + static_cast<uint64_t>(r) * block, d_send + static_cast<uint64_t>(r) * block,
+                                          by, cudaMemcpyDeviceToDevice, c->stream), "alltoall self"))
+      return rc;
+  if (n == 1 || block == 0) return ZC_OK;
+  if (int rc = resync_pieces(c)) return rc;
+  for (int t = 1; t < n; ++t) {
+    const int to = (r + t) % n, from = (r - t + n) % n;
+    if (int rc = staged_xfer(c, to, d_send + static_cast<uint64_t>(to) * block, by,
+                             d_recv + static_cast<uint64_t>(from) * block, by, c->cfg.pin, true))
+      return rc;
+  }
+  return ZC_OK;
+}
+
+// Broadcast along the ring from `root` (collectives.cpp:569-591): the root sends the message, the
+// last rank of the chain receives it, every rank in between stores each piece and forwards it
+// (store-and-forward per piece keeps the chain pipelined).  Forwarded frames are re-encoded from
+// the stored bytes, so every hop ships the frame the reference would.  Only ring edges carry
+// pieces, so the piece counters stay consistent for the ring collectives.
+int enqueue_broadcast(zc_comm* c, int32_t* d_data, uint64_t count, int root) {
+  const int n = c->nranks;
+  if (n == 1 || count == 0) return ZC_OK;
+  const int pos = (c->rank - root + n) % n, next = (c->rank + 1) % n;
+  const uint64_t by = count * 4;
+  const int pin = c->cfg.pin;
+  if (pos == 0) return staged_xfer(c, next, d_data, by, nullptr, 0, pin, true);
+  if (pos == n - 1) return staged_xfer(c, next, nullptr, 0, d_data, by, pin, true);
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * ZC_BATCH_RAW_BYTES;
+  for (uint64_t off = 0; off < by; off += pb) {
+    const uint64_t len = std::min(pb, by - off);
+    if (int rc = recv_piece(c, d_data + off / 4, len, true, pin)) return rc;
+    if (int rc = send_piece(c, next, d_data + off / 4, len, pin)) return rc;
   }
   return ZC_OK;
 }
@@ -680,6 +745,45 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
 }
 
 // Maps a device error word to the reference's exception kinds (root cause first).
+// group_execute's dispatch (collectives.cpp:593-616): one request, enqueued on the comm stream.
+int check_requests(zc_comm* c, const zc_coll_request* reqs, int nreqs) {
+  for (int i = 0; i < nreqs; ++i) {
+    const zc_coll_request& q = reqs[i];
+    if (q.op < ZC_COLL_ALLREDUCE || q.op > ZC_COLL_BROADCAST) return set_err(ZC_ERR_INVALID_ARGUMENT, "unknown collective op");
+    if (q.count > 0 && q.sym == nullptr) return set_err(ZC_ERR_INVALID_ARGUMENT, "request needs its symbols");
+    if ((q.op == ZC_COLL_ALLGATHER || q.op == ZC_COLL_ALLTOALL) && q.recv == nullptr)
+      return set_err(ZC_ERR_INVALID_ARGUMENT, q.op == ZC_COLL_ALLGATHER ? "allgather request needs an output"
+                                                                        : "alltoall request needs an output");
+    if (q.op == ZC_COLL_BROADCAST && c->nranks > 1 && q.count > 0 && (q.root < 0 || q.root >= c->nranks))
+      return set_err(ZC_ERR_INVALID_ARGUMENT, "broadcast root out of range");
+  }
+  return ZC_OK;
+}
+
+int enqueue_request(zc_comm* c, const zc_coll_request& q) {
+  switch (q.op) {
+    case ZC_COLL_ALLREDUCE:
+      return enqueue_allreduce_sym(c, q.sym, q.count, q.mode, q.scale, q.levels);
+    case ZC_COLL_ALLGATHER:
+      if (q.count)
+        if (int rc = cuda_err(cudaMemcpyAsync(q.recv + static_cast<uint64_t>(c->rank) * q.count, q.sym, q.count * 4,
+                                              cudaMemcpyDeviceToDevice, c->stream), "allgather self"))
+          return rc;
+      if (c->nranks == 1 || q.count == 0) return ZC_OK;
+      return enqueue_allgather(c, q.recv, q.count);
+    case ZC_COLL_ALLTOALL:
+      return enqueue_alltoall(c, q.sym, q.recv, q.count);
+    default:
+      return enqueue_broadcast(c, q.sym, q.count, q.root);
+  }
+}
+
+void read_back_scales(zc_comm* c, zc_coll_request* reqs, int nreqs) {
+  for (int i = 0; i < nreqs; ++i)
+    if (reqs[i].op == ZC_COLL_ALLREDUCE && c->nranks > 1 && reqs[i].count > 0)
+      cudaMemcpy(&reqs[i].scale, &c->scal()->scale, 8, cudaMemcpyDeviceToHost);
+}
+
 int status_from_err(uint32_t e) {
   if (!e) return ZC_OK;
   if (e & ZC_DERR_OVERFLOW) return set_err(ZC_ERR_OVERFLOW, "symbol sum exceeds 32-bit range");
@@ -760,6 +864,32 @@ int finalize_peers(zc_comm* c) {
   if (!rc) rc = cuda_err(cudaMemcpy(c->d_peers, c->peer.data(), 8ull * c->nranks, cudaMemcpyHostToDevice), "peer table");
   if (!rc) c->connected = true;
   return rc;
+}
+
+int finish(zc_comm* c);
+int reset_state(zc_comm* c);
+
+// Single-process group: every rank's work enqueued before any is awaited (ranks' kernels must run
+// concurrently), then one wait per rank; on failure every rank is reset.
+template <typename F>
+int run_group(zc_comm* const* cs, int n, F enqueue) {
+  int first = ZC_OK;
+  for (int r = 0; r < n && !first; ++r) {
+    if ((first = dev_guard(cs[r]))) break;
+    if ((first = order_after(cs[r], nullptr))) break;
+    first = enqueue(r);
+  }
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    int e = finish(cs[r]);
+    if (!first && e) first = e;
+  }
+  if (first) {
+    std::string msg = zc_last_error();
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+  }
+  return first;
 }
 
 int reset_state(zc_comm* c) {
@@ -944,6 +1074,37 @@ int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
   return rc;
 }
 
+int zc_comm_alltoall_sym(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_t block, void* stream) {
+  if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
+  if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = enqueue_alltoall(c, d_send, d_recv, block)) return rc;
+  return finish(c);
+}
+
+int zc_comm_broadcast_sym(zc_comm* c, int32_t* d_data, uint64_t count, int32_t root, void* stream) {
+  if (c->nranks == 1 || count == 0) return ZC_OK;
+  if (root < 0 || root >= c->nranks) return set_err(ZC_ERR_INVALID_ARGUMENT, "broadcast root out of range");
+  if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
+  if (!c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = enqueue_broadcast(c, d_data, count, root)) return rc;
+  return finish(c);
+}
+
+int zc_comm_group_execute(zc_comm* c, zc_coll_request* reqs, int32_t nreqs, void* stream) {
+  if (nreqs < 0 || (nreqs > 0 && reqs == nullptr)) return set_err(ZC_ERR_INVALID_ARGUMENT, "bad request list");
+  if (int rc = check_requests(c, reqs, nreqs)) return rc;
+  if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
+  if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  for (int i = 0; i < nreqs; ++i)
+    if (int rc = enqueue_request(c, reqs[i])) return rc;
+  int rc = finish(c);
+  if (!rc) read_back_scales(c, reqs, nreqs);
+  return rc;
+}
+
 int zc_comm_sync(zc_comm* c) {
   if (int rc = dev_guard(c)) return rc;
   return finish(c);
@@ -1115,6 +1276,30 @@ int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* 
     if (!e) cudaMemcpy(&outs[r], &cs[r]->scal()->out, 8, cudaMemcpyDeviceToHost);
   }
   return first;
+}
+
+int zc_group_alltoall_sym(zc_comm* const* cs, int n, const int32_t* const* d_sends, int32_t* const* d_recvs,
+                          uint64_t block) {
+  return run_group(cs, n, [&](int r) { return enqueue_alltoall(cs[r], d_sends[r], d_recvs[r], block); });
+}
+
+int zc_group_broadcast_sym(zc_comm* const* cs, int n, int32_t* const* d_datas, uint64_t count, int32_t root) {
+  if (n == 1 || count == 0) return ZC_OK;
+  if (root < 0 || root >= n) return set_err(ZC_ERR_INVALID_ARGUMENT, "broadcast root out of range");
+  return run_group(cs, n, [&](int r) { return enqueue_broadcast(cs[r], d_datas[r], count, root); });
+}
+
+int zc_group_execute(zc_comm* const* cs, int n, zc_coll_request* const* reqs, int32_t nreqs) {
+  for (int r = 0; r < n; ++r)
+    if (int rc = check_requests(cs[r], reqs[r], nreqs)) return rc;
+  int rc = run_group(cs, n, [&](int r) {
+    for (int i = 0; i < nreqs; ++i)
+      if (int e = enqueue_request(cs[r], reqs[r][i])) return e;
+    return ZC_OK;
+  });
+  if (!rc)
+    for (int r = 0; r < n; ++r) read_back_scales(cs[r], reqs[r], nreqs);
+  return rc;
 }
 
 }  // extern "C"

@@ -137,6 +137,12 @@ def lib():
     _sig(L, "zc_group_reduce_scatter_sym", C.c_int, P(vp), C.c_int, P(vp), u64)
     _sig(L, "zc_group_allgather_sym", C.c_int, P(vp), C.c_int, P(vp), u64)
     _sig(L, "zc_group_allreduce_max", C.c_int, P(vp), C.c_int, P(dbl), P(dbl))
+    _sig(L, "zc_comm_alltoall_sym", C.c_int, vp, vp, vp, u64, vp)
+    _sig(L, "zc_comm_broadcast_sym", C.c_int, vp, vp, u64, i32, vp)
+    _sig(L, "zc_comm_group_execute", C.c_int, vp, P(abi.CollRequest), i32, vp)
+    _sig(L, "zc_group_alltoall_sym", C.c_int, P(vp), C.c_int, P(vp), P(vp), u64)
+    _sig(L, "zc_group_broadcast_sym", C.c_int, P(vp), C.c_int, P(vp), u64, i32)
+    _sig(L, "zc_group_execute", C.c_int, P(vp), C.c_int, P(P(abi.CollRequest)), i32)
     _lib = L
     return L
 
@@ -553,6 +559,21 @@ def collective_config(pin: int = abi.PIN_AUTO, **kw) -> abi.CollectiveConfig:
     return c
 
 
+def _request(q: dict) -> abi.CollRequest:
+    """A CollectiveRequest (collectives.hpp:94-101) from a dict: op, sym (int32 tensor), and per op
+    recv (AllGather: nranks*block, AllToAll: like sym), root (Broadcast), scale/mode/levels
+    (AllReduce).  count: the block (AllGather/AllToAll per-rank block) or the symbol count."""
+    op = q["op"]
+    sym = q.get("sym")
+    recv = q.get("recv")
+    count = q.get("count")
+    if count is None:
+        count = 0 if sym is None else (sym.numel() if op != abi.COLL_ALLTOALL else sym.numel() // q["nranks"])
+    return abi.CollRequest(op, q.get("root", 0), q.get("mode", abi.QUANT_ERROR_BOUNDED), q.get("levels", 0),
+                           None if sym is None else sym.data_ptr(), None if recv is None else recv.data_ptr(),
+                           count, float(q.get("scale", 1.0)))
+
+
 class Group:
     """A single-process Communicator (collectives.cpp:66-190): nranks ranks on local devices
     (several ranks may share one GPU), every collective runs all ranks concurrently, like the
@@ -605,6 +626,36 @@ class Group:
             outs.append(o)
         check(lib().zc_group_allgather_sym(self._h, n, self._ptrs(outs), blocks[0].numel()))
         return outs
+
+    def alltoall(self, sends: Sequence[torch.Tensor]):
+        """RankCtx::alltoall (collectives.cpp:546-567) on every rank: block j of rank r's send goes
+        to rank j; returns each rank's received buffer."""
+        n = self.nranks
+        block = sends[0].numel() // n
+        for t in sends:
+            if t.numel() != block * n:
+                raise ValueError("alltoall buffer must split evenly across ranks")
+        outs = [torch.empty_like(t) for t in sends]
+        check(lib().zc_group_alltoall_sym(self._h, n, self._ptrs(sends), self._ptrs(outs), block))
+        return outs
+
+    def broadcast(self, datas: Sequence[torch.Tensor], root: int):
+        """RankCtx::broadcast (collectives.cpp:569-591) on every rank, in place."""
+        check(lib().zc_group_broadcast_sym(self._h, self.nranks, self._ptrs(datas), datas[0].numel(), root))
+
+    def group_execute(self, requests: Sequence[Sequence[dict]]):
+        """group_execute (collectives.cpp:593-616): requests[r] is rank r's list; see
+        make_requests.  Returns the requests with outputs (recv tensors, reconciled scales)."""
+        n = self.nranks
+        k = len(requests[0])
+        arrs = [(abi.CollRequest * k)(*[_request(q) for q in requests[r]]) for r in range(n)]
+        ptrs = (C.POINTER(abi.CollRequest) * n)(*[C.cast(a, C.POINTER(abi.CollRequest)) for a in arrs])
+        check(lib().zc_group_execute(self._h, n, ptrs, k))
+        for r in range(n):
+            for i, q in enumerate(requests[r]):
+                if q["op"] == abi.COLL_ALLREDUCE:
+                    q["scale"] = arrs[r][i].scale
+        return requests
 
     def allreduce_max(self, vs: Sequence[float]):
         a = (C.c_double * self.nranks)(*vs)
@@ -678,6 +729,25 @@ class Communicator:
 
     def allgather(self, all_blocks: torch.Tensor, block: int):
         check(lib().zc_comm_allgather_sym(self._h, _ptr(all_blocks), block, _stream()))
+
+    def alltoall(self, send: torch.Tensor) -> torch.Tensor:
+        if send.numel() % self.nranks:
+            raise ValueError("alltoall buffer must split evenly across ranks")
+        out = torch.empty_like(send)
+        check(lib().zc_comm_alltoall_sym(self._h, _ptr(send), _ptr(out), send.numel() // self.nranks, _stream()))
+        return out
+
+    def broadcast(self, data: torch.Tensor, root: int):
+        check(lib().zc_comm_broadcast_sym(self._h, _ptr(data), data.numel(), root, _stream()))
+
+    def group_execute(self, requests: Sequence[dict]):
+        k = len(requests)
+        arr = (abi.CollRequest * k)(*[_request(q) for q in requests])
+        check(lib().zc_comm_group_execute(self._h, arr, k, _stream()))
+        for i, q in enumerate(requests):
+            if q["op"] == abi.COLL_ALLREDUCE:
+                q["scale"] = arr[i].scale
+        return requests
 
     def allreduce_max(self, v: float) -> float:
         o = C.c_double()
