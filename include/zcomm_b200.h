@@ -381,6 +381,29 @@ typedef struct zc_coll_request {
   double scale;
 } zc_coll_request;
 int zc_comm_group_execute(zc_comm* comm, zc_coll_request* reqs, int32_t nreqs, void* stream);
+/* Measured send/receive timeline of the staged ring path (the B200 counterpart of the modelled
+ * BatchTimelineRow / write_timeline_csv, pipeline.hpp:32-46, pipeline.cpp:160-170): CUDA events on
+ * the communicator stream around every piece.  Send rows (kind 0) are per 4 MiB batch: the piece's
+ * encode, whose stores ARE the NVLink transfer, from launch to publication (start/end), with the
+ * frame's codec and total bytes.  Receive rows (kind 1) are per piece: wait start, frame arrival
+ * (ready) and decode end.  Times are seconds since zc_comm_timeline_enable.  max_pieces = 0
+ * disables; rows beyond the capacity are dropped. */
+typedef struct zc_timeline_row {
+  uint64_t seq;       /* piece sequence number (the receiver's count; sender and receiver agree) */
+  int32_t kind;       /* 0 send, 1 receive */
+  int32_t peer;       /* rank sent to / received from (-1: any) */
+  uint32_t batch;     /* batch within the piece (send rows) */
+  uint32_t codec;     /* ZC_CODEC_* of the frame (send rows); 0xFF for receive rows */
+  uint64_t raw_bytes;
+  uint64_t total_bytes; /* frame bytes (send rows); 0 for receive rows */
+  double start_sec, ready_sec, end_sec;
+} zc_timeline_row;
+int zc_comm_timeline_enable(zc_comm* comm, int32_t max_pieces);
+/* Rows recorded so far (waits for the rank's queued work): *n_rows = the row count, at most cap
+ * of them written to rows (rows may be NULL with cap 0). */
+int zc_comm_timeline_rows(zc_comm* comm, zc_timeline_row* rows, int32_t cap, int32_t* n_rows);
+/* Seconds from a's timeline origin to b's (both enabled on the same device). */
+int zc_comm_timeline_origin_delta(zc_comm* a, zc_comm* b, double* sec);
 /* Waits for the rank's queued work, checks its device error word, and maps it to a status. */
 int zc_comm_sync(zc_comm* comm);
 /* Clean epoch after an aborted collective (Connection::reset_sim, transport.cpp:97-105). */

@@ -92,6 +92,12 @@ class CollRequest(C.Structure):          # CollectiveRequest, collectives.hpp:94
                 ("sym", C.c_void_p), ("recv", C.c_void_p), ("count", C.c_uint64), ("scale", C.c_double)]
 
 
+class TimelineRow(C.Structure):          # zc_timeline_row (measured BatchTimelineRow, pipeline.hpp:32-46)
+    _fields_ = [("seq", C.c_uint64), ("kind", C.c_int32), ("peer", C.c_int32), ("batch", C.c_uint32),
+                ("codec", C.c_uint32), ("raw_bytes", C.c_uint64), ("total_bytes", C.c_uint64),
+                ("start_sec", C.c_double), ("ready_sec", C.c_double), ("end_sec", C.c_double)]
+
+
 class CollectiveConfig(C.Structure):     # collectives.hpp:24-34
     _fields_ = [("arb", ArbConfig), ("hint", TransportHint), ("pin", C.c_int32),
                 ("serialized", C.c_int32), ("fused_codec_min_msg_bytes", C.c_uint64)]

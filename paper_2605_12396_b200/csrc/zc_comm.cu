@@ -305,10 +305,12 @@ __global__ void wait_geq_kernel(const unsigned long long* flag, unsigned long lo
 // After a piece's frames are in the successor's region: count them into this rank's WireStats
 // (send_batch's accounting, collectives.cpp:285-296) and publish the piece (system-scope release).
 __global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, uint64_t raw_total,
-                                  zc_wire_stats* wire, unsigned long long* remote_ready, unsigned long long v) {
+                                  zc_wire_stats* wire, unsigned long long* remote_ready, unsigned long long v,
+                                  zc_encode_result* log) {
   unsigned long long f[3] = {0, 0, 0}, raw = 0, pay = 0, tot = 0, idx = 0;
   for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
     const zc_encode_result r = res[u];
+    if (log) log[u] = r;
     if (r.total_bytes == 0) continue;  // capacity failure: reported through the error word
     const uint64_t R = (raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES < ZC_BATCH_RAW_BYTES ? raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES : static_cast<uint64_t>(ZC_BATCH_RAW_BYTES));
     f[r.codec < 3 ? r.codec : 0] += 1;
@@ -373,6 +375,17 @@ struct zc_comm {
   int32_t* sym = nullptr;          // symbol scratch for allreduce_eb
   uint64_t sym_cap = 0;
   unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+  // measured timeline (zc_comm_timeline_enable): one record per piece, events on `stream`
+  struct TlPiece {
+    uint64_t seq, bytes;
+    int kind, peer;
+    uint32_t nunits;
+    cudaEvent_t e0, e1, e2;
+  };
+  int tl_cap = 0;
+  std::vector<TlPiece> tl;
+  cudaEvent_t tl_t0 = nullptr;
+  zc_encode_result* tl_res = nullptr;  // device log of every sent piece's EncodeResults
 
   Scal* scal() const { return reinterpret_cast<Scal*>(block + lay.off_scal); }
   uint32_t* err_word() const { return reinterpret_cast<uint32_t*>(block + lay.off_err); }
@@ -508,12 +521,26 @@ void launch_wait(zc_comm* c, const unsigned long long* flag, unsigned long long 
 // rank may send to any rank.  A region is reused once the receiver has consumed the piece that
 // last used it: the receiver publishes its consumed count in its own block (receiver-centric
 // credit), which stays correct when the sender into a rank changes from step to step.
+// Timeline records (no-ops unless zc_comm_timeline_enable): events around a piece.
+zc_comm::TlPiece* tl_begin(zc_comm* c, int kind, int peer, uint64_t seq, uint64_t bytes) {
+  if (c->tl_cap == 0 || static_cast<int>(c->tl.size()) >= c->tl_cap) return nullptr;
+  zc_comm::TlPiece t{seq, bytes, kind, peer, static_cast<uint32_t>(nbatches(bytes)), nullptr, nullptr, nullptr};
+  cudaEventCreate(&t.e0);
+  cudaEventCreate(&t.e1);
+  cudaEventCreate(&t.e2);
+  c->tl.push_back(t);
+  return &c->tl.back();
+}
+
 int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) {
   const Layout& y = c->lay;
+  zc_comm::TlPiece* tl = tl_begin(c, 0, to, c->ptx, bytes);
+  zc_encode_result* log = tl ? c->tl_res + (c->tl.size() - 1) * y.runits : nullptr;
   const uint64_t seq = c->ptx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
   if (seq >= kRegions)  // the receiver has consumed the piece that last used this region
     launch_wait(c, reinterpret_cast<const unsigned long long*>(c->peer[to] + y.off_scredit), seq - kRegions + 1);
+  if (tl) cudaEventRecord(tl->e0, c->stream);
   uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
   auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
   if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, dst, kStageStride, ZC_STAGE_BANK_BYTES, pin, &c->cfg.hint,
@@ -524,7 +551,8 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
   piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(bytes)), bytes,
                                              reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire),
                                              reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg,
-                                             seq + 1);
+                                             seq + 1, log);
+  if (tl) cudaEventRecord(tl->e1, c->stream);
   return cuda_err(cudaGetLastError(), "piece send");
 }
 
@@ -533,9 +561,12 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
   // all are FixedLen / RAW and the general decode kernels are skipped
   const bool own = c->shared == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN;
   const Layout& y = c->lay;
+  zc_comm::TlPiece* tl = tl_begin(c, 1, -1, c->prx, bytes);
+  if (tl) cudaEventRecord(tl->e0, c->stream);
   const uint64_t seq = c->prx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
   launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1);
+  if (tl) cudaEventRecord(tl->e1, c->stream);
   const uint8_t* region = c->block + y.off_reg + reg * y.reg_stride;
   if (int rc = zc_i_decode_batches(region, kStageStride, ZC_STAGE_BANK_BYTES,
                                    reinterpret_cast<const zc_encode_result*>(region + y.reg_res), bytes, c->shared,
@@ -544,6 +575,7 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
     return rc;
   note_launch();
   piece_done_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(c->block + y.off_scredit), seq + 1);
+  if (tl) cudaEventRecord(tl->e2, c->stream);
   return cuda_err(cudaGetLastError(), "piece recv");
 }
 
@@ -998,6 +1030,13 @@ void zc_comm_destroy(zc_comm* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->shared) zc_huff_ctx_destroy(c->shared);
+  for (auto& t : c->tl) {
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+    cudaEventDestroy(t.e2);
+  }
+  if (c->tl_res) cudaFree(c->tl_res);
+  if (c->tl_t0) cudaEventDestroy(c->tl_t0);
   delete c;
 }
 
@@ -1103,6 +1142,88 @@ int zc_comm_group_execute(zc_comm* c, zc_coll_request* reqs, int32_t nreqs, void
   int rc = finish(c);
   if (!rc) read_back_scales(c, reqs, nreqs);
   return rc;
+}
+
+int zc_comm_timeline_enable(zc_comm* c, int32_t max_pieces) {
+  if (max_pieces < 0) return set_err(ZC_ERR_INVALID_ARGUMENT, "max_pieces must be >= 0");
+  if (int rc = dev_guard(c)) return rc;
+  cudaStreamSynchronize(c->stream);
+  for (auto& t : c->tl) {
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+    cudaEventDestroy(t.e2);
+  }
+  c->tl.clear();
+  c->tl.reserve(static_cast<size_t>(max_pieces));
+  if (c->tl_res) cudaFree(c->tl_res);
+  c->tl_res = nullptr;
+  c->tl_cap = 0;
+  if (max_pieces == 0) return ZC_OK;
+  if (int rc = cuda_err(cudaMalloc(&c->tl_res, sizeof(zc_encode_result) * c->lay.runits * max_pieces), "timeline log"))
+    return rc;
+  if (!c->tl_t0) cudaEventCreate(&c->tl_t0);
+  cudaEventRecord(c->tl_t0, c->stream);
+  c->tl_cap = max_pieces;
+  return ZC_OK;
+}
+
+int zc_comm_timeline_rows(zc_comm* c, zc_timeline_row* rows, int32_t cap, int32_t* n_rows) {
+  *n_rows = 0;
+  if (int rc = dev_guard(c)) return rc;
+  if (int rc = cuda_err(cudaStreamSynchronize(c->stream), "timeline sync")) return rc;
+  if (c->tl_cap == 0) return ZC_OK;
+  std::vector<zc_encode_result> log(static_cast<size_t>(c->lay.runits) * c->tl.size());
+  if (!log.empty())
+    if (int rc = cuda_err(cudaMemcpy(log.data(), c->tl_res, sizeof(zc_encode_result) * log.size(), cudaMemcpyDeviceToHost),
+                          "timeline log"))
+      return rc;
+  auto sec = [&](cudaEvent_t e) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->tl_t0, e);
+    return static_cast<double>(ms) * 1e-3;
+  };
+  int n = 0;
+  for (size_t i = 0; i < c->tl.size(); ++i) {
+    const auto& t = c->tl[i];
+    const double a = sec(t.e0), b = sec(t.e1);
+    const uint32_t nr = t.kind == 0 ? t.nunits : 1u;
+    for (uint32_t u = 0; u < nr; ++u, ++n) {
+      if (n >= cap) continue;
+      zc_timeline_row& r = rows[n];
+      r.seq = t.seq;
+      r.kind = t.kind;
+      r.peer = t.peer;
+      r.batch = u;
+      if (t.kind == 0) {
+        const zc_encode_result& e = log[i * c->lay.runits + u];
+        const uint64_t off = static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES;
+        r.codec = e.codec;
+        r.raw_bytes = std::min<uint64_t>(ZC_BATCH_RAW_BYTES, t.bytes - off);
+        r.total_bytes = e.total_bytes;
+        r.start_sec = a;
+        r.ready_sec = a;
+        r.end_sec = b;
+      } else {
+        r.codec = 0xFF;
+        r.raw_bytes = t.bytes;
+        r.total_bytes = 0;
+        r.start_sec = a;
+        r.ready_sec = b;
+        r.end_sec = sec(t.e2);
+      }
+    }
+  }
+  *n_rows = n;
+  return ZC_OK;
+}
+
+int zc_comm_timeline_origin_delta(zc_comm* a, zc_comm* b, double* out) {
+  if (!a->tl_t0 || !b->tl_t0) return set_err(ZC_ERR_LOGIC, "timeline not enabled");
+  if (int rc = dev_guard(a)) return rc;
+  float ms = 0.f;
+  if (int rc = cuda_err(cudaEventElapsedTime(&ms, a->tl_t0, b->tl_t0), "timeline origin")) return rc;
+  *out = static_cast<double>(ms) * 1e-3;
+  return ZC_OK;
 }
 
 int zc_comm_sync(zc_comm* c) {

@@ -168,3 +168,43 @@ def emit_markdown(rows: Sequence[ReportRow]) -> str:
                    f"{QUANTS[r.quant]} | {_g(r.sim_time_sec, 6)} | {r.cr_final:.3f} | "
                    f"{_g(r.bus_bw_bytes_per_sec, 4)} | {r.speedup_vs_raw:.3f} |\n")
     return "".join(out)
+
+
+TIMELINE_HEADER = ("batch,codec,raw_bytes,total_bytes,enc_start_sec,enc_end_sec,"
+                   "xfer_start_sec,xfer_end_sec,dec_start_sec,dec_end_sec")
+CODEC_NAMES = {0: "raw", 1: "fixedlen", 2: "huffman"}                   # codec_name (frame.hpp:20-26)
+
+
+def emit_timeline_csv(rows: Sequence[dict]) -> str:
+    """write_timeline_csv (pipeline.cpp:160-170): header, then one line per batch with the times
+    at setprecision(9).  Rows come from Group.timeline() — MEASURED with CUDA events on B200, where
+    the reference's rows are its modelled schedule; batch ids number the rows in order."""
+    out = [TIMELINE_HEADER + "\n"]
+    for i, r in enumerate(rows):
+        out.append(",".join([str(i), CODEC_NAMES.get(r["codec"], "raw"), str(r["raw_bytes"]), str(r["total_bytes"])] +
+                            [_g(r[k], 9) for k in ("enc_start_sec", "enc_end_sec", "xfer_start_sec", "xfer_end_sec",
+                                                   "dec_start_sec", "dec_end_sec")]) + "\n")
+    return "".join(out)
+
+
+def overlap_summary(rows: Sequence[dict]) -> dict:
+    """How much of the codec work the pipeline hides: the union of all encode intervals and of all
+    decode intervals against the collective's span (first encode start to last decode end)."""
+    def union(iv):
+        iv = sorted(iv)
+        tot, cur = 0.0, None
+        for a, b in iv:
+            if cur is None or a > cur[1]:
+                if cur:
+                    tot += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        return tot + (cur[1] - cur[0] if cur else 0.0)
+    enc = [(r["enc_start_sec"], r["enc_end_sec"]) for r in rows]
+    dec = [(r["dec_start_sec"], r["dec_end_sec"]) for r in rows if r["dec_start_sec"] == r["dec_start_sec"]]
+    span = max(b for _, b in enc + dec) - min(a for a, _ in enc + dec)
+    busy_e, busy_d = union(enc), union(dec)
+    both = union(enc + dec)
+    return {"span_sec": span, "encode_busy_sec": busy_e, "decode_busy_sec": busy_d,
+            "overlap_sec": busy_e + busy_d - both, "serial_sum_sec": busy_e + busy_d}

@@ -143,6 +143,9 @@ def lib():
     _sig(L, "zc_group_alltoall_sym", C.c_int, P(vp), C.c_int, P(vp), P(vp), u64)
     _sig(L, "zc_group_broadcast_sym", C.c_int, P(vp), C.c_int, P(vp), u64, i32)
     _sig(L, "zc_group_execute", C.c_int, P(vp), C.c_int, P(P(abi.CollRequest)), i32)
+    _sig(L, "zc_comm_timeline_enable", C.c_int, vp, i32)
+    _sig(L, "zc_comm_timeline_rows", C.c_int, vp, P(abi.TimelineRow), i32, P(i32))
+    _sig(L, "zc_comm_timeline_origin_delta", C.c_int, vp, vp, P(dbl))
     _lib = L
     return L
 
@@ -559,6 +562,14 @@ def collective_config(pin: int = abi.PIN_AUTO, **kw) -> abi.CollectiveConfig:
     return c
 
 
+def _timeline_rows(h):
+    n = C.c_int32(0)
+    check(lib().zc_comm_timeline_rows(h, None, 0, C.byref(n)))
+    arr = (abi.TimelineRow * max(n.value, 1))()
+    check(lib().zc_comm_timeline_rows(h, arr, n.value, C.byref(n)))
+    return list(arr[:n.value])
+
+
 def _request(q: dict) -> abi.CollRequest:
     """A CollectiveRequest (collectives.hpp:94-101) from a dict: op, sym (int32 tensor), and per op
     recv (AllGather: nranks*block, AllToAll: like sym), root (Broadcast), scale/mode/levels
@@ -656,6 +667,41 @@ class Group:
                 if q["op"] == abi.COLL_ALLREDUCE:
                     q["scale"] = arrs[r][i].scale
         return requests
+
+    def timeline_enable(self, max_pieces: int = 4096) -> None:
+        """Start recording the measured piece timeline on every rank (0 stops)."""
+        for r in range(self.nranks):
+            check(lib().zc_comm_timeline_enable(self._h[r], max_pieces))
+
+    def timeline(self):
+        """Measured BatchTimelineRows (pipeline.hpp:32-46) of everything sent since
+        timeline_enable, one per 4 MiB batch: the sender's encode (its stores are the transfer over
+        peer memory) joined with the receiver's wait / decode of the same piece (matched by the
+        receiver's piece sequence number), all on rank 0's clock."""
+        per = []
+        for r in range(self.nranks):
+            rows = _timeline_rows(self._h[r])
+            d = C.c_double(0.0)
+            if r:
+                check(lib().zc_comm_timeline_origin_delta(self._h[0], self._h[r], C.byref(d)))
+            per.append((rows, d.value))
+        recv = {}
+        for r, (rows, off) in enumerate(per):
+            for x in rows:
+                if x.kind == 1:
+                    recv[(r, x.seq)] = (x.ready_sec + off, x.end_sec + off)
+        out = []
+        for r, (rows, off) in enumerate(per):
+            for x in rows:
+                if x.kind != 0:
+                    continue
+                dec = recv.get((x.peer, x.seq), (float("nan"), float("nan")))
+                out.append(dict(rank=r, seq=x.seq, batch=x.batch, codec=x.codec, raw_bytes=x.raw_bytes,
+                                total_bytes=x.total_bytes, enc_start_sec=x.start_sec + off,
+                                enc_end_sec=x.end_sec + off, xfer_start_sec=x.start_sec + off,
+                                xfer_end_sec=x.end_sec + off, dec_start_sec=dec[0], dec_end_sec=dec[1]))
+        out.sort(key=lambda d: (d["enc_start_sec"], d["rank"], d["batch"]))
+        return out
 
     def allreduce_max(self, vs: Sequence[float]):
         a = (C.c_double * self.nranks)(*vs)

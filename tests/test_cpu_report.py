@@ -58,3 +58,15 @@ def test_pretty_bytes_known():
     assert report.pretty_bytes(1 << 20) == "1 MiB"
     assert report.pretty_bytes(3 * (1 << 29)) == "1.5 GiB"
     assert report.pretty_bytes(1000) == "1000 B"
+
+
+def test_timeline_csv_format():
+    """write_timeline_csv (pipeline.cpp:160-170): the reference's header, codec names and
+    setprecision(9) times."""
+    from paper_2605_12396_b200 import report
+    assert report.TIMELINE_HEADER == ("batch,codec,raw_bytes,total_bytes,enc_start_sec,enc_end_sec,"
+                                      "xfer_start_sec,xfer_end_sec,dec_start_sec,dec_end_sec")
+    row = dict(codec=1, raw_bytes=4194304, total_bytes=1572896, enc_start_sec=1.0 / 3, enc_end_sec=2e-5,
+               xfer_start_sec=0.0, xfer_end_sec=1e-9, dec_start_sec=12.5, dec_end_sec=123456789.123)
+    lines = report.emit_timeline_csv([row]).splitlines()
+    assert lines[1] == "0,fixedlen,4194304,1572896,0.333333333,2e-05,0,1e-09,12.5,123456789"

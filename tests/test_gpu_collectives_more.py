@@ -162,3 +162,30 @@ def test_group_execute_matches_one_by_one(zc):
     with pytest.raises(ValueError):
         g.group_execute(bad)
     g.close()
+
+
+def test_measured_timeline(zc, monkeypatch):
+    """zc_comm_timeline_*: one send row per batch with its frame, joined with the receiver's decode
+    of the same piece; the times are causally ordered and the CSV has the reference's columns."""
+    from paper_2605_12396_b200 import report
+    monkeypatch.setenv("ZC_COMM_REGION_UNITS", "1")
+    n = 2
+    rng = np.random.default_rng(3)
+    syms = [_syms(rng, (12 << 20) // 4 + 9) for _ in range(n)]
+    g = zc.Group(n)
+    g.timeline_enable(256)
+    ts = [t(s) for s in syms]
+    g.allreduce(ts, [1.0] * n)
+    rows = g.timeline()
+    w = g.wire_stats()
+    # every frame the ring sent has a row (meta frames are host-counted control frames, not pieces)
+    assert len(rows) == sum(1 for _ in rows) == w.frames_by_codec[0] + w.frames_by_codec[1] + w.frames_by_codec[2] - 2
+    for r in rows:
+        assert r["enc_start_sec"] <= r["enc_end_sec"] <= r["dec_end_sec"] + 1e-6
+        assert r["dec_start_sec"] <= r["dec_end_sec"]
+        assert r["total_bytes"] > 32 and r["raw_bytes"] <= 4 << 20
+    csv = report.emit_timeline_csv(rows)
+    assert csv.splitlines()[0] == report.TIMELINE_HEADER and len(csv.splitlines()) == len(rows) + 1
+    s = report.overlap_summary(rows)
+    assert s["overlap_sec"] >= 0 and s["span_sec"] > 0
+    g.close()
