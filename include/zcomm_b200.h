@@ -197,6 +197,20 @@ int zc_frame_commit_raw(const uint8_t* d_raw, uint64_t raw_len, uint8_t* d_regio
                         uint64_t* d_total, void* stream);
 
 /* ---- L1 quantizer (quant.hpp:29-53) ---- */
+/* std::mt19937_64(seed) on the device, bit-exact: d_out[i] = the (skip+i)-th draw.  Chunks of the
+ * stream are generated in parallel from jump-ahead states (x^(2^j) mod the generator's
+ * characteristic polynomial, built once per process). */
+int zc_mt19937_64(uint64_t seed, uint64_t skip, uint64_t n, uint64_t* d_out, void* stream);
+/* qsgd_quantize_chunk (quant.cpp:64-82) with rng = mt19937_64(seed) after `skip` draws: one draw
+ * per element, in order.  Synchronous; non-finite input -> ZC_ERR_INVALID_ARGUMENT. */
+int zc_qsgd_quantize_chunk_f32(const float* d_x, uint64_t n, uint32_t levels, double norm, uint64_t seed,
+                               uint64_t skip, int32_t* d_sym, void* stream);
+/* The reference's norm: sqrt of the SEQUENTIAL double sum of squares (quant.cpp:87-91), one device
+ * thread (any parallel order rounds differently); non-finite input sets ZC_DERR_NONFINITE. */
+int zc_qsgd_norm_f32(const float* d_x, uint64_t n, double* d_norm, uint32_t* d_err, void* stream);
+/* qsgd_quantize (quant.cpp:84-98): symbols into d_sym, *h_scale = norm (1 when the norm is 0). */
+int zc_qsgd_quantize_f32(const float* d_x, uint64_t n, uint32_t levels, uint64_t seed, int32_t* d_sym,
+                         double* h_scale, void* stream);
 /* checked_absmax (quant.cpp:13-20): *d_absmax = max|x| (exact, as f64); non-finite -> ZC_DERR_NONFINITE. */
 int zc_absmax_f32(const float* d_x, uint64_t n, double* d_absmax, uint32_t* d_err, void* stream);
 int zc_absmax_f64(const double* d_x, uint64_t n, double* d_absmax, uint32_t* d_err, void* stream);
@@ -356,6 +370,11 @@ int zc_comm_reduce_scatter_sym(zc_comm* comm, int32_t* d_sym, uint64_t count, vo
 int zc_comm_allgather_sym(zc_comm* comm, int32_t* d_all, uint64_t block, void* stream);
 /* RankCtx::allreduce_max (collectives.cpp:398-421). */
 int zc_comm_allreduce_max(zc_comm* comm, double v, double* h_out, void* stream);
+/* RankCtx::allreduce_qsgd (collectives.cpp:518-523): qsgd_quantize on the device (sequential norm,
+ * bit-exact mt19937_64 draws), the compressed ring allreduce in QSGD mode (scale reconciliation as
+ * the reference's), dequantize (scale/levels)*sym into d_out (fp32, or fp64 when out_f64). */
+int zc_comm_allreduce_qsgd_f32(zc_comm* comm, const float* d_x, void* d_out, int32_t out_f64, uint64_t count,
+                               uint32_t levels, uint64_t seed, void* stream);
 /* RankCtx::alltoall (collectives.cpp:546-567): d_send / d_recv hold nranks*block symbols; block j of
  * d_send goes to rank j, block j of d_recv comes from rank j (zc_comm_alltoall_sym copies the own
  * block).  Frames use cfg.pin. */

@@ -68,6 +68,9 @@ class Port:
         _sig(L, "zo_frame_commit_raw", C.c_uint64, u8p, C.c_uint64, u8p, C.c_uint64)
         _sig(L, "zo_eb_quantize_f64", C.c_int, f64p, C.c_uint64, C.c_double, i32p)
         _sig(L, "zo_eb_quantize_f32", C.c_int, f32p, C.c_uint64, C.c_double, i32p)
+        _sig(L, "zo_qsgd_quantize_f32", C.c_int, f32p, C.c_uint64, C.c_uint32, C.c_uint64, i32p, P(C.c_double))
+        _sig(L, "zo_qsgd_quantize_chunk_f32", C.c_int, f32p, C.c_uint64, C.c_uint32, C.c_double, C.c_uint64,
+             C.c_uint64, i32p)
         _sig(L, "zo_absmax_f32", C.c_int, f32p, C.c_uint64, P(C.c_double))
         _sig(L, "zo_dequantize_f64", None, i32p, C.c_uint64, C.c_int, C.c_double, C.c_uint32, f64p)
         _sig(L, "zo_dequantize_f32", None, i32p, C.c_uint64, C.c_int, C.c_double, C.c_uint32, f32p)
@@ -113,6 +116,20 @@ class Port:
         out = np.zeros(len(x), np.int32)
         rc = self.lib.zo_eb_quantize_f32(x, len(x), scale, out)
         return rc, out
+
+    def qsgd_quantize_f32(self, x, levels, seed):
+        """qsgd_quantize (quant.cpp:84-98): (rc, symbols, scale)."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros(max(len(x), 1), np.int32)
+        sc = C.c_double(0.0)
+        rc = self.lib.zo_qsgd_quantize_f32(x, len(x), levels, seed, out, C.byref(sc))
+        return rc, out[:len(x)], sc.value
+
+    def qsgd_quantize_chunk_f32(self, x, levels, norm, seed, skip=0):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros(max(len(x), 1), np.int32)
+        rc = self.lib.zo_qsgd_quantize_chunk_f32(x, len(x), levels, norm, seed, skip, out)
+        return rc, out[:len(x)]
 
     def send_batch(self, raw, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None, cap=abi.STAGE_BANK_BYTES):
         raw = np.ascontiguousarray(raw).view(np.uint8).ravel()
@@ -238,6 +255,12 @@ class Ref:
         _sig(L, "zr_allgather_sym", C.c_int, C.c_int, P(abi.CollectiveConfig), i32p, C.c_uint64, vp, C.c_uint64,
              i32p, P(abi.WireStats))
         _sig(L, "zr_gen_data", C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, f64p)
+        _sig(L, "zr_qsgd_quantize", C.c_int, f64p, C.c_uint64, C.c_uint32, C.c_uint64, i32p, P(C.c_double))
+        _sig(L, "zr_qsgd_quantize_chunk", C.c_int, f64p, C.c_uint64, C.c_uint32, C.c_double, C.c_uint64, C.c_uint64,
+             i32p)
+        _sig(L, "zr_mt19937_64", C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, u64p)
+        _sig(L, "zr_allreduce_qsgd", C.c_int, C.c_int, P(abi.CollectiveConfig), f64p, C.c_uint64, C.c_uint32, u64p,
+             f64p)
         _sig(L, "zr_emit_csv", C.c_int, f64p, C.c_int, C.c_char_p, C.c_uint64)
         _sig(L, "zr_emit_markdown", C.c_int, f64p, C.c_int, C.c_char_p, C.c_uint64)
         _sig(L, "zr_codec_roundtrip_mt", C.c_int, f32p, C.c_uint64, C.c_double, C.c_int, vp, P(abi.ArbConfig),
@@ -249,6 +272,34 @@ class Ref:
         n = fn(flat, len(rows), buf, len(buf))
         assert n >= 0
         return buf.value.decode()
+
+    def qsgd_quantize(self, x, levels, seed):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(max(len(x), 1), np.int32)
+        sc = C.c_double(0.0)
+        rc = self.lib.zr_qsgd_quantize(x, len(x), levels, seed, out, C.byref(sc))
+        return rc, out[:len(x)], sc.value
+
+    def qsgd_quantize_chunk(self, x, levels, norm, seed, skip=0):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(max(len(x), 1), np.int32)
+        rc = self.lib.zr_qsgd_quantize_chunk(x, len(x), levels, norm, seed, skip, out)
+        return rc, out[:len(x)]
+
+    def mt19937_64(self, seed, skip, n):
+        out = np.zeros(max(n, 1), np.uint64)
+        self.lib.zr_mt19937_64(seed, skip, n, out)
+        return out[:n]
+
+    def allreduce_qsgd(self, xs, levels, seeds, pin=abi.PIN_AUTO):
+        """RankCtx::allreduce_qsgd (collectives.cpp:518-523) on n rank threads: f64 outputs."""
+        xs = np.ascontiguousarray(np.stack(xs), np.float64)
+        n, count = xs.shape
+        out = np.zeros(n * count, np.float64)
+        cfg = abi.default_collective_config(pin)
+        rc = self.lib.zr_allreduce_qsgd(n, C.byref(cfg), xs.ravel(), count, levels,
+                                        np.ascontiguousarray(seeds, np.uint64), out)
+        return rc, out.reshape(n, count)
 
     def emit_csv(self, rows):
         """bench.cpp:551-565 emit_csv over ReportRow records (report.ReportRow)."""

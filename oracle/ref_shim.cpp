@@ -8,6 +8,7 @@
 //   - as the CPU baseline (`--impl reference`).
 // Struct layouts are the zc_* PODs of include/zcomm_b200.h.
 #include <algorithm>
+#include <random>
 #include <atomic>
 #include <chrono>
 #include <iostream>
@@ -211,6 +212,46 @@ int zr_eb_quantize(const double* x, uint64_t n, double rel, int32_t* out, double
 int zr_eb_quantize_chunk(const double* x, uint64_t n, double scale, int32_t* out) {
   try {
     eb_quantize_chunk({x, n}, scale, {out, n});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_qsgd_quantize(const double* x, uint64_t n, uint32_t levels, uint64_t seed, int32_t* out, double* scale) {
+  try {
+    auto q = qsgd_quantize({x, n}, levels, seed);
+    if (n) std::memcpy(out, q.symbols.data(), n * 4);
+    *scale = q.meta.scale;
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_qsgd_quantize_chunk(const double* x, uint64_t n, uint32_t levels, double norm, uint64_t seed, uint64_t skip,
+                           int32_t* out) {
+  try {
+    std::mt19937_64 rng(seed);
+    rng.discard(skip);
+    qsgd_quantize_chunk({x, n}, levels, norm, rng, {out, n});
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+int zr_mt19937_64(uint64_t seed, uint64_t skip, uint64_t n, uint64_t* out) {
+  std::mt19937_64 rng(seed);
+  rng.discard(skip);
+  for (uint64_t i = 0; i < n; ++i) out[i] = rng();
+  return 0;
+}
+int zr_allreduce_qsgd(int nranks, const zc_collective_config* c, const double* xs, uint64_t count, uint32_t levels,
+                      const uint64_t* seeds, double* outs) {
+  try {
+    Communicator comm(nranks, to_ccfg(c));
+    comm.run([&](RankCtx& ctx) {
+      auto y = ctx.allreduce_qsgd({xs + static_cast<uint64_t>(ctx.rank()) * count, count}, levels, seeds[ctx.rank()]);
+      std::memcpy(outs + static_cast<uint64_t>(ctx.rank()) * count, y.data(), count * 8);
+    });
     return 0;
   } catch (...) {
     return map_exc();

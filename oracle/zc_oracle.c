@@ -124,6 +124,66 @@ int zo_absmax_f32(const float* x, uint64_t n, double* out) {
   return 0;
 }
 
+/* --------------------------------------------------------------- QSGD (quant.cpp:64-98) */
+/* std::mt19937_64 (libstdc++, the reference's generator; C++ [rand.eng.mers] parameters:
+ * w=64 n=312 m=156 r=31 a=0xB5026F5AA96619E9 u=29 d=0x5555555555555555 s=17 b=0x71D67FFFEDA60000
+ * t=37 c=0xFFF7EEE000000000 l=43 f=6364136223846793005). */
+void zo_mt64_seed(zo_mt64* g, uint64_t seed) {
+  g->x[0] = seed;
+  for (int i = 1; i < 312; ++i) g->x[i] = 6364136223846793005ull * (g->x[i - 1] ^ (g->x[i - 1] >> 62)) + (uint64_t)i;
+  g->i = 312;
+}
+uint64_t zo_mt64_next(zo_mt64* g) {
+  if (g->i >= 312) {
+    for (int k = 0; k < 312; ++k) {
+      uint64_t y = (g->x[k] & 0xFFFFFFFF80000000ull) | (g->x[(k + 1) % 312] & 0x7FFFFFFFull);
+      g->x[k] = g->x[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ull : 0ull);
+    }
+    g->i = 0;
+  }
+  uint64_t z = g->x[g->i++];
+  z ^= (z >> 29) & 0x5555555555555555ull;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+  z ^= (z << 37) & 0xFFF7EEE000000000ull;
+  z ^= z >> 43;
+  return z;
+}
+
+/* qsgd_quantize_chunk (quant.cpp:64-82) with rng = mt19937_64(seed) advanced by `skip` draws. */
+int zo_qsgd_quantize_chunk_f32(const float* x, uint64_t n, uint32_t levels, double norm, uint64_t seed, uint64_t skip,
+                               int32_t* out) {
+  if (levels == 0 || levels > (1u << 30)) return -1;
+  if (!(norm >= 0.0) || !isfinite(norm)) return -1;
+  zo_mt64 g;
+  zo_mt64_seed(&g, seed);
+  for (uint64_t k = 0; k < skip; ++k) zo_mt64_next(&g);
+  double scale = norm == 0.0 ? 1.0 : norm;
+  for (uint64_t i = 0; i < n; ++i) {
+    double v = (double)x[i];
+    if (!isfinite(v)) return ZC_DERR_NONFINITE;
+    double u = norm == 0.0 ? 0.0 : (double)levels * fabs(v) / scale;
+    double fl = floor(u);
+    double frac = u - fl;
+    double draw = (double)(zo_mt64_next(&g) >> 11) * 0x1.0p-53;
+    int64_t mag = (int64_t)fl + (draw < frac ? 1 : 0);
+    out[i] = (int32_t)(v < 0.0 ? -mag : mag);
+  }
+  return 0;
+}
+
+/* qsgd_quantize (quant.cpp:84-98): the norm is the sequential double sum of squares. */
+int zo_qsgd_quantize_f32(const float* x, uint64_t n, uint32_t levels, uint64_t seed, int32_t* out, double* scale) {
+  double sumsq = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    double v = (double)x[i];
+    if (!isfinite(v)) return ZC_DERR_NONFINITE;
+    sumsq += v * v;
+  }
+  double norm = sqrt(sumsq);
+  *scale = norm == 0.0 ? 1.0 : norm;
+  return zo_qsgd_quantize_chunk_f32(x, n, levels, norm, seed, 0, out);
+}
+
 /* quant.cpp:107-127 */
 void zo_dequantize_f64(const int32_t* s, uint64_t n, int mode, double scale, uint32_t levels, double* out) {
   if (mode == ZC_QUANT_ERROR_BOUNDED) {

@@ -41,6 +41,15 @@ uint64_t zo_frame_commit_raw(const uint8_t* raw, uint64_t n, uint8_t* region, ui
 int zo_eb_quantize_f64(const double* x, uint64_t n, double scale, int32_t* out);
 int zo_eb_quantize_f32(const float* x, uint64_t n, double scale, int32_t* out);
 int zo_absmax_f32(const float* x, uint64_t n, double* out);
+typedef struct zo_mt64 {
+  uint64_t x[312];
+  int i;
+} zo_mt64;
+void zo_mt64_seed(zo_mt64* g, uint64_t seed);
+uint64_t zo_mt64_next(zo_mt64* g);
+int zo_qsgd_quantize_chunk_f32(const float* x, uint64_t n, uint32_t levels, double norm, uint64_t seed, uint64_t skip,
+                               int32_t* out);
+int zo_qsgd_quantize_f32(const float* x, uint64_t n, uint32_t levels, uint64_t seed, int32_t* out, double* scale);
 void zo_dequantize_f64(const int32_t* s, uint64_t n, int mode, double scale, uint32_t levels, double* out);
 void zo_dequantize_f32(const int32_t* s, uint64_t n, int mode, double scale, uint32_t levels, float* out);
 

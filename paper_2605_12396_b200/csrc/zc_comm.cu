@@ -1113,6 +1113,24 @@ int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
   return rc;
 }
 
+int zc_comm_allreduce_qsgd_f32(zc_comm* c, const float* d_x, void* d_out, int32_t out_f64, uint64_t count,
+                               uint32_t levels, uint64_t seed, void* stream) {
+  if (int rc = dev_guard(c)) return rc;
+  if (int rc = order_after(c, stream)) return rc;
+  if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = ensure_sym(c, count)) return rc;
+  double scale = 1.0;
+  if (int rc = zc_qsgd_quantize_f32(d_x, count, levels, seed, c->sym, &scale, c->stream)) return rc;
+  if (int rc = enqueue_allreduce_sym(c, c->sym, count, ZC_QUANT_QSGD, scale, levels)) return rc;
+  if (int rc = finish(c)) return rc;
+  if (c->nranks > 1 && count > 0)
+    if (int rc = cuda_err(cudaMemcpy(&scale, &c->scal()->scale, 8, cudaMemcpyDeviceToHost), "scale")) return rc;
+  int rc = out_f64 ? zc_dequantize_f64(c->sym, count, ZC_QUANT_QSGD, scale, levels, static_cast<double*>(d_out), c->stream)
+                   : zc_dequantize_f32(c->sym, count, ZC_QUANT_QSGD, scale, levels, static_cast<float*>(d_out), c->stream);
+  if (rc) return rc;
+  return finish(c);
+}
+
 int zc_comm_alltoall_sym(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_t block, void* stream) {
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;

@@ -86,6 +86,11 @@ def lib():
     _sig(L, "zc_eb_quantize_rel_f32", C.c_int, vp, u64, dbl, vp, P(dbl), vp)
     _sig(L, "zc_dequantize_f64", C.c_int, vp, u64, i32, dbl, u32, vp, vp)
     _sig(L, "zc_dequantize_f32", C.c_int, vp, u64, i32, dbl, u32, vp, vp)
+    _sig(L, "zc_mt19937_64", C.c_int, u64, u64, u64, vp, vp)
+    _sig(L, "zc_qsgd_quantize_chunk_f32", C.c_int, vp, u64, u32, dbl, u64, u64, vp, vp)
+    _sig(L, "zc_qsgd_norm_f32", C.c_int, vp, u64, vp, vp, vp)
+    _sig(L, "zc_qsgd_quantize_f32", C.c_int, vp, u64, u32, u64, vp, P(dbl), vp)
+    _sig(L, "zc_comm_allreduce_qsgd_f32", C.c_int, vp, vp, vp, i32, u64, u32, u64, vp)
     _sig(L, "zc_fixedlen_encode", C.c_int, vp, u64, vp, u64, vp, vp, vp)
     _sig(L, "zc_fixedlen_decode", C.c_int, P(abi.FrameHeader), vp, u64, vp, u64, vp, vp)
     _sig(L, "zc_huff_ctx_create", C.c_int, vp, P(vp))
@@ -261,6 +266,32 @@ def eb_quantize(x: torch.Tensor, rel: float):
     scale = C.c_double()
     check(lib().zc_eb_quantize_rel_f32(_ptr(x), x.numel(), float(rel), _ptr(sym), C.byref(scale), _stream()))
     return sym, scale.value
+
+
+def mt19937_64(seed: int, n: int, skip: int = 0, device=None) -> torch.Tensor:
+    """std::mt19937_64(seed) draws skip .. skip+n-1, generated on the device (uint64 as int64)."""
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=device or "cuda")
+    check(lib().zc_mt19937_64(seed, skip, n, _ptr(out), _stream()))
+    return out[:n]
+
+
+def qsgd_quantize(x: torch.Tensor, levels: int, seed: int):
+    """qsgd_quantize (quant.cpp:84-98): returns (symbols, scale = norm or 1)."""
+    _dev(x)
+    x = x.contiguous().float()
+    sym = torch.empty(max(x.numel(), 1), dtype=torch.int32, device=x.device)
+    sc = C.c_double()
+    check(lib().zc_qsgd_quantize_f32(_ptr(x), x.numel(), levels, seed, _ptr(sym), C.byref(sc), _stream()))
+    return sym[:x.numel()], sc.value
+
+
+def qsgd_quantize_chunk(x: torch.Tensor, levels: int, norm: float, seed: int, skip: int = 0) -> torch.Tensor:
+    """qsgd_quantize_chunk (quant.cpp:64-82) with rng = mt19937_64(seed) after `skip` draws."""
+    _dev(x)
+    x = x.contiguous().float()
+    sym = torch.empty(max(x.numel(), 1), dtype=torch.int32, device=x.device)
+    check(lib().zc_qsgd_quantize_chunk_f32(_ptr(x), x.numel(), levels, float(norm), seed, skip, _ptr(sym), _stream()))
+    return sym[:x.numel()]
 
 
 def absmax(x: torch.Tensor) -> float:
@@ -668,6 +699,14 @@ class Group:
                     q["scale"] = arrs[r][i].scale
         return requests
 
+    def allreduce_qsgd(self, xs: Sequence[torch.Tensor], levels: int, seeds: Sequence[int], out_dtype=torch.float64):
+        """RankCtx::allreduce_qsgd (collectives.cpp:518-523) on every rank: qsgd_quantize per rank on
+        the device, the group's compressed allreduce in QSGD mode, dequantize."""
+        qs = [qsgd_quantize(x, levels, sd) for x, sd in zip(xs, seeds)]
+        syms = [q[0] for q in qs]
+        scales = self.allreduce(syms, [q[1] for q in qs], abi.QUANT_QSGD, levels)
+        return [dequantize(s, abi.QUANT_QSGD, sc, levels, out_dtype) for s, sc in zip(syms, scales)]
+
     def timeline_enable(self, max_pieces: int = 4096) -> None:
         """Start recording the measured piece timeline on every rank (0 stops)."""
         for r in range(self.nranks):
@@ -775,6 +814,12 @@ class Communicator:
 
     def allgather(self, all_blocks: torch.Tensor, block: int):
         check(lib().zc_comm_allgather_sym(self._h, _ptr(all_blocks), block, _stream()))
+
+    def allreduce_qsgd(self, x: torch.Tensor, levels: int, seed: int, out: Optional[torch.Tensor] = None):
+        out = out if out is not None else torch.empty(x.numel(), dtype=torch.float64, device=x.device)
+        check(lib().zc_comm_allreduce_qsgd_f32(self._h, _ptr(x), _ptr(out), 1 if out.dtype == torch.float64 else 0,
+                                               x.numel(), levels, seed, _stream()))
+        return out
 
     def alltoall(self, send: torch.Tensor) -> torch.Tensor:
         if send.numel() % self.nranks:

@@ -235,3 +235,25 @@ def test_gen_data_matches_reference(port, ref):
             b = np.zeros(5000)
             assert ref.lib.zr_gen_data(dist, 0.7, seed, rank, off, 5000, b) == 0
             assert (a == b).all(), (dist, seed, rank, off)
+
+
+def test_qsgd_restatement_matches_reference():
+    """zo_qsgd_quantize_f32 / zo_mt19937_64 (zc_oracle.c) against the compiled reference's
+    qsgd_quantize / std::mt19937_64 (quant.cpp:64-98), including the C++ standard's known answer."""
+    import oracle
+    try:
+        ref = oracle.ref()
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"compiled reference unavailable: {e}")
+    port = oracle.port()
+    assert int(ref.mt19937_64(5489, 9999, 1)[0]) == 9981545732273789042
+    rng = np.random.default_rng(0)
+    for n, lv, seed in [(0, 4, 1), (1, 1, 2), (1000, 15, 3), (100003, 255, 1234567), (5000, 1 << 30, 9)]:
+        x = rng.standard_normal(n).astype(np.float32)
+        a = port.qsgd_quantize_f32(x, lv, seed)
+        b = ref.qsgd_quantize(x.astype(np.float64), lv, seed)
+        assert a[0] == b[0] == 0 and a[2] == b[2] and np.array_equal(a[1], b[1])
+    x = rng.standard_normal(7777).astype(np.float32)
+    a = port.qsgd_quantize_chunk_f32(x, 7, 3.5, 42, 1000)
+    b = ref.qsgd_quantize_chunk(x.astype(np.float64), 7, 3.5, 42, 1000)
+    assert np.array_equal(a[1], b[1])
