@@ -261,7 +261,9 @@ __device__ __forceinline__ uint32_t huff_long(const DevHuff* t, unsigned long lo
 // read as zero, as in the reference.  Codes past the stream end are caught by the final position
 // check: positions only grow, so any code crossing the end leaves *end > 8*slen.  Returns false
 // on an undecodable code or an overrun.  s must be 4-byte aligned.
-template <bool kCoherent, bool kChecked>
+// kShort: every code fits the root LUT (max_len <= ROOT_BITS), so there is no over-root branch; a
+// LUT entry of length 0 can then only be a pattern no code starts with, reported undecodable.
+template <bool kCoherent, bool kChecked, bool kShort>
 __device__ __forceinline__ bool huff_grain(const DevHuff* t, const uint8_t* s, uint64_t slen, uint64_t start, uint32_t n,
                                            const Sink& sink, uint64_t ob, uint64_t* end, uint32_t& err) {
   const uint32_t* ws = reinterpret_cast<const uint32_t*>(s);
@@ -293,7 +295,10 @@ __device__ __forceinline__ bool huff_grain(const DevHuff* t, const uint8_t* s, u
     uint32_t e;
     asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut + 2u * static_cast<uint32_t>(acc & ((1u << ZC_HUFF_ROOT_BITS) - 1))));
     uint32_t l = e >> 8, sym = e & 0xFFu;
-    if (l == 0) {
+    if (kShort) {
+      ok &= l != 0;
+      l = l ? l : 1u;  // keep the reader moving; the grain is reported undecodable
+    } else if (l == 0) {
       l = huff_long(t, acc, sym);
       if (l == 0) {
         ok = false;
@@ -467,10 +472,12 @@ __device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* pay
         bool good;
         // unchecked 16-byte reads only where even a corrupt grain cannot leave the payload: a
         // grain consumes <= 1024 codes x 32 bits, the reader runs <= 384 bits ahead
+        const bool shortc = s_t->max_len <= ZC_HUFF_ROOT_BITS;
         if ((reinterpret_cast<uintptr_t>(s) & 3) == 0 && start + 32768 + 1024 <= slen * 8)
-          good = huff_grain<kCoherent, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
+          good = shortc ? huff_grain<kCoherent, false, true>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err)
+                        : huff_grain<kCoherent, false, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
         else if ((reinterpret_cast<uintptr_t>(s) & 3) == 0)
-          good = huff_grain<kCoherent, true>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
+          good = huff_grain<kCoherent, true, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
         else good = huff_run<kCoherent>(s_t, s, slen, start, n, &endb, [&](uint64_t j, uint32_t sym) {
           const uint32_t k = static_cast<uint32_t>(j & 15);
           if (k < 8) lo |= static_cast<unsigned long long>(sym) << (8 * k);
