@@ -856,6 +856,10 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
   g.fast = ((SRC == SRC_F32 || SRC == SRC_BYTES) && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
+  // fp32 FixedLen targets: one read of the input (speculative width, redo on a miss)
+  g.spec = (g.fast && SRC == SRC_F32 && (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) &&
+            std::getenv("ZC_NO_SPEC") == nullptr) ? 1u : 0u;
+  const int fmode = g.spec ? 1 : 0;
   if (p.pin == ZC_PIN_AUTO && !g.fast) {
     note_launch();
     profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
@@ -865,13 +869,19 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms)));
   if (g.fast) {
     // the range kernel also profiles the window and plans (Auto): no separate profile launch
-    if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN)
-      if (cudaError_t e = launch_fixed_range(p, scratch, g.total, g.s_full, sms, s)) return e;
+    if (g.spec) {  // window profiles (plan, width guess) only: the emit reads the input once
+      note_launch();
+      profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
+    } else if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) {
+      if (cudaError_t e = launch_fixed_range_m(p, scratch, g.total, g.s_full, sms, fmode, s)) return e;
+    }
     if (huff_possible) {
       note_launch();
       scan_kernel<SRC><<<grid, NT, 0, s>>>(p, us, g);
     }
-    if (cudaError_t e = launch_fixed_emit(p, scratch, g.total, g.s_full, sms, s)) return e;
+    if (cudaError_t e = launch_fixed_emit_m(p, scratch, g.total, g.s_full, sms, fmode, s)) return e;
+    if (g.spec)  // units whose decision differed from the speculated width
+      if (cudaError_t e = launch_fixed_emit_m(p, scratch, g.total, g.s_full, sms, 2, s)) return e;
     if (huff_possible) {  // Huffman targets: frames without an index, and the RAW fallbacks
       note_launch();
       emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);

@@ -28,6 +28,7 @@ struct BUnit {  // per unit, zeroed before every launch
   uint32_t maxzz, bad, hdone;  // hdone: Huffman bit-count slices (scan_kernel, fast mode)
   uint32_t fmin_c, fmax_k;           // fp32 range as order-preserving keys (min complemented)
   unsigned long long dmin_c, dmax_k;  // fp64 range, same encoding
+  uint32_t guess, redo, tdone;         // speculative FixedLen emit (zc_fixed.cu): window width, redo flag, tiles done
   BPart part[BMAX];
   unsigned long long hbase[BMAX];
   unsigned long long head_idx[BMAX], tail_idx[BMAX];
@@ -37,7 +38,8 @@ struct BUnit {  // per unit, zeroed before every launch
 struct BGlobal {  // after the BUnit array in the scratch block (zeroed with it)
   uint32_t n_huff;  // units the selector planned as Huffman (Auto)
   uint32_t next_task;  // range kernel work counter (zc_fixed.cu)
-  uint32_t pad[62];
+  uint32_t n_redo;     // speculative FixedLen units sent to the redo emit (zc_fixed.cu)
+  uint32_t pad[61];
 };
 __device__ __forceinline__ BGlobal* bglobal(BUnit* us, uint32_t nunits) { return reinterpret_cast<BGlobal*>(us + nunits); }
 
@@ -45,6 +47,7 @@ struct BGeom {
   uint32_t s_full;  // slices per full unit
   uint64_t total;   // slices in the message
   uint32_t fast;    // zc_fixed.cu handles the FixedLen / RAW units (range + emit)
+  uint32_t spec;    // speculative FixedLen: range pass = window profiles only, emit packs with the window's width
   __device__ __forceinline__ void unit_of(uint64_t t, uint32_t nunits, uint32_t& u, uint32_t& s) const {
     const uint64_t head = static_cast<uint64_t>(nunits - 1) * s_full;
     if (t < head) {
@@ -193,4 +196,13 @@ __device__ __forceinline__ void write_frame_header(const EncParams& p, uint32_t 
 }
 
 }  // namespace
+
+// zc_fixed.cu: the speculative single-read FixedLen path (see its header comment).
+// mode: 0 two-read (range over every slice, then emit), 1 speculative (range = window profiles
+// only; emit packs FixedLen units with the window's width and decides), 2 the redo emit of the
+// units whose decision differed from the speculation.
+cudaError_t launch_fixed_range_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                                 int mode, cudaStream_t s);
+cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                                int mode, cudaStream_t s);
 }  // namespace zc

@@ -137,6 +137,7 @@ __device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uin
     uint32_t m = 0;
     for (int i = 0; i < RT / 32; ++i) m = max(m, sm.wmz[i]);
     st.max_zigzag = m;
+    U.wmz = m;
     st.ctx_code_len_bits = el_ok ? el : 0.0;
     st.ctx_code_len_valid = el_ok ? 1u : 0u;
     st.self_code_len_bits = 0.0;
@@ -177,8 +178,8 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
   __shared__ uint32_t s_task;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool automode = p.pin == ZC_PIN_AUTO;
-  const uint32_t nprof = automode ? p.nunits : 0u;
-  const uint64_t nchunks = (g.total + RCH - 1) / RCH;
+  const uint32_t nprof = (automode || g.spec) ? p.nunits : 0u;
+  const uint64_t nchunks = g.spec ? 0 : (g.total + RCH - 1) / RCH;
   BGlobal* gl = bglobal(us, p.nunits);
   uint32_t err = 0;
   float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
@@ -244,7 +245,14 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
         window_profile<SRC>(p, us[u], u, src, R, ctx_ok, s_prof, err);
       }
       __syncthreads();
-      if (tid == 0) finish(us[u], u, 1u);
+      if (tid == 0) {
+        if (g.spec) {  // the emit decides; here only the plan census and the width guess
+          BUnit& U = us[u];
+          if (automode && U.plan == ZC_CODEC_HUFFMAN) atomicAdd(&gl->n_huff, 1u);
+        } else {
+          finish(us[u], u, 1u);
+        }
+      }
       continue;
     }
     const uint64_t ch = task - nprof;
@@ -412,11 +420,30 @@ constexpr uint32_t kForeign = 0xFEu;  // unit owned by the general kernels
 struct UnitView {
   uint32_t codec, width;
   uint64_t P;
-  bool big;
+  bool big, spec;
 };
 
 // Per-unit view for the emit kernel: owned (RAW / FixedLen) or not, and whether the fast
 // quantizer applies (max |q| < 2^30 over the unit, from the range pass).
+__device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* us, uint32_t u, bool ctx_ok);
+
+// mode 1: a FixedLen-target unit is packed with the window's width (`spec`; its header waits for
+// the decision); mode 2: only the units the decision sent back (redo) are owned.
+template <int kMode>
+__device__ __forceinline__ UnitView unit_view_m(const EncParams& p, const BUnit* us, uint32_t u, bool ctx_ok) {
+  UnitView v = unit_view(p, us, u, ctx_ok);
+  v.spec = false;
+  if (kMode == 1 && p.stage_len > kHeaderBytes && target_codec(p, us[u], ctx_ok) == ZC_CODEC_FIXEDLEN) {
+    v.codec = ZC_CODEC_FIXEDLEN;
+    v.width = width_from_maxzz(us[u].wmz);
+    v.P = packed_bytes(unit_R(p, u) / 4, v.width);
+    v.big = v.width >= 31;
+    v.spec = true;
+  }
+  if (kMode == 2 && !us[u].redo) v.codec = kForeign;
+  return v;
+}
+
 __device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* us, uint32_t u, bool ctx_ok) {
   UnitView v;
   final_codec(p, us[u], u, ctx_ok, v.codec, v.width, v.P);
@@ -433,7 +460,34 @@ __device__ __forceinline__ UnitView unit_view(const EncParams& p, const BUnit* u
 
 __device__ __forceinline__ bool owned(uint32_t codec) { return codec == ZC_CODEC_RAW || codec == ZC_CODEC_FIXEDLEN; }
 
+// Speculative FixedLen (mode 1): the tile's value range goes into the unit (the range pass's
+// keys), and the unit's last tile decides it (decide_unit: encode_best's post-checks / the pinned
+// fallbacks).  When the decision is FixedLen at the speculated width, the frame is complete and
+// its header is written; otherwise the unit is marked for the redo emit.  One lane per warp.
 template <int SRC>
+__device__ __noinline__ void spec_flush(const EncParams& p, BUnit* us, uint32_t u, float mn, float mx, uint32_t ntiles,
+                                       uint32_t* err) {
+  BUnit& U = us[u];
+  const bool bad = !(fabsf(mn) <= 3.402823466e38f) || !(fabsf(mx) <= 3.402823466e38f);  // NaN / Inf
+  if (bad) atomicOr(&U.bad, 1u);
+  atomicMax(&U.fmin_c, ~fkey(mn));
+  atomicMax(&U.fmax_k, fkey(mx));
+  const uint32_t ntu = static_cast<uint32_t>((unit_R(p, u) / 4 + TILE_ELEMS - 1) / TILE_ELEMS);
+  uint32_t old;  // release: this warp's range is in before its tiles count; acquire: the decider sees all
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&U.tdone), "r"(ntiles) : "memory");
+  if (old + ntiles != ntu) return;
+  uint32_t e = 0;
+  decide_unit<SRC>(p, U, u, true, true, e);
+  *err |= e;
+  if (U.codec == ZC_CODEC_FIXEDLEN && U.width == width_from_maxzz(U.wmz)) {
+    write_frame_header(p, u, ZC_CODEC_FIXEDLEN, U.width, U.payload);
+  } else {
+    U.redo = 1;
+    atomicAdd(&bglobal(us, p.nunits)->n_redo, 1u);
+  }
+}
+
+template <int SRC, int kMode>
 __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ EncParams p, const BUnit* us, BGeom g,
                                                      const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
                                                      uint64_t nfull) {
@@ -444,10 +498,14 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES) + warp * STAGES;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   uint32_t err = 0;
+  // the redo emit has nothing to do unless a speculation missed
+  if (kMode == 2 && *reinterpret_cast<const volatile uint32_t*>(&bglobal(const_cast<BUnit*>(us), p.nunits)->n_redo) == 0)
+    return;
 
   // headers / results of every owned unit, and the capacity failures (send_batch throws)
   for (uint32_t u = blockIdx.x * ET + tid; u < p.nunits; u += gridDim.x * ET) {
-    const UnitView v = unit_view(p, us, u, ctx_ok);
+    const UnitView v = unit_view_m<kMode>(p, us, u, ctx_ok);
+    if (v.spec || v.codec == kForeign) continue;  // spec: the decision writes it; foreign: not ours
     if (owned(v.codec) || v.codec == CODEC_NONE) write_frame_header(p, u, v.codec, v.width, v.P);
     if (v.codec == CODEC_NONE) err |= ZC_DERR_CAPACITY;
   }
@@ -467,7 +525,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
       if (u != iss_u) {
         iss_u = u;
-        iss_owned = owned(unit_view(p, us, u, ctx_ok).codec);
+        iss_owned = owned(unit_view_m<kMode>(p, us, u, ctx_ok).codec);
       }
       if (iss_owned) return c;
       c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
@@ -496,6 +554,18 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     c_first = next_tile(gw * CHUNK);
     iss_u = 0xffffffffu;
   }
+  float sp_mn = __int_as_float(0x7f800000), sp_mx = -__int_as_float(0x7f800000);
+  uint32_t sp_u = 0xffffffffu, sp_n = 0;
+  auto spec_run_flush = [&]() {  // all lanes: the run's range and tile count into the unit
+    for (int o = 16; o > 0; o >>= 1) {
+      sp_mn = fmin_nan(sp_mn, __shfl_xor_sync(FULL, sp_mn, o));
+      sp_mx = fmax_nan(sp_mx, __shfl_xor_sync(FULL, sp_mx, o));
+    }
+    if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), sp_u, sp_mn, sp_mx, sp_n, &err);
+    sp_mn = __int_as_float(0x7f800000);
+    sp_mx = -__int_as_float(0x7f800000);
+    sp_n = 0;
+  };
   for (uint64_t c = c_first; c < nfull; c = next_tile(tile_adv(c, tw)), ++k) {
     const uint32_t st = k % STAGES;
     tma::mbar_wait(&bars[st], (k / STAGES) & 1u);
@@ -517,8 +587,20 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
     if (u != cur_u) {
       cur_u = u;
-      v = unit_view(p, us, u, ctx_ok);
+      v = unit_view_m<kMode>(p, us, u, ctx_ok);
       payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+    }
+    if (kMode == 1) {
+      if (sp_n && sp_u != u) spec_run_flush();
+      if (v.spec) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          sp_mn = fmin_nan(sp_mn, x[i]);
+          sp_mx = fmax_nan(sp_mx, x[i]);
+        }
+        sp_u = u;
+        ++sp_n;
+      }
     }
     uint32_t s[32];
     if (SRC == SRC_F32) {
@@ -530,11 +612,12 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     store_row(v.codec, v.width, s, payload, (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
   }
 
+  if (kMode == 1 && sp_n) spec_run_flush();
   // the message's last, partial tile (direct guarded loads / byte-exact tail stores)
   if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
     const uint64_t c = nfull;
     const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
-    v = unit_view(p, us, u, ctx_ok);
+    v = unit_view_m<kMode>(p, us, u, ctx_ok);
     if (owned(v.codec)) {
       const uint64_t R = unit_R(p, u);
       const uint64_t n = R / 4;  // symbols of the unit
@@ -547,6 +630,21 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
         s[i] = e0 + i < n ? (SRC == SRC_F32 ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err)
                                             : __float_as_uint(__ldg(src + e0 + i)))
                           : 0u;
+      if (kMode == 1 && v.spec) {  // the partial tile's range (its valid elements only)
+        const float* xs = src + e0;
+        float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+        for (int i = 0; i < 32; ++i)
+          if (e0 + i < n) {
+            const float xv = __ldg(xs + i);
+            mn = fmin_nan(mn, xv);
+            mx = fmax_nan(mx, xv);
+          }
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fmin_nan(mn, __shfl_xor_sync(FULL, mn, o));
+          mx = fmax_nan(mx, __shfl_xor_sync(FULL, mx, o));
+        }
+        if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), u, mn, mx, 1u, &err);
+      }
       if (v.codec == ZC_CODEC_RAW) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -829,26 +927,37 @@ bool fixed_path_ok(const EncParams& p) {
          p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook;
 }
 
-cudaError_t launch_fixed_range(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
-                               cudaStream_t s) {
+cudaError_t launch_fixed_range_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                                 int mode, cudaStream_t s) {
   BGeom g;
   g.s_full = s_full;
   g.total = total_slices;
+  g.fast = 1;
+  g.spec = mode == 1 ? 1u : 0u;
   note_launch();
-  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(total_slices + p.nunits, 2ull * sms));
+  const uint64_t tasks = mode == 1 ? p.nunits : total_slices + p.nunits;
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(tasks, 2ull * sms)));
   if (p.src_kind == SRC_F32)
     range_kernel<SRC_F32><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
   else
     range_kernel<SRC_BYTES><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
   return cudaGetLastError();
 }
-
-cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
-                              cudaStream_t s) {
+cudaError_t launch_fixed_range(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                               cudaStream_t s) {
+  return launch_fixed_range_m(p, scratch, total_slices, s_full, sms, 0, s);
+}
+static void set_emit_attrs() {
+  cudaFuncSetAttribute(emit_kernel<SRC_F32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncSetAttribute(emit_kernel<SRC_F32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncSetAttribute(emit_kernel<SRC_F32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  cudaFuncSetAttribute(emit_kernel<SRC_BYTES, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+}
+cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                                int mode, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
-    cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+    set_emit_attrs();
     attr = true;
   }
   const uint64_t count = p.total_bytes / 4;
@@ -863,14 +972,27 @@ cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_
   BGeom g;
   g.s_full = s_full;
   g.total = total_slices;
+  g.fast = 1;
+  g.spec = mode == 1 ? 1u : 0u;
   const uint64_t want = (ntiles + ET_WARPS * CHUNK - 1) / (ET_WARPS * CHUNK);
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
   note_launch();
-  if (p.src_kind == SRC_F32)
-    emit_kernel<SRC_F32><<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
-  else
-    emit_kernel<SRC_BYTES><<<grid, ET, EMIT_SMEM, s>>>(p, static_cast<const BUnit*>(scratch), g, map, ntiles, nfull);
+  const BUnit* us = static_cast<const BUnit*>(scratch);
+  if (p.src_kind == SRC_F32) {
+    if (mode == 1)
+      emit_kernel<SRC_F32, 1><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+    else if (mode == 2)
+      emit_kernel<SRC_F32, 2><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+    else
+      emit_kernel<SRC_F32, 0><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+  } else {
+    emit_kernel<SRC_BYTES, 0><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+  }
   return cudaGetLastError();
+}
+cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
+                              cudaStream_t s) {
+  return launch_fixed_emit_m(p, scratch, total_slices, s_full, sms, 0, s);
 }
 
 bool fixed_decode_ok(const DecParams& p) {
@@ -913,8 +1035,7 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
 
 
 void preload_fixed_kernels() {
-  cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
-  cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(EMIT_SMEM));
+  set_emit_attrs();
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, range_kernel<SRC_F32>);
   cudaFuncGetAttributes(&a, range_kernel<SRC_BYTES>);
