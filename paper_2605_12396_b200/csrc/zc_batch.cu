@@ -29,8 +29,8 @@ namespace zc {
 namespace {
 
 // ------------------------------------------------------------------ pass 1: window profile + plan
-constexpr uint32_t PC = 16;            // CTAs per unit window (64 KiB / 16 = 4 KiB each)
-constexpr uint32_t PT = 256;           // threads per profile CTA: one 16-byte vector each
+constexpr uint32_t PC = 8;             // CTAs per unit window (64 KiB / 8 = 8 KiB each)
+constexpr uint32_t PT = 256;           // threads per profile CTA: two 16-byte vectors each
 constexpr uint32_t PV = ZC_SAMPLE_WINDOW_BYTES / 16 / PC;
 
 template <int SRC>
@@ -58,13 +58,24 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
   for (int i = tid; i < 256 * (PT / 32); i += PT) (&s_whist[0][0])[i] = 0;
   __syncthreads();
   const uint64_t W = R < kSampleWindow ? R : kSampleWindow;
-  const uint64_t v = static_cast<uint64_t>(part) * PV + tid;
   uint32_t wmz = 0, err = 0;
+  RawVec rvs[PV / PT];
+#pragma unroll
+  for (uint32_t k = 0; k < PV / PT; ++k) {
+    const uint64_t v = static_cast<uint64_t>(part) * PV + k * PT + tid;
+    rvs[k].nb = 0;
+    if (v * 16 < W) fetch<SRC, false>(p, uoff, R, v, rvs[k]);
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < PV / PT; ++k) {
+  const uint64_t v = static_cast<uint64_t>(part) * PV + k * PT + tid;
   if (v * 16 < W) {
-    RawVec rv;
-    fetch<SRC, false>(p, uoff, R, v, rv);
+    const RawVec& rv = rvs[k];
     uint32_t w[4];
-    to_words<SRC>(p, rv, w, err);
+    if (rv.nb == 16)
+      words_full<SRC>(p, rv, w, err);
+    else
+      to_words<SRC>(p, rv, w, err);
     const uint32_t nb = static_cast<uint32_t>(W - v * 16 < 16 ? W - v * 16 : 16);
 #pragma unroll
     for (uint32_t q = 0; q < 4; ++q)
@@ -76,6 +87,7 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
       const uint32_t jj = (j + static_cast<uint32_t>(lane)) & 15u;
       if (jj < nb) atomicAdd(&s_whist[warp][byte_of(w, jj)], 1u);
     }
+  }
   }
   for (int o = 16; o > 0; o >>= 1) wmz = max(wmz, __shfl_xor_sync(FULL, wmz, o));
   if (lane == 0) s_wmz[warp] = wmz;
