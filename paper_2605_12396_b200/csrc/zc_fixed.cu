@@ -465,19 +465,16 @@ __device__ __forceinline__ bool owned(uint32_t codec) { return codec == ZC_CODEC
 // fallbacks).  When the decision is FixedLen at the speculated width, the frame is complete and
 // its header is written; otherwise the unit is marked for the redo emit.  One lane per warp.
 template <int SRC>
-__device__ __noinline__ void spec_flush(const EncParams& p, BUnit* us, uint32_t u, float mn, float mx, uint32_t ntiles,
+__device__ __noinline__ void spec_flush(const EncParams& p, BUnit* us, uint32_t u, uint32_t mz, uint32_t ntiles,
                                        uint32_t* err) {
   BUnit& U = us[u];
-  const bool bad = !(fabsf(mn) <= 3.402823466e38f) || !(fabsf(mx) <= 3.402823466e38f);  // NaN / Inf
-  if (bad) atomicOr(&U.bad, 1u);
-  atomicMax(&U.fmin_c, ~fkey(mn));
-  atomicMax(&U.fmax_k, fkey(mx));
+  atomicMax(&U.maxzz, mz);
   const uint32_t ntu = static_cast<uint32_t>((unit_R(p, u) / 4 + TILE_ELEMS - 1) / TILE_ELEMS);
   uint32_t old;  // release: this warp's range is in before its tiles count; acquire: the decider sees all
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&U.tdone), "r"(ntiles) : "memory");
   if (old + ntiles != ntu) return;
   uint32_t e = 0;
-  decide_unit<SRC>(p, U, u, true, true, e);
+  decide_unit<SRC>(p, U, u, true, false, e);  // from the symbols' max zig-zag (U.maxzz)
   *err |= e;
   if (U.codec == ZC_CODEC_FIXEDLEN && U.width == width_from_maxzz(U.wmz)) {
     write_frame_header(p, u, ZC_CODEC_FIXEDLEN, U.width, U.payload);
@@ -554,16 +551,11 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     c_first = next_tile(gw * CHUNK);
     iss_u = 0xffffffffu;
   }
-  float sp_mn = __int_as_float(0x7f800000), sp_mx = -__int_as_float(0x7f800000);
-  uint32_t sp_u = 0xffffffffu, sp_n = 0;
-  auto spec_run_flush = [&]() {  // all lanes: the run's range and tile count into the unit
-    for (int o = 16; o > 0; o >>= 1) {
-      sp_mn = fmin_nan(sp_mn, __shfl_xor_sync(FULL, sp_mn, o));
-      sp_mx = fmax_nan(sp_mx, __shfl_xor_sync(FULL, sp_mx, o));
-    }
-    if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), sp_u, sp_mn, sp_mx, sp_n, &err);
-    sp_mn = __int_as_float(0x7f800000);
-    sp_mx = -__int_as_float(0x7f800000);
+  uint32_t sp_mz = 0, sp_u = 0xffffffffu, sp_n = 0;
+  auto spec_run_flush = [&]() {  // all lanes: the run's max zig-zag and tile count into the unit
+    sp_mz = __reduce_max_sync(FULL, sp_mz);
+    if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), sp_u, sp_mz, sp_n, &err);
+    sp_mz = 0;
     sp_n = 0;
   };
   for (uint64_t c = c_first; c < nfull; c = next_tile(tile_adv(c, tw)), ++k) {
@@ -590,24 +582,19 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       v = unit_view_m<kMode>(p, us, u, ctx_ok);
       payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
     }
-    if (kMode == 1) {
-      if (sp_n && sp_u != u) spec_run_flush();
-      if (v.spec) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          sp_mn = fmin_nan(sp_mn, x[i]);
-          sp_mx = fmax_nan(sp_mx, x[i]);
-        }
-        sp_u = u;
-        ++sp_n;
-      }
-    }
+    if (kMode == 1 && sp_n && sp_u != u) spec_run_flush();
     uint32_t s[32];
     if (SRC == SRC_F32) {
       quantize_row(x, scale, rcp, v.big, s, err);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) s[i] = __float_as_uint(x[i]);
+    }
+    if (kMode == 1 && v.spec) {  // the exact symbols' max zig-zag (non-finite inputs raised by quantize_row)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) sp_mz = max(sp_mz, zigzag32(static_cast<int32_t>(s[i])));
+      sp_u = u;
+      ++sp_n;
     }
     store_row(v.codec, v.width, s, payload, (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
   }
@@ -630,20 +617,13 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
         s[i] = e0 + i < n ? (SRC == SRC_F32 ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err)
                                             : __float_as_uint(__ldg(src + e0 + i)))
                           : 0u;
-      if (kMode == 1 && v.spec) {  // the partial tile's range (its valid elements only)
-        const float* xs = src + e0;
-        float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+      if (kMode == 1 && v.spec) {  // the partial tile's max zig-zag (its valid elements only)
+        uint32_t mz = 0;
+#pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (e0 + i < n) {
-            const float xv = __ldg(xs + i);
-            mn = fmin_nan(mn, xv);
-            mx = fmax_nan(mx, xv);
-          }
-        for (int o = 16; o > 0; o >>= 1) {
-          mn = fmin_nan(mn, __shfl_xor_sync(FULL, mn, o));
-          mx = fmax_nan(mx, __shfl_xor_sync(FULL, mx, o));
-        }
-        if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), u, mn, mx, 1u, &err);
+          if (e0 + i < n) mz = max(mz, zigzag32(static_cast<int32_t>(s[i])));
+        mz = __reduce_max_sync(FULL, mz);
+        if (lane == 0) spec_flush<SRC>(p, const_cast<BUnit*>(us), u, mz, 1u, &err);
       }
       if (v.codec == ZC_CODEC_RAW) {
 #pragma unroll
