@@ -480,3 +480,31 @@ def test_embedded_codebook_batches_vs_oracle(zc, port, pin):
         codecs.append(r.codec)
     assert abi.CODEC_HUFFMAN in codecs
     assert np.array_equal(npy(zc.decode_batches(fr, None)).view(np.uint8), msg)
+
+
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN])
+def test_speculative_width_misses_vs_oracle(zc, port, pin, monkeypatch):
+    """The single-read encoder packs each unit at its 64 KiB window's width and redoes units whose
+    decision differs: an outlier past the window (wider FixedLen), one near the int32 limit (Auto:
+    the gain check fails -> RAW; pinned: width 32), a hit, and a tiny last unit (window profile
+    skipped).  Frames must equal the oracle's and the two-read path's."""
+    scale = 2e-4
+    U = (4 << 20) // 4
+    rng = np.random.default_rng(pin + 5)
+    x = (rng.normal(0, 1, 3 * U + 700) * 2e-3).astype(np.float32)    # |q| ~ tens
+    x[U // 2] = 3.0                                                  # unit 0: outlier past the window
+    x[U + U // 3] = np.float32(2e9 * scale)                          # unit 1: |q| near 2^31
+    rc, sym = port.eb_quantize_f32(x, scale)
+    assert rc == 0
+    hint = abi.make_hint()
+    fr = zc.encode_batches(t(x), pin, scale=scale, hint=hint)
+    exp = port.encode_batches(sym.view(np.uint8), pin, hint, None)
+    for b, (er, ef) in enumerate(exp):
+        r = fr.encode_results()[b]
+        assert (r.codec, r.payload_bytes, r.total_bytes) == (er.codec, er.payload_bytes, er.total_bytes), f"unit {b}"
+        assert np.array_equal(npy(fr.frame(b)), ef), f"frame {b}"
+    assert np.array_equal(npy(zc.decode_batches(fr, None)), sym)
+    monkeypatch.setenv("ZC_NO_SPEC", "1")
+    two = zc.encode_batches(t(x), pin, scale=scale, hint=hint)
+    for b in range(fr.nbatches):
+        assert np.array_equal(npy(fr.frame(b)), npy(two.frame(b)))
