@@ -733,29 +733,168 @@ __device__ __forceinline__ void grain_pack(const EncParams& p, const RawVec rv[2
   }
 }
 
-template <int SRC>
+// kFused (fast fp32 / byte path with an index): the whole Huffman side of the send path in ONE
+// launch — the grain counts and the unit decisions of scan_kernel, the RAW fallbacks of
+// emit_kernel and the frames above — as an ordered task queue: every count task is claimed before
+// any emit task, and an emit task waits (spinning) only for decisions whose count tasks are
+// already held by running CTAs, so no wait can deadlock.  Auto messages with no Huffman plan exit
+// at once: one launch instead of three.
+template <int SRC, bool kFused>
 __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUnit* us, BGeom g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ unsigned long long s_enc[256];
   __shared__ uint32_t s_start[BS / kIndexGrain + 1];
+  __shared__ uint8_t s_clens[256];
+  __shared__ unsigned long long s_r64[NW];
+  __shared__ uint32_t s_r32[NW];
+  __shared__ uint32_t s_task;
   extern __shared__ __align__(16) uint32_t s_tiles[];
   uint32_t* tile = s_tiles + warp * HT;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
-  if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<const volatile uint32_t*>(&bglobal(us, p.nunits)->n_huff) == 0) return;
+  BGlobal* gl = bglobal(us, p.nunits);
+  if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<const volatile uint32_t*>(&gl->n_huff) == 0) return;
   if (!ctx_ok) return;
-  for (int i = tid; i < 256; i += NT) s_enc[i] = p.ctx->enc[i];
+  for (int i = tid; i < 256; i += NT) {
+    s_enc[i] = p.ctx->enc[i];
+    s_clens[i] = p.ctx->len[i];
+  }
   __syncthreads();
   uint32_t err = 0;
-  for (uint64_t tt = blockIdx.x; tt < g.total; tt += gridDim.x) {
-    const uint64_t t = g.total - 1 - tt;  // reverse: pass 2 ended on the last units (L2-resident)
+  const uint64_t T = g.total;
+  for (uint64_t it = blockIdx.x;; it += gridDim.x) {
+    uint64_t tsk;
+    if (kFused) {
+      __syncthreads();
+      if (tid == 0) s_task = atomicAdd(&gl->huff_task, 1u);
+      __syncthreads();
+      tsk = s_task;
+      if (tsk >= 2 * T) break;
+    } else {
+      if (it >= T) break;
+      tsk = T + it;
+    }
+    if (tsk < T) {  // count task (fused): scan_kernel's per-grain Huffman bit counts of slice tsk
+      uint32_t u, s;
+      g.unit_of(tsk, p.nunits, u, s);
+      BUnit& U = us[u];
+      if (target_codec(p, U, ctx_ok) != ZC_CODEC_HUFFMAN) continue;
+      const uint64_t R = unit_R(p, u);
+      const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
+      const uint64_t v0 = static_cast<uint64_t>(s) * BV;
+      const uint64_t v1 = min(v0 + BV, (R + 15) / 16);
+      uint32_t* uindex = p.index + static_cast<uint64_t>(u) * p.index_stride;
+      uint32_t zero = 0;
+      unsigned long long hb = 0;
+      for (uint64_t gv = v0 + static_cast<uint64_t>(warp) * 64; gv < v1; gv += NT * 2) {
+        RawVec rv[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint64_t v = gv + 2 * lane + k;
+          rv[k].nb = 0;
+          if (v < v1) fetch<SRC, false>(p, uoff, R, v, rv[k]);
+        }
+        uint32_t gb = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (rv[k].nb == 0) continue;
+          uint32_t w[4];
+          if (rv[k].nb == 16)
+            words_full<SRC>(p, rv[k], w, err);
+          else
+            to_words<SRC>(p, rv[k], w, err);
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            if (j < rv[k].nb) {
+              const uint32_t l = s_clens[byte_of(w, j)];
+              gb += l;
+              zero |= (l == 0);
+            }
+          }
+        }
+        hb += gb;
+        gb = __reduce_add_sync(FULL, gb);
+        if (lane == 0) uindex[gv / 64] = gb;
+      }
+      for (int o = 16; o > 0; o >>= 1) hb += __shfl_xor_sync(FULL, hb, o);
+      zero = __reduce_or_sync(FULL, zero);
+      if (lane == 0) {
+        s_r64[warp] = hb;
+        s_r32[warp] = zero;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int i = 1; i < NW; ++i) {
+          hb += s_r64[i];
+          zero |= s_r32[i];
+        }
+        U.part[s].bits = hb;
+        U.part[s].zero = zero;
+        __threadfence();
+        if (atomicAdd(&U.hdone, 1u) + 1 == unit_slices(p, u)) {
+          __threadfence();
+          decide_unit<SRC>(p, U, u, false, fast_ok, err);
+          __threadfence();
+          *reinterpret_cast<volatile uint32_t*>(&U.hdec) = 1u;
+        }
+      }
+      continue;
+    }
+    const uint64_t t = 2 * T - 1 - tsk;  // reverse: the count pass ended on the last units (L2-resident)
     uint32_t u, s;
     g.unit_of(t, p.nunits, u, s);
     BUnit& U = us[u];
     uint32_t codec, width;
     uint64_t P;
-    final_codec(p, U, u, ctx_ok, codec, width, P);
-    if (codec != ZC_CODEC_HUFFMAN) continue;
+    if (kFused) {
+      if (target_codec(p, U, ctx_ok) != ZC_CODEC_HUFFMAN) continue;
+      if (tid == 0)
+        while (*reinterpret_cast<const volatile uint32_t*>(&U.hdec) == 0) __nanosleep(64);
+      __syncthreads();
+      __threadfence();
+      const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
+      const uint64_t Ru = unit_R(p, u);
+      width = 0;
+      if (p.stage_len <= kHeaderBytes) {
+        codec = CODEC_NONE;
+        P = 0;
+      } else {
+        codec = __ldcg(&U.codec);
+        P = __ldcg(&U.payload);
+        if (codec == ZC_CODEC_RAW && Ru > pcap) codec = CODEC_NONE;
+      }
+      if (codec != ZC_CODEC_HUFFMAN) {  // emit_kernel's RAW fallback of a Huffman target (or capacity failure)
+        if (codec == ZC_CODEC_RAW) {
+          const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
+          uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
+          const uint64_t v0 = static_cast<uint64_t>(s) * BV;
+          const uint64_t v1 = min(v0 + BV, (Ru + 15) / 16);
+          for (uint64_t v = v0 + tid; v < v1; v += NT) {
+            RawVec rv;
+            fetch<SRC, false>(p, uoff, Ru, v, rv);
+            uint32_t w[4];
+            if (rv.nb == 16)
+              words_full<SRC>(p, rv, w, err);
+            else
+              to_words<SRC>(p, rv, w, err);
+            uint8_t* d = payload + v * 16;
+            if (rv.nb == 16 && aligned16(d)) {
+              *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else {
+              for (uint32_t j = 0; j < 16; ++j)
+                if (j < rv.nb) d[j] = static_cast<uint8_t>(byte_of(w, j));
+            }
+          }
+        } else if (s == 0 && tid == 0) {
+          err |= ZC_DERR_CAPACITY;
+        }
+        if (s == 0 && tid == 0) write_frame_header(p, u, codec, 0, P);
+        continue;
+      }
+    } else {
+      final_codec(p, U, u, ctx_ok, codec, width, P);
+      if (codec != ZC_CODEC_HUFFMAN) continue;
+    }
     const uint64_t R = unit_R(p, u);
     const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
     const uint64_t nvec = (R + 15) / 16;
@@ -839,16 +978,17 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
 
 constexpr size_t kHuffEmitSmem = sizeof(uint32_t) * NW * HT;
 
-template <int SRC>
+template <int SRC, bool kFused>
 void launch_huff_emit(const EncParams& p, BUnit* us, const BGeom& g, int sms, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(huff_emit_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+    cudaFuncSetAttribute(huff_emit_kernel<SRC, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kHuffEmitSmem));
     attr = true;
   }
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(2 * sms)));
   note_launch();
-  huff_emit_kernel<SRC><<<grid, NT, kHuffEmitSmem, s>>>(p, us, g);
+  huff_emit_kernel<SRC, kFused><<<grid, NT, kHuffEmitSmem, s>>>(p, us, g);
 }
 
 template <int SRC>
@@ -887,18 +1027,19 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
     } else if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) {
       if (cudaError_t e = launch_fixed_range_m(p, scratch, g.total, g.s_full, sms, fmode, s)) return e;
     }
-    if (huff_possible) {
+    const bool fused = huff_possible && p.index != nullptr;  // one launch for the whole Huffman side
+    if (huff_possible && !fused) {
       note_launch();
       scan_kernel<SRC><<<grid, NT, 0, s>>>(p, us, g);
     }
     if (cudaError_t e = launch_fixed_emit_m(p, scratch, g.total, g.s_full, sms, fmode, s)) return e;
     if (g.spec)  // units whose decision differed from the speculated width
       if (cudaError_t e = launch_fixed_emit_m(p, scratch, g.total, g.s_full, sms, 2, s)) return e;
-    if (huff_possible) {  // Huffman targets: frames without an index, and the RAW fallbacks
+    if (huff_possible && !fused) {  // Huffman targets without an index, and their RAW fallbacks
       note_launch();
       emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
     }
-    if (huff_possible && p.index != nullptr) launch_huff_emit<SRC>(p, us, g, sms, s);
+    if (fused) launch_huff_emit<SRC, true>(p, us, g, sms, s);
     return cudaGetLastError();
   }
   if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN || (p.pin == ZC_PIN_HUFFMAN && ctx_ok_host)) {
@@ -907,7 +1048,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   }
   note_launch();
   emit_kernel<SRC><<<grid, NT, sizeof(Scratch), s>>>(p, us, g);
-  if (huff_possible && p.index != nullptr) launch_huff_emit<SRC>(p, us, g, sms, s);
+  if (huff_possible && p.index != nullptr) launch_huff_emit<SRC, false>(p, us, g, sms, s);
   return cudaGetLastError();
 }
 
@@ -919,9 +1060,11 @@ void preload_batch_kernels() {
   cudaFuncSetAttribute(emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
   cudaFuncSetAttribute(emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
   cudaFuncSetAttribute(emit_kernel<SRC_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
-  cudaFuncSetAttribute(huff_emit_kernel<SRC_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
-  cudaFuncSetAttribute(huff_emit_kernel<SRC_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
-  cudaFuncSetAttribute(huff_emit_kernel<SRC_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_BYTES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_F64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_BYTES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
+  cudaFuncSetAttribute(huff_emit_kernel<SRC_F32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kHuffEmitSmem));
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, profile_kernel<SRC_BYTES>);
   cudaFuncGetAttributes(&a, profile_kernel<SRC_F32>);

@@ -28,7 +28,7 @@ struct BUnit {  // per unit, zeroed before every launch
   uint32_t maxzz, bad, hdone;  // hdone: Huffman bit-count slices (scan_kernel, fast mode)
   uint32_t fmin_c, fmax_k;           // fp32 range as order-preserving keys (min complemented)
   unsigned long long dmin_c, dmax_k;  // fp64 range, same encoding
-  uint32_t guess, redo, tdone;         // speculative FixedLen emit (zc_fixed.cu): window width, redo flag, tiles done
+  uint32_t guess, redo, tdone, hdec;  // hdec: Huffman-target decision published (fused Huffman kernel)         // speculative FixedLen emit (zc_fixed.cu): window width, redo flag, tiles done
   BPart part[BMAX];
   unsigned long long hbase[BMAX];
   unsigned long long head_idx[BMAX], tail_idx[BMAX];
@@ -39,7 +39,8 @@ struct BGlobal {  // after the BUnit array in the scratch block (zeroed with it)
   uint32_t n_huff;  // units the selector planned as Huffman (Auto)
   uint32_t next_task;  // range kernel work counter (zc_fixed.cu)
   uint32_t n_redo;     // speculative FixedLen units sent to the redo emit (zc_fixed.cu)
-  uint32_t pad[61];
+  uint32_t huff_task;  // fused Huffman kernel work counter (zc_batch.cu)
+  uint32_t pad[60];
 };
 __device__ __forceinline__ BGlobal* bglobal(BUnit* us, uint32_t nunits) { return reinterpret_cast<BGlobal*>(us + nunits); }
 
