@@ -33,63 +33,14 @@ __device__ __forceinline__ uint64_t unit_region(const DecParams& p, uint32_t u) 
   return p.frame_len ? p.frame_len[u].total_bytes : p.region;
 }
 
-__global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
-  const uint32_t u = blockIdx.y;
-  const uint64_t R = unit_raw(p, u);
-  const uint64_t nvec = (R + 15) / 16;
-  const uint64_t v0 = static_cast<uint64_t>(blockIdx.x) * SLICE_VEC;
-  if (v0 >= nvec && blockIdx.x != 0) return;
-  const uint64_t v1 = min(nvec, v0 + SLICE_VEC);
-  const uint8_t* stage = p.stages + static_cast<uint64_t>(u) * p.stride;
-  const uint8_t* payload = p.bare ? stage : stage + kHeaderBytes;
-  const uint64_t obase = p.bare ? 0 : static_cast<uint64_t>(u) * p.unit_bytes;
-  const int tid = threadIdx.x, lane = tid & 31;
-
-  __shared__ FrameCheck fc;
-  // a frame is one codec: the Huffman tables and the FixedLen staging words share the space, which
-  // leaves the L1 room for every thread's current 128-byte line of its Huffman grain
-  constexpr size_t kWordsBytes = sizeof(uint32_t) * (DT / 32) * 136 * 4;
-  __shared__ __align__(16) uint8_t s_pool[sizeof(DevHuff) > kWordsBytes ? sizeof(DevHuff) : kWordsBytes];
-  DevHuff& s_t = *reinterpret_cast<DevHuff*>(s_pool);
-  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pool);
-  __shared__ uint8_t s_lens[256];
-  __shared__ uint32_t s_flag;
-  uint32_t err = 0;
-
-  if (tid == 0)
-    check_frame<false>(stage, unit_region(p, u), R, p.bare ? &p.hdr : nullptr, p.bare != 0, p.ctx, p.index != nullptr, fc);
-  __syncthreads();
-  if (blockIdx.x == 0 && tid == 0) {
-    if (p.codec_out && !p.bare && !(p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)))
-      p.codec_out[u] = fc.codec;
-    if (p.bare && p.ok_out) *p.ok_out = fc.codec == kFallback ? 0 : 1;
-    if (fc.need_seq) atomicOr(&p.flags[u], 1u);
-  }
-  if (fc.codec == kFallback && p.bare) return;
-  if (p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)) return;  // zc_fixed.cu decoded it
-  Sink sink{p.out_kind, p.out, p.scale};
-  const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
-  uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
-  f = __reduce_or_sync(FULL, f);
-  if (lane == 0 && f) atomicOr(&p.flags[u], f);
-  err = __reduce_or_sync(FULL, err);
-  if (lane == 0 && err && p.err) atomicOr(p.err, err);
-}
-
-// Second pass, one CTA per unit: sequential Huffman decode for units whose index is missing or
+// The unit's last decode CTA (one per unit, when a flag is set): sequential Huffman decode for units whose index is missing or
 // disagrees with the payload (flag bit 0), and the raw-copy fallback for undecodable units.
-__global__ void __launch_bounds__(DT) fixup_kernel(const DecParams p) {
-  const uint32_t u = blockIdx.x;
-  const uint32_t f = p.flags[u];
-  if (f == 0) return;
+__device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameCheck& fc, DevHuff& s_t, uint8_t* s_lens,
+                           uint32_t& s_flag, uint32_t& s_fail) {
   const uint64_t R = unit_raw(p, u);
   const uint8_t* stage = p.stages + static_cast<uint64_t>(u) * p.stride;
   const uint8_t* payload = p.bare ? stage : stage + kHeaderBytes;
   const uint64_t obase = p.bare ? 0 : static_cast<uint64_t>(u) * p.unit_bytes;
-  __shared__ FrameCheck fc;
-  __shared__ DevHuff s_t;
-  __shared__ uint8_t s_lens[256];
-  __shared__ uint32_t s_flag, s_fail;
   uint32_t err = 0;
   // Bit 0 makes the sequential decode authoritative; bit 1 alone (a grain hit an undecodable
   // code on a consistent index) is a failure the sequential decoder reaches identically.  A
@@ -152,13 +103,75 @@ __global__ void __launch_bounds__(DT) fixup_kernel(const DecParams p) {
   if (err && p.err) atomicOr(p.err, err);
 }
 
+__global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
+  const uint32_t u = blockIdx.y;
+  const uint64_t R = unit_raw(p, u);
+  const uint64_t nvec = (R + 15) / 16;
+  const uint64_t v0 = static_cast<uint64_t>(blockIdx.x) * SLICE_VEC;
+  if (v0 >= nvec && blockIdx.x != 0) return;
+  const uint64_t v1 = min(nvec, v0 + SLICE_VEC);
+  const uint8_t* stage = p.stages + static_cast<uint64_t>(u) * p.stride;
+  const uint8_t* payload = p.bare ? stage : stage + kHeaderBytes;
+  const uint64_t obase = p.bare ? 0 : static_cast<uint64_t>(u) * p.unit_bytes;
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  __shared__ FrameCheck fc;
+  // a frame is one codec: the Huffman tables and the FixedLen staging words share the space, which
+  // leaves the L1 room for every thread's current 128-byte line of its Huffman grain
+  constexpr size_t kWordsBytes = sizeof(uint32_t) * (DT / 32) * 136 * 4;
+  __shared__ __align__(16) uint8_t s_pool[sizeof(DevHuff) > kWordsBytes ? sizeof(DevHuff) : kWordsBytes];
+  DevHuff& s_t = *reinterpret_cast<DevHuff*>(s_pool);
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pool);
+  __shared__ uint8_t s_lens[256];
+  __shared__ uint32_t s_flag;
+  uint32_t err = 0;
+
+  if (tid == 0)
+    check_frame<false>(stage, unit_region(p, u), R, p.bare ? &p.hdr : nullptr, p.bare != 0, p.ctx, p.index != nullptr, fc);
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    if (p.codec_out && !p.bare && !(p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)))
+      p.codec_out[u] = fc.codec;
+    if (p.bare && p.ok_out) *p.ok_out = fc.codec == kFallback ? 0 : 1;
+    if (fc.need_seq) atomicOr(&p.flags[u], 1u);
+  }
+  if (fc.codec == kFallback && p.bare) return;
+  if (p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)) return;  // zc_fixed.cu decoded it
+  Sink sink{p.out_kind, p.out, p.scale};
+  const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
+  uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
+  f = __reduce_or_sync(FULL, f);
+  if (lane == 0 && f) atomicOr(&p.flags[u], f);
+  err = __reduce_or_sync(FULL, err);
+  if (lane == 0 && err && p.err) atomicOr(p.err, err);
+  // the unit's CTAs count themselves in the flag word's upper bits; the last one runs the fixup
+  // (sequential decode / raw-copy fallback) when a flag is set, after every other CTA's output
+  __shared__ uint32_t s_last, s_fail;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const uint64_t nct = (nvec + SLICE_VEC - 1) / SLICE_VEC;
+    const uint32_t old = atomicAdd(&p.flags[u], 0x100u);
+    s_last = ((old >> 8) + 1 == (nct > 0 ? nct : 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint32_t fl = __ldcg(&p.flags[u]) & 0xFFu;
+  if (fl == 0) {
+    if (tid == 0) p.flags[u] = 0;
+    return;
+  }
+  __syncthreads();
+  fixup_unit(p, u, fl, fc, s_t, s_lens, s_flag, s_fail);
+}
+
 }  // namespace
 
 void preload_decode_kernels() {
   cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, decode_kernel);
-  cudaFuncGetAttributes(&a, fixup_kernel);
   cudaGetLastError();
 }
 
@@ -182,11 +195,6 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   }
   note_launch();
   decode_kernel<<<grid, DT, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e; {
-  note_launch();
-  fixup_kernel<<<p.nunits, DT, 0, s>>>(p);
-}
   return cudaGetLastError();
 }
 
