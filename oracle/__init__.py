@@ -172,12 +172,12 @@ class Port:
                                         C.byref(cfg or abi.default_arb_config()), out.ravel(), C.byref(w))
         return rc, out, w
 
-    def encode_batches(self, raw, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None):
+    def encode_batches(self, raw, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None, stage_len=abi.STAGE_BANK_BYTES):
         """Frame every 4 MiB batch of a message exactly as send_encoded does (collectives.cpp:350-356)."""
         raw = np.ascontiguousarray(raw).view(np.uint8).ravel()
         out = []
         for off in range(0, len(raw), abi.BATCH_RAW_BYTES):
-            out.append(self.send_batch(raw[off:off + abi.BATCH_RAW_BYTES], pin, hint, ctx, cfg))
+            out.append(self.send_batch(raw[off:off + abi.BATCH_RAW_BYTES], pin, hint, ctx, cfg, cap=stage_len))
         return out
 
     def recv_batch(self, frame, dlen, ctx=None):

@@ -767,7 +767,9 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
   const uint64_t ngroups = (nb + gb - 1) / gb;
   // frames of this call's own encoder: without a usable Huffman path every valid frame is
   // FixedLen / RAW and the general decode kernels have nothing to do
-  const int own = (ctx == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN) ? 1 : 0;
+  // (embedded codebooks: Auto may pick Huffman without a shared context, rea.cpp:160)
+  const bool embed = cfg != nullptr && cfg->embed_codebook != 0;
+  const int own = (pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN || (ctx == nullptr && !embed)) ? 1 : 0;
   if (int rc = cuda_err(cudaEventRecord(pp->start, caller), "pipeline start")) return rc;
   for (cudaStream_t s : {pp->h2d, pp->work, pp->d2h})
     if (int rc = cuda_err(cudaStreamWaitEvent(s, pp->start, 0), "pipeline wait")) return rc;

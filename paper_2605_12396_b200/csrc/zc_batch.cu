@@ -980,11 +980,10 @@ constexpr size_t kHuffEmitSmem = sizeof(uint32_t) * NW * HT;
 
 template <int SRC, bool kFused>
 void launch_huff_emit(const EncParams& p, BUnit* us, const BGeom& g, int sms, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(huff_emit_kernel<SRC, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kHuffEmitSmem));
-    attr = true;
   }
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(2 * sms)));
   note_launch();
@@ -993,10 +992,9 @@ void launch_huff_emit(const EncParams& p, BUnit* us, const BGeom& g, int sms, cu
 
 template <int SRC>
 cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(emit_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Scratch)));
-    attr = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1008,9 +1006,12 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
   g.fast = ((SRC == SRC_F32 || SRC == SRC_BYTES) && fixed_path_ok(p) && std::getenv("ZC_NO_FIXED") == nullptr) ? 1u : 0u;
-  // fp32 FixedLen targets: one read of the input (speculative width, redo on a miss)
+  // fp32 FixedLen targets: one read of the input (speculative width, redo on a miss).  The
+  // speculative emit stores a unit's payload before its decision is known, so it needs stages
+  // that hold any FixedLen payload of a unit (<= the unit's raw bytes); smaller stages take the
+  // two-read path, whose decision (capacity check included) precedes every store.
   g.spec = (g.fast && SRC == SRC_F32 && (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) &&
-            std::getenv("ZC_NO_SPEC") == nullptr) ? 1u : 0u;
+            p.stage_len >= kHeaderBytes + p.unit_bytes && std::getenv("ZC_NO_SPEC") == nullptr) ? 1u : 0u;
   const int fmode = g.spec ? 1 : 0;
   if (p.pin == ZC_PIN_AUTO && !g.fast) {
     note_launch();

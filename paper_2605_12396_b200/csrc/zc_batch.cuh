@@ -28,7 +28,9 @@ struct BUnit {  // per unit, zeroed before every launch
   uint32_t maxzz, bad, hdone;  // hdone: Huffman bit-count slices (scan_kernel, fast mode)
   uint32_t fmin_c, fmax_k;           // fp32 range as order-preserving keys (min complemented)
   unsigned long long dmin_c, dmax_k;  // fp64 range, same encoding
-  uint32_t guess, redo, tdone, hdec;  // hdec: Huffman-target decision published (fused Huffman kernel)         // speculative FixedLen emit (zc_fixed.cu): window width, redo flag, tiles done
+  // speculative FixedLen emit (zc_fixed.cu): guess = window width, redo = decision missed the
+  // guess, tdone = tiles done; hdec = Huffman-target decision published (fused Huffman kernel)
+  uint32_t guess, redo, tdone, hdec;
   BPart part[BMAX];
   unsigned long long hbase[BMAX];
   unsigned long long head_idx[BMAX], tail_idx[BMAX];

@@ -558,8 +558,9 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
 
 int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
   // frames of our own batched encoder: without a Huffman context (or with a FixedLen / RAW pin)
-  // all are FixedLen / RAW and the general decode kernels are skipped
-  const bool own = c->shared == nullptr || pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN;
+  // all are FixedLen / RAW and the general decode kernels are skipped.  Embedded codebooks let
+  // Auto pick Huffman with no shared context (rea.cpp:160), so those frames take the general path.
+  const bool own = pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN || (c->shared == nullptr && !c->cfg.arb.embed_codebook);
   const Layout& y = c->lay;
   zc_comm::TlPiece* tl = tl_begin(c, 1, -1, c->prx, bytes);
   if (tl) cudaEventRecord(tl->e0, c->stream);

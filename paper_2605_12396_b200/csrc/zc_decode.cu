@@ -188,11 +188,8 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   const uint64_t nvec = (maxR + 15) / 16;
   const uint32_t slices = static_cast<uint32_t>((nvec + SLICE_VEC - 1) / SLICE_VEC);
   dim3 grid(slices > 0 ? slices : 1, p.nunits);
-  static bool carve = false;
-  if (!carve) {
-    cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
-    carve = true;
-  }
+  static std::atomic<uint64_t> carve{0};
+  if (first_on_device(carve)) cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
   note_launch();
   decode_kernel<<<grid, DT, 0, s>>>(p);
   return cudaGetLastError();

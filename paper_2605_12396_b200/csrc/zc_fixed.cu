@@ -328,10 +328,24 @@ __device__ __noinline__ uint32_t quantize_exact(float x, double scale, double rc
   return r;
 }
 
-__device__ __forceinline__ void quantize_row(const float (&x)[32], double scale, double rcp, bool big, uint32_t (&s)[32],
-                                             uint32_t& err) {
+// |a| max |b| max |c| in one FMNMX3 (three-input max, sm_100+).
+__device__ __forceinline__ float absmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(fabsf(b)), "f"(fabsf(c)));
+  return r;
+}
+
+// The fast path below is exact only while |q| < 2^30 (the low word of t holds the integer and
+// |x*rcp - x/scale| < 2^-22).  `xlim` = RZ(2^29 * scale): a row holding any |x| >= xlim takes the
+// exact division, which raises the reference's int32-range error (quant.cpp:22-27) where it is
+// due.  NaN compares false here, but its residual is NaN and trips the tie test.
+__device__ __forceinline__ float fast_xlim(double scale) { return __double2float_rz(__dmul_rn(scale, 536870912.0)); }
+
+__device__ __forceinline__ void quantize_row(const float (&x)[32], double scale, double rcp, float xlim, bool big,
+                                             uint32_t (&s)[32], uint32_t& err) {
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   uint32_t rm = 0;  // max over the row of the high word of |r|, r = q - round(q)
+  float am = 0.f;   // max |x| over the row
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     // t = RN(x*rcp + M): the nearest integer to x*rcp in its low word; r = RN(x*rcp - k) is the
@@ -341,10 +355,11 @@ __device__ __forceinline__ void quantize_row(const float (&x)[32], double scale,
     const double r = __fma_rn(xd, rcp, -__dsub_rn(t, kMagic));
     rm = max(rm, static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu);
     s[i] = static_cast<uint32_t>(__double2loint(t));
+    if (i & 1) am = absmax3(am, x[i - 1], x[i]);
   }
-  // a value within 2^-18 of a rounding tie (|r| >= 0.5 - 2^-18, high word >= 0x3FDFFFF0), or a
-  // unit that may leave the fast range: exact path for the row
-  if (big || rm >= 0x3FDFFFF0u) {
+  // a value within 2^-18 of a rounding tie (|r| >= 0.5 - 2^-18, high word >= 0x3FDFFFF0), a value
+  // outside the fast range, or a unit flagged as such: exact path for the row
+  if (big || rm >= 0x3FDFFFF0u || !(am < xlim)) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) s[i] = quantize_exact(x[i], scale, rcp, &err);
   }
@@ -545,6 +560,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   UnitView v;
   uint8_t* payload = nullptr;
   const double scale = p.scale, rcp = p.rcp;
+  const float xlim = fast_xlim(scale);
   uint64_t c_first = gw;
   {  // the processing sequence restarts from the first tile (its own unit cache)
     iss_u = 0xffffffffu;
@@ -585,7 +601,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     if (kMode == 1 && sp_n && sp_u != u) spec_run_flush();
     uint32_t s[32];
     if (SRC == SRC_F32) {
-      quantize_row(x, scale, rcp, v.big, s, err);
+      quantize_row(x, scale, rcp, xlim, v.big, s, err);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) s[i] = __float_as_uint(x[i]);
@@ -935,10 +951,9 @@ static void set_emit_attrs() {
 }
 cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
                                 int mode, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     set_emit_attrs();
-    attr = true;
   }
   const uint64_t count = p.total_bytes / 4;
   const uint64_t rows = count / 32;
@@ -983,12 +998,11 @@ bool fixed_decode_ok(const DecParams& p) {
 }
 
 cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(fl_decode_kernel<OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
     cudaFuncSetAttribute(fl_decode_kernel<OUT_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
     cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
-    attr = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

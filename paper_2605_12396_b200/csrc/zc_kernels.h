@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "zc_common.cuh"
 
 namespace zc {
@@ -109,6 +111,14 @@ struct DecParams {
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
 // can state how many of OUR kernels a region launched.
 void note_launch();
+// Function attributes (cudaFuncSetAttribute) are per device: true the first time the current
+// device is seen by the caller's `mask`.
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
 // The default batched send path: profile -> scan -> emit streaming kernels (zc_batch.cu).

@@ -508,3 +508,108 @@ def test_speculative_width_misses_vs_oracle(zc, port, pin, monkeypatch):
     two = zc.encode_batches(t(x), pin, scale=scale, hint=hint)
     for b in range(fr.nbatches):
         assert np.array_equal(npy(fr.frame(b)), npy(two.frame(b)))
+
+
+_RANGE_CASES = {
+    # |q| past 2^32: the low word alone looks like a small symbol (858993.5 / 2e-4 = 4294967500)
+    "wrap_small": [858993.5],
+    "wrap_pos": [np.float32((2.0 ** 32 + 4096) * 2e-4)],
+    "wrap_neg": [np.float32(-(2.0 ** 32 - 8192) * 2e-4)],
+    "huge": [np.float32(2.0 ** 40 * 2e-4)],
+    "just_over": [np.float32(2.0 ** 31 * 2e-4)],
+    # inside the int32 range but past the fast path's 2^30: exact, no error
+    "inside": [np.float32(2.0e9 * 2e-4), np.float32(-1.5e9 * 2e-4)],
+}
+
+
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_RAW])
+@pytest.mark.parametrize("case", sorted(_RANGE_CASES))
+def test_int32_range_past_window(zc, port, pin, case):
+    """eb_quantize_chunk throws when |x/scale| >= 2147483647.5 (quant.cpp:22-27,
+    test_quant.cpp:61-68) wherever the value sits: here past every unit's 64 KiB profile window,
+    so the single-read encoder's width guess never saw it.  The fused encoder must raise exactly
+    where the oracle does, and otherwise produce the oracle's frames."""
+    scale = 2e-4
+    U = (4 << 20) // 4
+    rng = np.random.default_rng(11)
+    x = rng.normal(0, 1, 2 * U + 1000).astype(np.float32)
+    vals = _RANGE_CASES[case]
+    for i, v in enumerate(vals):
+        x[U // 2 + 7919 * i] = v            # unit 0, past the window
+        x[U + U - 33 - i] = v               # unit 1, its last full tile
+    rc, sym = port.eb_quantize_f32(x, scale)
+    hint = abi.make_hint()
+    if rc != 0:
+        assert rc == 2  # bin index exceeds int32 range
+        with pytest.raises(ValueError, match="int32"):
+            zc.encode_batches(t(x), pin, scale=scale, hint=hint)
+        with pytest.raises(ValueError, match="int32"):
+            zc.eb_quantize_with_scale(t(x), scale)
+        return
+    fr = zc.encode_batches(t(x), pin, scale=scale, hint=hint)
+    exp = port.encode_batches(sym.view(np.uint8), pin, hint, None)
+    for b, (er, ef) in enumerate(exp):
+        assert np.array_equal(npy(fr.frame(b)), ef), f"frame {b}"
+    assert np.array_equal(npy(zc.decode_batches(fr, None)), sym)
+
+
+def test_int32_range_host_roundtrip(zc, port):
+    """The same rejection through the C-ABI host round trip (zc_codec_roundtrip_host_f32): the
+    device error word carries ZC_DERR_RANGE."""
+    L = zc.lib()
+    count = 3 * ((4 << 20) // 4) + 5
+    x = np.random.default_rng(3).normal(0, 1, count).astype(np.float32)
+    x[(4 << 20) // 4 + 300000] = 858993.5
+    assert port.eb_quantize_f32(x, 2e-4)[0] == 2
+    hx = torch.from_numpy(x).pin_memory()
+    hy = torch.empty(count, dtype=torch.float32).pin_memory()
+    work = torch.empty(count, dtype=torch.float32, device=DEV)
+    fr = zc.alloc_frames(count * 4, DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    hint, cfg = abi.make_hint(), zc.default_arb_config()
+    s = torch.cuda.current_stream()
+    for pin in (abi.PIN_AUTO, abi.PIN_FIXEDLEN):
+        err.zero_()
+        zc.check(L.zc_codec_roundtrip_host_f32(hx.data_ptr(), count, 2e-4, zc._ptr(work), zc._ptr(fr.stages),
+                                               zc.STAGE_STRIDE, abi.STAGE_BANK_BYTES, pin, C.byref(hint), None,
+                                               C.byref(cfg), zc._ptr(fr.results), zc._ptr(fr.index), zc._ptr(err),
+                                               hy.data_ptr(), 2, C.c_void_p(s.cuda_stream)))
+        torch.cuda.synchronize()
+        assert int(err.item()) & abi.DERR_RANGE
+
+
+@pytest.mark.parametrize("stage_len", [(2 << 20) + 32, (3 << 20) + 100, (4 << 20)])
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN])
+def test_small_stage_capacity_vs_oracle(zc, port, pin, stage_len):
+    """A caller stage smaller than a unit's raw bytes: the payload cap (stage_len - 32) decides
+    FixedLen vs RAW vs failure as in encode_best / send_batch; no store may pass the stage.
+    Stages sit at a stride with a guard pattern after each, which must survive."""
+    scale = 2e-4
+    U = (4 << 20) // 4
+    rng = np.random.default_rng(pin + stage_len % 97)
+    x = rng.normal(0, 1, 3 * U).astype(np.float32)
+    x[U:2 * U] *= 4.0                                         # unit 1: width 18 -> 2.25 MiB
+    x[2 * U:] *= 0.01                                         # unit 2: width 9
+    rc, sym = port.eb_quantize_f32(x, scale)
+    assert rc == 0
+    hint = abi.make_hint()
+    exp = port.encode_batches(sym.view(np.uint8), pin, hint, None, stage_len=stage_len)
+    stride = zc.STAGE_STRIDE
+    stages = torch.full((3 * stride,), 0xA5, dtype=torch.uint8, device=DEV)
+    results = torch.zeros(3 * 3, dtype=torch.int64, device=DEV)
+    index = torch.zeros(3 * abi.HUFF_INDEX_ENTRIES, dtype=torch.int32, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    L = zc.lib()
+    zc.check(L.zc_encode_batches_f32(zc._ptr(t(x)), x.size, scale, zc._ptr(stages), stride, stage_len, pin,
+                                     C.byref(hint), None, C.byref(zc.default_arb_config()), zc._ptr(results),
+                                     zc._ptr(index), zc._ptr(err), zc._stream()))
+    torch.cuda.synchronize()
+    st = npy(stages)
+    res = npy(results).reshape(3, 3)
+    failed = any(er.total_bytes == 0 for er, _ in exp)
+    assert bool(int(err.item()) & abi.DERR_CAPACITY) == failed
+    for b, (er, ef) in enumerate(exp):
+        assert (res[b, 0] & 0xffffffff, res[b, 1], res[b, 2]) == (er.codec, er.payload_bytes, er.total_bytes), f"unit {b}"
+        if er.total_bytes:
+            assert np.array_equal(st[b * stride: b * stride + er.total_bytes], ef), f"frame {b}"
+        assert np.all(st[b * stride + stage_len:(b + 1) * stride] == 0xA5), f"stage {b} overrun"

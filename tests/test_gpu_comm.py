@@ -166,3 +166,132 @@ def test_c2_laplacian_two_ranks_large(zc, port):
     assert np.max(np.abs(npy(outs[0]) - exact)) <= n * scale / 2 * (1 + 1e-9)
     w = g.wire_stats()
     assert w.frames_by_codec[abi.CODEC_FIXEDLEN] > 0
+
+
+def _ring_check(zc, port, g, syms, pin, ctx_np=None, cfg=None):
+    """g.allreduce on `syms` == the oracle ring (symbols and WireStats)."""
+    n = len(syms)
+    cfgp = cfg or abi.default_collective_config(pin)
+    rc, exp, _, wire = port.ring_allreduce(np.stack(syms), [1.0] * n, pin, cfgp.hint, ctx_np, cfgp.arb,
+                                           cfgp.fused_codec_min_msg_bytes)
+    assert rc == 0
+    ts = [t(s) for s in syms]
+    g.allreduce(ts, [1.0] * n)
+    for r in range(n):
+        assert np.array_equal(npy(ts[r]), exp[r]), f"rank {r}"
+    w = g.wire_stats()
+    assert list(w.frames_by_codec) == list(wire.frames_by_codec)
+    assert (w.raw_bytes, w.payload_bytes, w.total_bytes) == (wire.raw_bytes, wire.payload_bytes, wire.total_bytes)
+    return w
+
+
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_HUFFMAN])
+def test_allreduce_n8_multipiece_vs_oracle_ring(zc, port, pin, monkeypatch):
+    """8 ranks, chunks of two 4 MiB batches (one full, one ragged) moved one batch per piece
+    (ZC_COMM_REGION_UNITS=1), so every step runs several pieces and the 3 piece regions are
+    reused many times over the 7 RS + 7 AG steps.  Count not a multiple of 8."""
+    monkeypatch.setenv("ZC_COMM_REGION_UNITS", "1")
+    n = 8
+    count = n * ((5 << 20) // 4) + 13
+    rng = np.random.default_rng(80 + pin)
+    syms = [np.clip(rng.laplace(0, 40 * (r + 1), count), -2**19, 2**19).astype(np.int32) for r in range(n)]
+    sample = syms[0].view(np.uint8)[: 4 << 20]
+    g = zc.Group(n, cfg=zc.collective_config(pin))
+    g.set_shared_huffman(zc.HuffmanContext.from_bytes(sample))
+    _ring_check(zc, port, g, syms, pin, port.huff_from_bytes(sample))
+    g.close()
+
+
+def _smooth_field(nz, rank, n=512):
+    """C3's synthetic scientific field: sin(2 pi i/512) cos(4 pi j/512) +
+    0.5 sin(6 pi k/512) with a per-rank phase, on a 512 x 512 x nz slab, fp32."""
+    i = np.arange(n, dtype=np.float64)[:, None, None]
+    j = np.arange(n, dtype=np.float64)[None, :, None]
+    k = np.arange(nz, dtype=np.float64)[None, None, :]
+    ph = 0.37 * rank
+    f = np.sin(2 * np.pi * i / n + ph) * np.cos(4 * np.pi * j / n) + 0.5 * np.sin(6 * np.pi * k / n + ph)
+    return f.astype(np.float32).ravel()
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_allreduce_eb_c3_smooth_field(zc, port, n):
+    """BASELINE config 3 at a slab size: the 512^3 smooth field's generator on 512 x 512 x 24
+    (6 Mi elements per rank), relative bound 1e-3 through allreduce_eb (scale = 2 rel gmax,
+    collectives.cpp:505-513).  Output bit-identical to the serial oracle; error <= N eb."""
+    rel = 1e-3
+    xs = [_smooth_field(24, r) for r in range(n)]
+    scale, syms, exp = _serial_eb(port, xs, rel)
+    g = zc.Group(n)
+    outs = g.allreduce_eb([t(x) for x in xs], rel, torch.float64)
+    for o in outs:
+        assert np.array_equal(npy(o).view(np.uint64), exp.view(np.uint64))
+    exact = np.sum(np.stack([x.astype(np.float64) for x in xs]), axis=0)
+    assert np.max(np.abs(npy(outs[0]) - exact)) <= n * scale / 2 * (1 + 1e-9)
+    g.close()
+    # the same symbols through the ring: wire stats equal the oracle ring's (FixedLen frames)
+    g = zc.Group(n)
+    w = _ring_check(zc, port, g, syms, abi.PIN_AUTO)
+    assert w.frames_by_codec[abi.CODEC_FIXEDLEN] > 0
+    g.close()
+
+
+@pytest.mark.parametrize("n,count", [
+    (2, (1 << 20) // 4),            # 1 MiB: RS steps ship RAW below fusedCodecMinMsgBytes
+    (2, (4 << 20) // 4 + 3),        # just past one batch
+    (2, (64 << 20) // 4),
+    (8, (1 << 20) // 4 + 5),        # count % 8 != 0, tiny chunks
+    (8, (40 << 20) // 4 + 7),
+])
+def test_allreduce_c5_sizes_vs_oracle_ring(zc, port, n, count):
+    """C5's message-size sweep points against the oracle ring (auto selector, shared context)."""
+    rng = np.random.default_rng(count % 1000 + n)
+    syms = [np.clip(rng.laplace(0, 30, count), -2**18, 2**18).astype(np.int32) for _ in range(n)]
+    sample = syms[0].view(np.uint8)[: 4 << 20]
+    g = zc.Group(n)
+    g.set_shared_huffman(zc.HuffmanContext.from_bytes(sample))
+    _ring_check(zc, port, g, syms, abi.PIN_AUTO, port.huff_from_bytes(sample))
+    g.close()
+
+
+@pytest.mark.slow
+def test_allreduce_eb_1gib_two_ranks(zc, port):
+    """C5's top end: 1 GiB of fp32 per rank (256 Mi elements), abs eb 1e-4, 2 ranks; exact
+    against the symbol sum (int64, checked to fit int32) dequantized as the reference does."""
+    n, count = 2, 1 << 28
+    rng = np.random.default_rng(5)
+    xs = [rng.laplace(0, 1e-2, count).astype(np.float32) for _ in range(n)]
+    scale = 2e-4
+    gmax = max(float(np.abs(x).max()) for x in xs)
+    rel = scale / (2 * gmax)
+    acc = np.zeros(count, np.int64)
+    for x in xs:
+        rc, s = port.eb_quantize_f32(x, 2.0 * rel * gmax)
+        assert rc == 0
+        acc += s
+    g = zc.Group(n)
+    outs = g.allreduce_eb([t(x) for x in xs], rel, torch.float32)
+    sc = 2.0 * rel * gmax
+    exp = (sc * acc.astype(np.int32).astype(np.float64)).astype(np.float32)
+    for o in outs:
+        assert np.array_equal(npy(o), exp)
+    g.close()
+
+
+def test_embedded_codebook_ring_without_shared_ctx(zc, port):
+    """cfg.embedCodebook with no shared table: Auto picks Huffman with a per-frame codebook
+    (rea.cpp:160, 214-221).  Every rank must decode those frames (RS adds, AG stores)."""
+    n = 3
+    count = 3 * ((6 << 20) // 4) + 11
+    rng = np.random.default_rng(17)
+    syms = []
+    for r in range(n):
+        s = rng.integers(-2, 3, count).astype(np.int32)
+        hit = rng.random(count) < 1e-3
+        s[hit] = rng.integers(-(1 << 19), 1 << 19, int(hit.sum()))
+        syms.append(s)
+    cfg = zc.collective_config(abi.PIN_AUTO)
+    cfg.arb.embed_codebook = 1
+    g = zc.Group(n, cfg=cfg)
+    w = _ring_check(zc, port, g, syms, abi.PIN_AUTO, None, cfg)
+    assert w.frames_by_codec[abi.CODEC_HUFFMAN] > 0
+    g.close()
