@@ -26,6 +26,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -106,6 +108,65 @@ def load_traffic(kernel):
         return None
 
 
+# ------------------------------------------------------------------------------- synthetic inputs
+# Both arms (ours and --impl reference) build their inputs with these host generators, so the two
+# JSON lines describe the same data and the same config.
+DATA_C0 = "synthetic: numpy default_rng(1).standard_normal fp32 (BASELINE config 0 Gaussian)"
+DATA_C1 = "synthetic: Laplacian(0, 1e-2) fp32 per rank, numpy default_rng(100 + rank)"
+DATA_C2 = ("synthetic: 512^3 smooth field per rank, sin(2 pi i/512 + 0.37 r) cos(4 pi j/512) + "
+           "0.5 sin(6 pi k/512 + 0.37 r), fp32")
+
+
+def gen_c0(count):
+    import numpy as np
+    return np.random.default_rng(1).standard_normal(count, dtype=np.float32)
+
+
+def gen_rank(world, rank, count):
+    """Per-rank input of the N>1 workloads: config 1 (N=2) Laplacian gradients, config 2 (N>=4)
+    the smooth scientific field (first `count` elements of the 512^3 field)."""
+    import numpy as np
+    if world == 2:
+        return np.random.default_rng(100 + rank).laplace(0.0, 1e-2, count).astype(np.float32)
+    n = 512
+    slabs = min(n, -(-count // (n * n)))
+    out = np.empty(slabs * n * n, np.float32)
+    i = np.arange(n, dtype=np.float64)
+    ph = 0.37 * rank
+    a = np.sin(2 * np.pi * i / n + ph)[:, None] * np.cos(4 * np.pi * i / n)[None, :]   # (i, j)
+    b = 0.5 * np.sin(6 * np.pi * i / n + ph)                                             # (k)
+    for ii in range(slabs):
+        out[ii * n * n:(ii + 1) * n * n] = (a[ii][:, None] + b[None, :]).astype(np.float32).ravel()
+    return out[:count]
+
+
+def workload_config(world, count):
+    """The config dict both arms print (identical keys and values)."""
+    if world == 1:
+        return {"workload": "BASELINE config 0: single-rank codec round trip, 64 Mi Gaussian fp32, abs eb 1e-4",
+                "count": count, "raw_bytes": 4 * count, "scale": SCALE, "pin": "auto (encode_best)",
+                "hint_beta_bytes_per_sec": BETA, "batches": (4 * count + (4 << 20) - 1) // (4 << 20),
+                "batch_bytes": 4 << 20}
+    if world == 2:
+        wl, q = "BASELINE config 1: ring AllReduce, 256 MB Laplacian per rank, abs eb 1e-4", "abs eb 1e-4"
+    else:
+        wl, q = "BASELINE config 2: ring RS+AG (allreduce_eb), 512^3 smooth field per rank, rel eb 1e-3", "rel eb 1e-3"
+    return {"workload": wl, "count_per_rank": count, "quantizer": q, "pin": "auto (encode_best)",
+            "hint_beta_bytes_per_sec": BETA, "shared_huffman": "primed from rank 0's first 1 Mi symbols (bench.cpp:169-204)",
+            "parallelism": f"ring{world}"}
+
+
+def world_count(world, count_arg):
+    if count_arg:
+        return count_arg
+    return COUNT_C0 if world <= 2 else 512 * 512 * 512
+
+
+def eb_rel(world, xs_absmax):
+    """allreduce_eb's rel: config 1 fixes the absolute bound 1e-4 (scale 2e-4 = 2 rel gmax)."""
+    return ABS_EB / xs_absmax if world == 2 else 1e-3
+
+
 # ---------------------------------------------------------------------------------------- N = 1
 def codec_bench(args):
     import torch
@@ -116,9 +177,7 @@ def codec_bench(args):
     torch.cuda.set_device(dev)
     count = args.count
     raw_bytes = 4 * count
-    g = torch.Generator(device=dev)
-    g.manual_seed(1)
-    x = torch.randn(count, generator=g, device=dev, dtype=torch.float32)
+    x = torch.from_numpy(gen_c0(count)).to(dev)
     hint = abi.make_hint(BETA)
     cfg = zcomm.default_arb_config()
     # shared Huffman context primed like prime_shared_huffman (bench.cpp:169-204): rank 0's first
@@ -292,14 +351,10 @@ def codec_bench(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32->int32 (fp64 quantizer arithmetic)",
-        "data": "synthetic: torch.randn N(0,1) fp32, seed 1",
-        "config": {
-            "workload": "BASELINE config 0: single-rank codec round trip, 64 Mi Gaussian fp32, abs eb 1e-4",
-            "count": count, "raw_bytes": raw_bytes, "scale": SCALE, "pin": "auto (encode_best)",
-            "hint_beta_bytes_per_sec": BETA, "batches": F, "batch_bytes": abi.BATCH_RAW_BYTES,
-            "l2": "inputs (256 MiB fp32) exceed the 126 MB L2; no flush needed",
-            "launch": "cuda_graph (one captured step replayed)" if graph_ms is not None else "eager",
-        },
+        "data": DATA_C0,
+        "config": workload_config(1, count),
+        "l2": "inputs (256 MiB fp32) exceed the 126 MB L2; no flush needed",
+        "launch": "cuda_graph (one captured step replayed)" if graph_ms is not None else "eager",
         "eager_ms_per_step": round(auto["ms"], 4),
         "compression_ratio": round(raw_bytes / P_auto, 4),
         "frames_by_codec": {"raw": auto["frames"][0], "fixedlen": auto["frames"][1], "huffman": auto["frames"][2]},
@@ -409,13 +464,14 @@ def cpu_baseline(xs, prime_syms, pin, threads=None, reps=1):
 
 
 def reference_arm(args):
-    import numpy as np
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
+    if world > 1:
+        return reference_collective_arm(args, world)
     n = args.cpu_sample
-    rng = np.random.default_rng(1)
-    x = rng.standard_normal(n).astype(np.float32)
+    x = gen_c0(n)
     prime = np.clip(np.round(x[: 1 << 20].astype(np.float64) / SCALE), -2**31, 2**31 - 1).astype(np.int32)
     for _ in range(args.warmup):
         cpu_baseline(x[: min(n, 4 << 20)], prime, 0)
@@ -432,13 +488,73 @@ def reference_arm(args):
         "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t_all / args.steps, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32->int32 (fp64 quantizer arithmetic)",
-        "data": "synthetic: numpy standard_normal fp32, seed 1", "impl": "reference",
-        "config": {"workload": "BASELINE config 0: single-rank codec round trip, 64 Mi Gaussian fp32, abs eb 1e-4",
-                   "count": n, "raw_bytes": 4 * n, "scale": SCALE, "pin": "auto (encode_best)",
-                   "hint_beta_bytes_per_sec": BETA, "batches": (4 * n + (4 << 20) - 1) // (4 << 20),
-                   "batch_bytes": 4 << 20},
+        "data": DATA_C0, "impl": "reference",
+        "config": workload_config(1, n),
         "cpu_baseline": cb,
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+_XS_CACHE = {}
+
+
+def collective_cpu_baseline(world, count, sample_count, reps=1):
+    """The reference's own collective runtime: Communicator(world, cfg).run with one host thread per
+    rank, each calling RankCtx::allreduce_eb on its rank's input (bench.cpp:206-289 times
+    Communicator::run by wall clock).  Shared Huffman context primed like prime_shared_huffman.
+    Bounded sample: the first `sample_count` elements of every rank's input."""
+    import oracle
+    from paper_2605_12396_b200 import abi
+    ref = oracle.ref()
+    if ref is None:
+        raise RuntimeError("oracle/_ref is not built; the CPU baseline needs the compiled reference")
+    m = min(count, sample_count)
+    key = (world, m)
+    if key not in _XS_CACHE:
+        _XS_CACHE.clear()
+        _XS_CACHE[key] = np.stack([gen_rank(world, r, m) for r in range(world)]).astype(np.float64)
+    xs = _XS_CACHE[key]
+    gmax = float(np.abs(xs).max())
+    rel = eb_rel(world, gmax)
+    scale = 2.0 * rel * gmax
+    prime = np.clip(np.round(xs[0, : 1 << 20] / scale), -2**31, 2**31 - 1).astype(np.int32).view(np.uint8)
+    cfg = abi.default_collective_config(abi.PIN_AUTO)
+    cfg.hint = abi.make_hint(BETA)
+    out = np.zeros_like(xs)
+    w = abi.WireStats()
+    wall = C.c_double()
+    total = 0.0
+    for _ in range(reps):
+        rc = ref.lib.zr_allreduce_eb(world, C.byref(cfg), np.ascontiguousarray(xs).ravel(), m, rel, prime.ctypes.data, len(prime),
+                                     out.ravel(), C.byref(w), C.byref(wall))
+        if rc:
+            raise RuntimeError(ref.error())
+        total += wall.value
+    return {"value": round(reps * 4 * m / total / 1e9, 4), "unit": "GB/s", "cores": world, "kind": "reference",
+            "sample": f"{reps} x allreduce_eb of {m} fp32 elements per rank ({4 * m >> 20} MiB; the first {m} of the "
+                      f"{count}-element workload), {world} rank threads of the compiled reference's Communicator::run",
+            "compression_ratio": round(w.raw_bytes / max(w.payload_bytes, 1), 4), "seconds": round(total, 3)}
+
+
+def reference_collective_arm(args, world):
+    count = world_count(world, args.count)
+    for _ in range(max(0, min(args.warmup, 1))):
+        collective_cpu_baseline(world, count, min(args.ref_sample, 1 << 20))
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(collective_cpu_baseline(world, count, args.ref_sample))
+    t_all = time.perf_counter() - t_all
+    v = statistics.mean(r["value"] for r in vals)
+    cb = dict(vals[-1])
+    cb["value"] = round(v, 4)
+    return {
+        "metric": "compressed AllReduce algbw GB/s", "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_all / args.steps, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32->int32 symbols (int32 sum)",
+        "data": DATA_C1 if world == 2 else DATA_C2, "impl": "reference",
+        "config": workload_config(world, count), "cpu_baseline": cb,
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
@@ -470,28 +586,21 @@ def allreduce_bench(args):
     dist.init_process_group("nccl" if use_nccl else "gloo",
                             **({"device_id": torch.device("cuda", dev_index)} if use_nccl else {}))
     dev = torch.device("cuda", dev_index)
-    if world == 2:
-        count, workload, rel_mode = 64 << 20, "BASELINE config 1: ring AllReduce, 256 MB Laplacian per rank, abs eb 1e-4", "abs"
-        g = torch.Generator(device=dev)
-        g.manual_seed(100 + rank)
-        u = torch.rand(count, generator=g, device=dev, dtype=torch.float64) - 0.5
-        x = (-1e-2 * torch.sign(u) * torch.log1p(-2 * u.abs())).float()
-        del u
-    else:
-        count, workload, rel_mode = 512 * 512 * 512, "BASELINE config 2: ring RS+AG, 512^3 smooth field per rank, rel eb 1e-3", "rel"
-        i = torch.arange(512, device=dev, dtype=torch.float32)
-        f = (torch.sin(2 * torch.pi * i / 512)[:, None, None] * torch.cos(4 * torch.pi * i / 512)[None, :, None]
-             + 0.5 * torch.sin(6 * torch.pi * (i + 7 * rank) / 512)[None, None, :])
-        x = f.reshape(-1).contiguous()
-        del f
-    if args.count:
-        count = args.count
-        x = x[:count].contiguous()
+    count = world_count(world, args.count)
+    xh = gen_rank(world, rank, count)
+    x = torch.from_numpy(xh).to(dev)
     comm = zcomm.Communicator(rank, world, dev_index)
-    if rel_mode == "abs":
-        rel = ABS_EB / max_over_ranks(x.abs().max().item())
-    else:
-        rel = 1e-3
+    gmax = max_over_ranks(float(np.abs(xh).max()))
+    rel = eb_rel(world, gmax)
+    # shared Huffman context primed like prime_shared_huffman (bench.cpp:169-204): rank 0's first
+    # 1 Mi symbols at the run's global scale, broadcast so every rank holds the same table
+    prime = torch.zeros(1 << 20, dtype=torch.int32)
+    if rank == 0:
+        prime = torch.from_numpy(np.clip(np.round(xh[: 1 << 20].astype(np.float64) / (2.0 * rel * gmax)),
+                                         -2**31, 2**31 - 1).astype(np.int32))
+    pt = prime.to(dev) if dist.get_backend() == "nccl" else prime
+    dist.broadcast(pt, 0)
+    comm.set_shared_huffman_from_bytes(pt.cpu().numpy().tobytes())
     out = torch.empty_like(x)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -572,6 +681,8 @@ def allreduce_bench(args):
                     "h2d_bytes_per_step": S, "d2h_bytes_per_step": S},
             "gpu_launches": launches, "clocks": clk.summary(),
         }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = collective_cpu_baseline(world, count, args.ref_sample)
     comm.close()
     dist.destroy_process_group()
     return line
@@ -588,9 +699,20 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-loopback", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=16 << 20,
+                    help="elements per rank of the collective CPU baseline's bounded sample")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun (what the driver does itself)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         line = reference_arm(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1:

@@ -13,13 +13,27 @@
 // them: mailbox exchange -> (scale reconciliation) -> one exchange kernel per ring step
 // (zc_encode.cu: per 4 MiB unit, profile/select/encode straight into the successor's bank, then
 // decode the predecessor's frame and int32-add / store it into the local chunk) -> (dequantize).
+//
+// Flag protocol: every wait is on a word in the rank's OWN block and is a stream memory operation
+// (cuStreamWaitValue64, GEQ) — no kernel spins, so a collective holds no SM while it waits, does
+// not depend on co-residency with its peers' kernels, and can be profiled under ncu's kernel
+// serialisation.  Signals are stream writes (cuStreamWriteValue64, with its implicit system-scope
+// fence) or release stores from the kernel that produced the data.  A peer that never signals
+// is caught by the host watchdog in finish(), which poisons every rank (transport.cpp:90-95) and
+// releases the local waits so the stream drains.
+#include <cuda.h>
+#include <time.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "zc_api_internal.h"
@@ -70,8 +84,8 @@ Layout make_layout(uint32_t nbanks, uint32_t runits) {
   o += align_up(8ull * nbanks, kAlign);
   L.off_sready = o;  // [kRegions] pieces received in region i (written by the predecessor)
   o += kAlign;
-  L.off_scredit = o;  // [0]: pieces this rank has consumed from its regions (read by its senders)
-  o += kAlign;
+  L.off_scredit = o;  // [r]: pieces rank r has consumed from its regions (written by rank r)
+  o += align_up(8ull * kMaxRanks, kAlign);
   L.off_err = o;
   o += kAlign;
   L.off_mbox = o;
@@ -149,11 +163,10 @@ struct MailArgs {
 // epoch), then the op's reduction.  This carries the StreamMeta ring (collectives.cpp:437-458)
 // and allreduce_max (:398-421): each is n-1 raw frames per rank in the reference's WireStats,
 // which the host adds (they are 24- and 8-byte control messages either way).
-__global__ void mailbox_kernel(MailArgs a) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  uint32_t* err_self = reinterpret_cast<uint32_t*>(a.peers[a.rank] + a.off_err);
-  const int par = static_cast<int>(a.epoch & 1);
-  uint32_t rec[8];
+// mail_post_kernel writes this rank's record into every rank's slot; the flags that publish it
+// and the waits for the peers' records are stream memory operations (launch_mail); then
+// mail_reduce_kernel reduces the local mailbox.
+__device__ __forceinline__ void mail_record(const MailArgs& a, uint32_t (&rec)[8]) {
   for (int i = 0; i < 8; ++i) rec[i] = a.rec[i];
   if (a.rec_from_absmax) {
     unsigned long long b = __double_as_longlong(a.scal->absmax);
@@ -165,27 +178,21 @@ __global__ void mailbox_kernel(MailArgs a) {
     rec[4] = static_cast<uint32_t>(b);
     rec[5] = static_cast<uint32_t>(b >> 32);
   }
-  for (int r = 0; r < a.nranks; ++r) {
-    uint32_t* slot = reinterpret_cast<uint32_t*>(a.peers[r] + a.off_mbox + (par * kMaxRanks + a.rank) * 32);
-    for (int i = 0; i < 8; ++i) slot[i] = rec[i];
-  }
-  __threadfence_system();
-  for (int r = 0; r < a.nranks; ++r)
-    st_rel(reinterpret_cast<unsigned long long*>(a.peers[r] + a.off_mflag) + a.rank, a.epoch);
-  const unsigned long long* my_flags = reinterpret_cast<const unsigned long long*>(a.peers[a.rank] + a.off_mflag);
-  const unsigned long long t0 = gtimer();
-  for (int r = 0; r < a.nranks; ++r) {
-    while (ld_acq(my_flags + r) < a.epoch) {
-      if (*reinterpret_cast<volatile uint32_t*>(err_self) != 0) return;
-      if (gtimer() - t0 > a.timeout_ns) {
-        for (int q = 0; q < a.nranks; ++q)
-          atomicOr(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_err), ZC_DERR_TIMEOUT);
-        return;
-      }
-      __nanosleep(64);
-    }
-  }
-  if (a.op == MAIL_BARRIER) return;
+}
+
+__global__ void mail_post_kernel(MailArgs a) {
+  const int r = threadIdx.x;
+  if (r >= a.nranks) return;
+  uint32_t rec[8];
+  mail_record(a, rec);
+  const int par = static_cast<int>(a.epoch & 1);
+  uint4* slot = reinterpret_cast<uint4*>(a.peers[r] + a.off_mbox + (par * kMaxRanks + a.rank) * 32);
+  slot[0] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+  slot[1] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
+}
+
+__device__ void mail_reduce(const MailArgs& a) {
+  const int par = static_cast<int>(a.epoch & 1);
   const uint8_t* mb = a.peers[a.rank] + a.off_mbox + par * kMaxRanks * 32;
   Scal* s = a.scal;
   if (a.op == MAIL_MAX || a.op == MAIL_EB_SCALE) {
@@ -223,6 +230,41 @@ __global__ void mailbox_kernel(MailArgs a) {
     s->requant = (shared != my_scale && my_scale > 0.0) ? 1u : 0u;
     s->requant_f = my_scale / shared;
   }
+}
+
+__global__ void mail_reduce_kernel(MailArgs a) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) mail_reduce(a);
+}
+
+// Fallback when the device has no 64-bit stream memory operations: the whole exchange in one
+// kernel that spins on the flags (bounded by the timeout; any rank's error word ends it).
+__global__ void mailbox_kernel(MailArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t* err_self = reinterpret_cast<uint32_t*>(a.peers[a.rank] + a.off_err);
+  const int par = static_cast<int>(a.epoch & 1);
+  uint32_t rec[8];
+  mail_record(a, rec);
+  for (int r = 0; r < a.nranks; ++r) {
+    uint32_t* slot = reinterpret_cast<uint32_t*>(a.peers[r] + a.off_mbox + (par * kMaxRanks + a.rank) * 32);
+    for (int i = 0; i < 8; ++i) slot[i] = rec[i];
+  }
+  __threadfence_system();
+  for (int r = 0; r < a.nranks; ++r)
+    st_rel(reinterpret_cast<unsigned long long*>(a.peers[r] + a.off_mflag) + a.rank, a.epoch);
+  const unsigned long long* my_flags = reinterpret_cast<const unsigned long long*>(a.peers[a.rank] + a.off_mflag);
+  const unsigned long long t0 = gtimer();
+  for (int r = 0; r < a.nranks; ++r) {
+    while (ld_acq(my_flags + r) < a.epoch) {
+      if (*reinterpret_cast<volatile uint32_t*>(err_self) != 0) return;
+      if (gtimer() - t0 > a.timeout_ns) {
+        for (int q = 0; q < a.nranks; ++q)
+          atomicOr(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_err), ZC_DERR_TIMEOUT);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+  if (a.op != MAIL_BARRIER) mail_reduce(a);
 }
 
 // Requantize to the shared scale: s = llround(s * (scale / shared)) (collectives.cpp:454-458).
@@ -338,10 +380,12 @@ __global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, 
   }
 }
 
-// The predecessor may reuse its target region: this rank has decoded the piece that was in it.
-__global__ void piece_done_kernel(unsigned long long* remote_credit, unsigned long long v) {
+// Fallback of the credit broadcast (no stream memory operations): this rank has decoded the
+// piece `v - 1`; every rank's copy of its consumed count advances (any of them may send next).
+__global__ void piece_done_kernel(uint8_t* const* peers, uint64_t off, int rank, int nranks, unsigned long long v) {
   __threadfence_system();
-  st_rel(remote_credit, v);
+  for (int r = threadIdx.x; r < nranks; r += blockDim.x)
+    st_rel(reinterpret_cast<unsigned long long*>(peers[r] + off) + rank, v);
 }
 
 int sm_count(int dev) {
@@ -371,6 +415,8 @@ struct zc_comm {
   unsigned long long epoch = 0;
   zc_wire_stats host_wire{};       // control frames (meta / max) counted on the host
   int share = 1;                   // ranks sharing this device (loopback groups)
+  bool memops = false;             // flag waits / writes as stream memory operations
+  unsigned wait_flags = 0;         // CU_STREAM_WAIT_VALUE_GEQ (| FLUSH where supported)
   bool connected = false;
   int32_t* sym = nullptr;          // symbol scratch for allreduce_eb
   uint64_t sym_cap = 0;
@@ -457,6 +503,144 @@ EncParams ring_enc(zc_comm* c, const int32_t* src, uint64_t bytes, int pin, int 
   return p;
 }
 
+// ---- enqueue order of single-process groups (the Communicator::run analogue)
+// Every rank of a group is enqueued by its own host thread, one thread at a time (a baton).  A
+// rank about to enqueue a wait for a flag value that no rank has enqueued the signal for yet
+// hands the baton on and resumes once some rank has.  So every wait is enqueued after the signal
+// that satisfies it: no launch ever depends on work enqueued after it, which is what ncu's
+// serialised kernel replay (and any launch-order scheduler) needs.  Signals are recorded in a
+// process-wide map of flag address -> highest value enqueued (flags only grow between resets).
+std::mutex g_sig_mu;
+std::unordered_map<const void*, unsigned long long>& posted_map() {
+  static std::unordered_map<const void*, unsigned long long> m;
+  return m;
+}
+void post_signal(const void* addr, unsigned long long v) {
+  std::lock_guard<std::mutex> g(g_sig_mu);
+  auto& x = posted_map()[addr];
+  x = std::max(x, v);
+}
+void forget_signals(const uint8_t* lo, const uint8_t* hi) {  // flags in [lo, hi) were zeroed
+  std::lock_guard<std::mutex> g(g_sig_mu);
+  auto& m = posted_map();
+  for (auto it = m.begin(); it != m.end();)
+    it = (it->first >= static_cast<const void*>(lo) && it->first < static_cast<const void*>(hi)) ? m.erase(it) : std::next(it);
+}
+bool signal_posted(const void* addr, unsigned long long v) {
+  std::lock_guard<std::mutex> g(g_sig_mu);
+  auto& m = posted_map();
+  auto it = m.find(addr);
+  return it != m.end() && it->second >= v;
+}
+
+struct Baton {
+  std::mutex mu;
+  std::condition_variable cv;
+  int n = 0, turn = 0;
+  std::vector<int> state;  // 0 runnable, 1 waiting for a signal, 2 finished
+  std::vector<const void*> w_addr;
+  std::vector<unsigned long long> w_val;
+  // next rank to run after `r` (call with mu held); -1 when every rank has finished
+  int next_locked(int r) {
+    for (int k = 1; k <= n; ++k) {
+      const int q = (r + k) % n;
+      if (state[q] == 0 || (state[q] == 1 && signal_posted(w_addr[q], w_val[q]))) return q;
+    }
+    for (int k = 1; k <= n; ++k)  // no rank can make progress: a protocol error; let the
+      if (state[(r + k) % n] == 1) return (r + k) % n;  // watchdog catch it instead of hanging here
+    return -1;
+  }
+};
+thread_local Baton* tl_baton = nullptr;
+thread_local int tl_rank = -1;
+
+// Called by a rank thread before it enqueues a wait for *addr >= v.
+void baton_wait(const void* addr, unsigned long long v) {
+  Baton* b = tl_baton;
+  if (b == nullptr || signal_posted(addr, v)) return;
+  std::unique_lock<std::mutex> lk(b->mu);
+  const int r = tl_rank;
+  b->state[r] = 1;
+  b->w_addr[r] = addr;
+  b->w_val[r] = v;
+  const int q = b->next_locked(r);
+  b->turn = q < 0 ? r : q;
+  b->state[b->turn] = 0;
+  b->cv.notify_all();
+  b->cv.wait(lk, [&] { return b->turn == r; });
+  b->state[r] = 0;
+}
+
+// Runs enqueue(r) for every rank on its own thread under the baton; returns each rank's status
+// and error text.
+template <typename F>
+void baton_run(int n, F enqueue, std::vector<int>& rcs, std::vector<std::string>& msgs) {
+  Baton b;
+  b.n = n;
+  b.state.assign(n, 0);
+  b.w_addr.assign(n, nullptr);
+  b.w_val.assign(n, 0);
+  rcs.assign(n, ZC_OK);
+  msgs.assign(n, std::string());
+  std::vector<std::thread> th;
+  for (int r = 0; r < n; ++r)
+    th.emplace_back([&, r] {
+      tl_baton = &b;
+      tl_rank = r;
+      {
+        std::unique_lock<std::mutex> lk(b.mu);
+        b.cv.wait(lk, [&] { return b.turn == r; });
+      }
+      rcs[r] = enqueue(r);
+      if (rcs[r]) msgs[r] = zc_last_error();
+      std::unique_lock<std::mutex> lk(b.mu);
+      b.state[r] = 2;
+      const int q = b.next_locked(r);
+      if (q >= 0) {
+        b.turn = q;
+        b.state[q] = 0;
+      }
+      b.cv.notify_all();
+      tl_baton = nullptr;
+    });
+  for (auto& t : th) t.join();
+}
+
+// Stream memory operations on this rank's stream.  Waits are always on the rank's own block.
+// Driver entry points are resolved through the runtime (the library does not link libcuda).
+struct MemOps {
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  using AttrFn = CUresult (*)(int*, CUdevice_attribute, CUdevice);
+  WaitFn wait = nullptr, write = nullptr;
+  AttrFn attr = nullptr;
+  MemOps() {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess) wait = reinterpret_cast<WaitFn>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess) write = reinterpret_cast<WaitFn>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &f, cudaEnableDefault, &q) == cudaSuccess) attr = reinterpret_cast<AttrFn>(f);
+  }
+};
+const MemOps& memops() {
+  static MemOps m;
+  return m;
+}
+
+int stream_wait_geq(zc_comm* c, const void* flag, unsigned long long v) {
+  baton_wait(flag, v);
+  const CUresult r = memops().wait(reinterpret_cast<CUstream>(c->stream), reinterpret_cast<CUdeviceptr>(flag), v,
+                                   c->wait_flags);
+  return r == CUDA_SUCCESS ? ZC_OK : set_err(ZC_ERR_CUDA, "cuStreamWaitValue64 failed");
+}
+int stream_write(zc_comm* c, void* addr, unsigned long long v) {
+  post_signal(addr, v);
+  const CUresult r = memops().write(reinterpret_cast<CUstream>(c->stream), reinterpret_cast<CUdeviceptr>(addr), v,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? ZC_OK : set_err(ZC_ERR_CUDA, "cuStreamWriteValue64 failed");
+}
+
 int launch_mail(zc_comm* c, int op, const uint32_t rec[8], int from_absmax, double rel, int scale_from_scal = 0) {
   MailArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -474,9 +658,27 @@ int launch_mail(zc_comm* c, int op, const uint32_t rec[8], int from_absmax, doub
   a.rec_scale_from_scal = scale_from_scal;
   a.rel = rel;
   a.scal = c->scal();
+  if (!c->memops) {
+    for (int r = 0; r < c->nranks; ++r) post_signal(c->peer[r] + c->lay.off_mflag + 8ull * c->rank, a.epoch);
+    for (int r = 0; r < c->nranks; ++r) baton_wait(c->block + c->lay.off_mflag + 8ull * r, a.epoch);
+    note_launch();
+    mailbox_kernel<<<1, 32, 0, c->stream>>>(a);
+    return cuda_err(cudaGetLastError(), "mailbox");
+  }
+  if (op != MAIL_BARRIER) {
+    note_launch();
+    mail_post_kernel<<<1, 64, 0, c->stream>>>(a);
+    if (int rc = cuda_err(cudaGetLastError(), "mailbox post")) return rc;
+  }
+  // publish (the write's fence orders the records before the flag), then collect every record
+  for (int r = 0; r < c->nranks; ++r)
+    if (int rc = stream_write(c, c->peer[r] + c->lay.off_mflag + 8ull * c->rank, a.epoch)) return rc;
+  for (int r = 0; r < c->nranks; ++r)
+    if (int rc = stream_wait_geq(c, c->block + c->lay.off_mflag + 8ull * r, a.epoch)) return rc;
+  if (op == MAIL_BARRIER) return ZC_OK;
   note_launch();
-  mailbox_kernel<<<1, 32, 0, c->stream>>>(a);
-  return cuda_err(cudaGetLastError(), "mailbox");
+  mail_reduce_kernel<<<1, 32, 0, c->stream>>>(a);
+  return cuda_err(cudaGetLastError(), "mailbox reduce");
 }
 
 void count_ctrl_frames(zc_comm* c, uint64_t bytes) {
@@ -511,9 +713,26 @@ int exchange_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx,
 // published with a system-scope release; the successor decodes it with the fused sink (int32
 // add for reduce-scatter, store for all-gather) and returns the region with a credit.  Sends run
 // one piece ahead of receives, so a rank's encode of piece k overlaps its peers' decode of k-1.
-void launch_wait(zc_comm* c, const unsigned long long* flag, unsigned long long v) {
+int launch_wait(zc_comm* c, const unsigned long long* flag, unsigned long long v) {
+  if (c->memops) return stream_wait_geq(c, flag, v);
+  baton_wait(flag, v);
   note_launch();
   wait_geq_kernel<<<1, 1, 0, c->stream>>>(flag, v, c->d_peers, c->lay.off_err, c->rank, c->nranks, c->timeout_ns);
+  return cuda_err(cudaGetLastError(), "wait");
+}
+
+// This rank has consumed piece v-1 of its regions: every rank's copy of the count advances.
+int post_credit(zc_comm* c, unsigned long long v) {
+  const uint64_t off = c->lay.off_scredit + 8ull * c->rank;
+  if (!c->memops) {
+    for (int r = 0; r < c->nranks; ++r) post_signal(c->peer[r] + off, v);
+    note_launch();
+    piece_done_kernel<<<1, 64, 0, c->stream>>>(c->d_peers, c->lay.off_scredit, c->rank, c->nranks, v);
+    return cuda_err(cudaGetLastError(), "credit");
+  }
+  for (int r = 0; r < c->nranks; ++r)
+    if (int rc = stream_write(c, c->peer[r] + off, v)) return rc;
+  return ZC_OK;
 }
 
 // Piece sequence numbers are the RECEIVER's: a sender's ptx equals its receiver's prx whenever the
@@ -539,7 +758,9 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
   const uint64_t seq = c->ptx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
   if (seq >= kRegions)  // the receiver has consumed the piece that last used this region
-    launch_wait(c, reinterpret_cast<const unsigned long long*>(c->peer[to] + y.off_scredit), seq - kRegions + 1);
+    if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_scredit) + to,
+                             seq - kRegions + 1))
+      return rc;
   if (tl) cudaEventRecord(tl->e0, c->stream);
   uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
   auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
@@ -547,6 +768,7 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
                                    c->shared, &c->cfg.arb, res, reinterpret_cast<uint32_t*>(dst + y.reg_idx),
                                    c->err_word(), c->stream))
     return rc;
+  post_signal(reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg, seq + 1);
   note_launch();
   piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(bytes)), bytes,
                                              reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire),
@@ -566,7 +788,8 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
   if (tl) cudaEventRecord(tl->e0, c->stream);
   const uint64_t seq = c->prx++;
   const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
-  launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1);
+  if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1))
+    return rc;
   if (tl) cudaEventRecord(tl->e1, c->stream);
   const uint8_t* region = c->block + y.off_reg + reg * y.reg_stride;
   if (int rc = zc_i_decode_batches(region, kStageStride, ZC_STAGE_BANK_BYTES,
@@ -574,8 +797,7 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
                                    reinterpret_cast<const uint32_t*>(region + y.reg_idx), store ? OUT_BYTES : OUT_ADD_I32,
                                    dst, 1.0, nullptr, c->err_word(), c->stream, own ? 1 : 0))
     return rc;
-  note_launch();
-  piece_done_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(c->block + y.off_scredit), seq + 1);
+  if (int rc = post_credit(c, seq + 1)) return rc;
   if (tl) cudaEventRecord(tl->e2, c->stream);
   return cuda_err(cudaGetLastError(), "piece recv");
 }
@@ -666,6 +888,7 @@ int resync_pieces(zc_comm* c) {
   const Layout& y = c->lay;
   if (int rc = cuda_err(cudaMemsetAsync(c->block + y.off_sready, 0, y.off_err - y.off_sready, c->stream), "resync"))
     return rc;
+  forget_signals(c->block + y.off_sready, c->block + y.off_err);
   c->ptx = c->prx = 0;
   return launch_mail(c, MAIL_BARRIER, nullptr, 0, 0.0);
 }
@@ -829,8 +1052,58 @@ int status_from_err(uint32_t e) {
   return set_err(ZC_ERR_PEER, "link poisoned by an aborting peer");
 }
 
+void release_rank(zc_comm* c, uint32_t bit);
+
+// Host watchdog over a collective in flight: the stream's waits are memory operations with no
+// timeout of their own, so while it runs the rank's flag words are sampled; when none has moved
+// for the communicator's timeout, every rank is poisoned (ZC_DERR_TIMEOUT, the reference's link
+// poisoning) and this rank's flags are released so its stream drains.
+int drain(zc_comm* c) {
+  if (!c->memops) return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+  const Layout& y = c->lay;
+  const uint64_t lo = y.off_sready, hi = y.off_err;  // sready, scredit
+  std::vector<uint8_t> snap(hi - lo + 8ull * kMaxRanks), cur(snap.size());
+  auto sample = [&](std::vector<uint8_t>& v) {
+    cudaMemcpy(v.data(), c->block + lo, hi - lo, cudaMemcpyDeviceToHost);
+    cudaMemcpy(v.data() + (hi - lo), c->block + y.off_mflag, 8ull * kMaxRanks, cudaMemcpyDeviceToHost);
+  };
+  auto now = [] {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return static_cast<unsigned long long>(ts.tv_sec) * 1000000000ull + static_cast<unsigned long long>(ts.tv_nsec);
+  };
+  unsigned long long last = now(), spins = 0;
+  bool have = false;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return ZC_OK;
+    if (q != cudaErrorNotReady) return cuda_err(q, "collective");
+    if (++spins < 2000) {  // the common case: done within a few ms, no sampling
+      usleep(spins < 200 ? 5 : 50);
+      continue;
+    }
+    usleep(2000);
+    sample(cur);
+    if (!have || cur != snap) {
+      snap.swap(cur);
+      have = true;
+      last = now();
+      continue;
+    }
+    if (now() - last < c->timeout_ns) continue;
+    for (int r = 0; r < c->nranks; ++r) {  // poison every rank (link poisoning), release our waits
+      uint32_t e = 0;
+      cudaMemcpy(&e, c->peer[r] + y.off_err, 4, cudaMemcpyDeviceToHost);
+      e |= ZC_DERR_TIMEOUT;
+      cudaMemcpy(c->peer[r] + y.off_err, &e, 4, cudaMemcpyHostToDevice);
+    }
+    release_rank(c, ZC_DERR_TIMEOUT);
+    return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+  }
+}
+
 int finish(zc_comm* c) {
-  if (int rc = cuda_err(cudaStreamSynchronize(c->stream), "collective")) return rc;
+  if (int rc = drain(c)) return rc;
   uint32_t e = 0;
   if (int rc = cuda_err(cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost), "error word")) return rc;
   return status_from_err(e);
@@ -863,6 +1136,8 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     preload_fixed_kernels();
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, mailbox_kernel);
+    cudaFuncGetAttributes(&fa, mail_post_kernel);
+    cudaFuncGetAttributes(&fa, mail_reduce_kernel);
     cudaFuncGetAttributes(&fa, requant_kernel);
     cudaFuncGetAttributes(&fa, quantize_dev_kernel);
     cudaFuncGetAttributes(&fa, dequantize_dev_kernel);
@@ -875,6 +1150,16 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
   if (!rc) rc = cuda_err(cudaMalloc(&c->block, c->lay.total), "cudaMalloc block");
   if (!rc) rc = cuda_err(cudaMemset(c->block + c->lay.off_ready, 0, c->lay.total - c->lay.off_ready), "memset");
   if (!rc) rc = cuda_err(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  if (!rc) {
+    int ok = 0, flush = 0;
+    const MemOps& m = memops();
+    if (m.wait && m.write && m.attr) {  // CUdevice is the ordinal
+      m.attr(&ok, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, static_cast<CUdevice>(device));
+      m.attr(&flush, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, static_cast<CUdevice>(device));
+    }
+    c->memops = ok != 0 && std::getenv("ZC_COMM_SPIN") == nullptr;
+    c->wait_flags = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+  }
   if (!rc) rc = zc_i_reserve_scratch(c->stream, runits);
   if (rc) {
     if (c->block) cudaFree(c->block);
@@ -902,23 +1187,50 @@ int finalize_peers(zc_comm* c) {
 int finish(zc_comm* c);
 int reset_state(zc_comm* c);
 
-// Single-process group: every rank's work enqueued before any is awaited (ranks' kernels must run
-// concurrently), then one wait per rank; on failure every rank is reset.
+// Releases every wait of rank c's stream (its flag words to a huge value) after poisoning it.
+void release_rank(zc_comm* c, uint32_t bit) {
+  const Layout& y = c->lay;
+  uint32_t e = 0;
+  cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost);
+  e |= bit;
+  cudaMemcpy(c->err_word(), &e, 4, cudaMemcpyHostToDevice);
+  std::vector<unsigned long long> big((y.off_err - y.off_sready) / 8, 1ull << 62), bigm(kMaxRanks, 1ull << 62);
+  cudaMemcpy(c->block + y.off_sready, big.data(), y.off_err - y.off_sready, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->block + y.off_mflag, bigm.data(), 8ull * kMaxRanks, cudaMemcpyHostToDevice);
+}
+
+// Single-process group: every rank's collective is enqueued by its own host thread under the
+// baton (see baton_run), then each rank's stream is drained; on failure every rank is reset.
 template <typename F>
 int run_group(zc_comm* const* cs, int n, F enqueue) {
+  std::vector<int> rcs;
+  std::vector<std::string> msgs;
+  baton_run(n, [&](int r) -> int {
+    if (int rc = dev_guard(cs[r])) return rc;
+    if (int rc = order_after(cs[r], nullptr)) return rc;
+    return enqueue(r);
+  }, rcs, msgs);
   int first = ZC_OK;
-  for (int r = 0; r < n && !first; ++r) {
-    if ((first = dev_guard(cs[r]))) break;
-    if ((first = order_after(cs[r], nullptr))) break;
-    first = enqueue(r);
-  }
+  std::string msg;
+  for (int r = 0; r < n; ++r)
+    if (rcs[r] && !first) {
+      first = rcs[r];
+      msg = msgs[r];
+    }
+  if (first)  // a rank could not enqueue all of its part: its peers' waits would never be met
+    for (int r = 0; r < n; ++r) {
+      dev_guard(cs[r]);
+      release_rank(cs[r], ZC_DERR_ABORT);
+    }
   for (int r = 0; r < n; ++r) {
     dev_guard(cs[r]);
     int e = finish(cs[r]);
-    if (!first && e) first = e;
+    if (!first && e) {
+      first = e;
+      msg = zc_last_error();
+    }
   }
   if (first) {
-    std::string msg = zc_last_error();
     for (int r = 0; r < n; ++r) reset_state(cs[r]);
     set_err(first, msg);
   }
@@ -931,6 +1243,7 @@ int reset_state(zc_comm* c) {
   cudaStreamSynchronize(c->stream);
   const Layout& y = c->lay;
   int rc = cuda_err(cudaMemset(c->block + y.off_ready, 0, y.off_wire - y.off_ready), "reset");
+  forget_signals(c->block + y.off_ready, c->block + y.off_wire);
   c->tx_seq = c->rx_seq = 0;
   c->ptx = c->prx = 0;
   c->epoch = 0;
@@ -1298,24 +1611,8 @@ int zc_comm_reset_stats(zc_comm* c) {
 // Communicator::run analogue; ranks' kernels must run concurrently).
 int zc_group_allreduce_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count, int32_t mode,
                            double* h_scales, uint32_t levels) {
-  int rc = ZC_OK;
-  for (int r = 0; r < n && !rc; ++r) {
-    if ((rc = dev_guard(cs[r]))) break;
-    if ((rc = order_after(cs[r], nullptr))) break;
-    rc = enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels);
-  }
-  int first = rc;
-  for (int r = 0; r < n; ++r) {
-    dev_guard(cs[r]);
-    int e = finish(cs[r]);
-    if (!first && e) first = e;
-  }
-  if (first) {
-    std::string msg = zc_last_error();
-    for (int r = 0; r < n; ++r) reset_state(cs[r]);
-    set_err(first, msg);
-    return first;
-  }
+  int rc = run_group(cs, n, [&](int r) { return enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels); });
+  if (rc) return rc;
   for (int r = 0; r < n; ++r)
     if (n > 1 && count > 0) cudaMemcpy(&h_scales[r], &cs[r]->scal()->scale, 8, cudaMemcpyDeviceToHost);
   return ZC_OK;
@@ -1324,71 +1621,21 @@ int zc_group_allreduce_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, ui
 int zc_group_allreduce_eb_f32(zc_comm* const* cs, int n, const float* const* d_xs, void* const* d_outs, int32_t out_f64,
                               uint64_t count, double rel) {
   if (!(rel > 0.0) || rel > 1.0) return set_err(ZC_ERR_INVALID_ARGUMENT, "eb_quantize: rel must be in (0, 1]");
-  int rc = ZC_OK;
   // every allocation before any rank's kernels run: cudaFree/cudaMalloc may wait for the device
-  for (int r = 0; r < n && !rc; ++r) {
-    if ((rc = dev_guard(cs[r]))) break;
-    rc = ensure_sym(cs[r], count);
-  }
-  for (int r = 0; r < n && !rc; ++r) {
-    if ((rc = dev_guard(cs[r]))) break;
-    if ((rc = order_after(cs[r], nullptr))) break;
-    rc = enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel);
-  }
-  int first = rc;
   for (int r = 0; r < n; ++r) {
-    dev_guard(cs[r]);
-    int e = finish(cs[r]);
-    if (!first && e) first = e;
+    if (int rc = dev_guard(cs[r])) return rc;
+    if (int rc = ensure_sym(cs[r], count)) return rc;
   }
-  if (first) {
-    std::string msg = zc_last_error();
-    for (int r = 0; r < n; ++r) reset_state(cs[r]);
-    set_err(first, msg);
-  }
-  return first;
+  return run_group(cs, n, [&](int r) { return enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel); });
 }
 
 int zc_group_allgather_sym(zc_comm* const* cs, int n, int32_t* const* d_alls, uint64_t block) {
-  // enqueue-only variant of zc_comm_allgather_sym for every rank, then one sync per rank
-  int first = ZC_OK;
-  for (int r = 0; r < n && !first; ++r) {
-    if ((first = dev_guard(cs[r]))) break;
-    if ((first = order_after(cs[r], nullptr))) break;
-    first = enqueue_allgather(cs[r], d_alls[r], block);
-  }
-  for (int r = 0; r < n; ++r) {
-    dev_guard(cs[r]);
-    int e = finish(cs[r]);
-    if (!first && e) first = e;
-  }
-  if (first) {
-    std::string msg = zc_last_error();
-    for (int r = 0; r < n; ++r) reset_state(cs[r]);
-    set_err(first, msg);
-  }
-  return first;
+  return run_group(cs, n, [&](int r) { return enqueue_allgather(cs[r], d_alls[r], block); });
 }
 
 int zc_group_reduce_scatter_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count) {
-  int first = ZC_OK;
-  if (n > 1 && count > 0)
-    for (int r = 0; r < n && !first; ++r) {
-      if ((first = dev_guard(cs[r]))) break;
-      if ((first = order_after(cs[r], nullptr))) break;
-      first = enqueue_ring(cs[r], d_syms[r], count, false);
-    }
-  for (int r = 0; r < n; ++r) {
-    dev_guard(cs[r]);
-    int e = finish(cs[r]);
-    if (!first && e) first = e;
-  }
-  if (first) {
-    std::string msg = zc_last_error();
-    for (int r = 0; r < n; ++r) reset_state(cs[r]);
-    set_err(first, msg);
-  }
-  return first;
+  if (n == 1 || count == 0) return ZC_OK;
+  return run_group(cs, n, [&](int r) { return enqueue_ring(cs[r], d_syms[r], count, false); });
 }
 
 int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* outs) {
@@ -1398,24 +1645,21 @@ int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* 
     outs[0] = vs[0];
     return ZC_OK;
   }
-  int first = ZC_OK;
-  for (int r = 0; r < n && !first; ++r) {
-    if ((first = dev_guard(cs[r]))) break;
+  int rc = run_group(cs, n, [&](int r) {
     uint32_t rec[8] = {0};
     uint64_t b;
     std::memcpy(&b, &vs[r], 8);
     rec[0] = static_cast<uint32_t>(b);
     rec[1] = static_cast<uint32_t>(b >> 32);
     count_ctrl_frames(cs[r], 8);
-    first = launch_mail(cs[r], MAIL_MAX, rec, 0, 0.0);
-  }
+    return launch_mail(cs[r], MAIL_MAX, rec, 0, 0.0);
+  });
+  if (rc) return rc;
   for (int r = 0; r < n; ++r) {
     dev_guard(cs[r]);
-    int e = finish(cs[r]);
-    if (!first && e) first = e;
-    if (!e) cudaMemcpy(&outs[r], &cs[r]->scal()->out, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&outs[r], &cs[r]->scal()->out, 8, cudaMemcpyDeviceToHost);
   }
-  return first;
+  return ZC_OK;
 }
 
 int zc_group_alltoall_sym(zc_comm* const* cs, int n, const int32_t* const* d_sends, int32_t* const* d_recvs,

@@ -798,6 +798,10 @@ class Communicator:
     def set_shared_huffman(self, ctx: HuffmanContext):
         check(lib().zc_comm_set_shared_huffman(self._h, ctx.handle))
 
+    def set_shared_huffman_from_bytes(self, sample) -> None:
+        """Communicator::set_shared_huffman_from_bytes (collectives.cpp:99-106)."""
+        self.set_shared_huffman(HuffmanContext.from_bytes(sample))
+
     def allreduce(self, sym: torch.Tensor, scale: float, mode: int = abi.QUANT_ERROR_BOUNDED, levels: int = 0) -> float:
         s = C.c_double(scale)
         check(lib().zc_comm_allreduce_sym(self._h, _ptr(sym), sym.numel(), mode, C.byref(s), levels, _stream()))
