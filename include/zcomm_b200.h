@@ -166,6 +166,8 @@ typedef struct zc_collective_config { /* collectives.hpp:24-34 */
   int32_t pin;            /* ZC_PIN_* */
   int32_t serialized;     /* OverlapMode::Serialized forces lam = 1 (collectives.cpp:71-74) */
   uint64_t fused_codec_min_msg_bytes;
+  int32_t per_slot_framing; /* perSlotFraming: collectives batch at ZC_SLOT_BYTES (collectives.cpp:197-199) */
+  int32_t _pad;
 } zc_collective_config;
 
 /* Opaque handles. */
@@ -178,6 +180,14 @@ const char* zc_version(void);
 /* Kernels this library has launched in this process (all devices and streams). */
 uint64_t zc_launch_count(void);
 int zc_device_count(int* h_count);
+/* Plumbing for callers without the CUDA runtime (the C++ layer's host-returning helpers, C and
+ * FFI bindings): device allocation on the current device, and synchronous copies / fills whose
+ * direction follows the pointers (unified addressing). */
+int zc_device_malloc(uint64_t bytes, void** d_out);
+void zc_device_free(void* d_ptr);
+int zc_memcpy(void* dst, const void* src, uint64_t bytes);
+int zc_memset(void* d_ptr, int value, uint64_t bytes);
+int zc_stream_synchronize(void* stream); /* NULL = the legacy default stream */
 /* Reference defaults: ArbitrationConfig{} (rea.hpp:64-79), TransportHint{} (rea.hpp:33-36),
  * CollectiveConfig{} (collectives.hpp:24-34). */
 void zc_default_arb_config(zc_arb_config* h_cfg);
@@ -427,6 +437,18 @@ int zc_comm_timeline_origin_delta(zc_comm* a, zc_comm* b, double* sec);
 int zc_comm_sync(zc_comm* comm);
 /* Clean epoch after an aborted collective (Connection::reset_sim, transport.cpp:97-105). */
 int zc_comm_reset(zc_comm* comm);
+/* RankCtx::send_encoded / recv_decoded (collectives.cpp:350-364): point-to-point, any pair of ranks.
+ * The message is cut into batches (4 MiB, or ZC_SLOT_BYTES under per-slot framing), each framed by
+ * send_batch's dispatch (cfg.pin) straight into the pair's channel in the receiver's memory and
+ * counted in the sender's WireStats; the receiver decodes each frame (recv_batch, raw-copy
+ * fallback included).  A send returns once its frames are written, which needs the receiver to
+ * have consumed all but the last two pieces (the credit window); a receive returns with the data
+ * in d_dst. */
+int zc_comm_send_encoded(zc_comm* comm, int32_t peer, const void* d_raw, uint64_t raw_bytes, void* stream);
+int zc_comm_recv_decoded(zc_comm* comm, int32_t peer, void* d_dst, uint64_t dst_bytes, void* stream);
+/* Link poisoning from the host (Communicator::run when one rank's body throws, transport.cpp:90-95):
+ * every rank's pending and next collective fails with ZC_ERR_PEER until zc_comm_reset. */
+int zc_comm_abort(zc_comm* comm);
 /* Communicator::wire_stats / reset_stats (collectives.cpp:175-190). */
 int zc_comm_wire_stats(zc_comm* comm, zc_wire_stats* h_out);
 int zc_comm_reset_stats(zc_comm* comm);

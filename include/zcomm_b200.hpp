@@ -9,10 +9,12 @@
 // frame.hpp, quant.hpp, fixedlen.hpp, huffman.hpp, rea.hpp, collectives.hpp.
 #pragma once
 #include <cstdint>
+#include <exception>
 #include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "zcomm_b200.h"
@@ -174,6 +176,212 @@ inline void encode_best(const uint8_t* d_raw, size_t n, uint8_t* d_stage, size_t
   check(zc_encode_best(d_raw, n, d_stage, stage_len, &hint, ctx ? ctx->get() : nullptr, &cfg, d_result, stream));
 }
 
+// Device scratch for the host-returning helpers below (RAII over zc_device_malloc).
+class DeviceScratch {
+ public:
+  explicit DeviceScratch(size_t bytes) {
+    void* p = nullptr;
+    check(zc_device_malloc(bytes, &p));
+    p_ = p;
+  }
+  ~DeviceScratch() { zc_device_free(p_); }
+  DeviceScratch(const DeviceScratch&) = delete;
+  DeviceScratch& operator=(const DeviceScratch&) = delete;
+  template <class T>
+  T* as(size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(p_) + byte_off);
+  }
+
+ private:
+  void* p_ = nullptr;
+};
+// A device result of work queued on `stream`, read once that work is complete.
+template <class T>
+inline T read_back(const T* d_src, void* stream) {
+  check(zc_stream_synchronize(stream));
+  T v;
+  check(zc_memcpy(&v, d_src, sizeof(T)));
+  return v;
+}
+
+// ---- frame.hpp:52-58: frame_commit_raw on the device; returns the committed frame size (0: no room).
+inline size_t frame_commit_raw(const uint8_t* d_raw, size_t n, uint8_t* d_region, size_t region_len,
+                               void* stream = nullptr) {
+  DeviceScratch s(8);
+  check(zc_frame_commit_raw(d_raw, n, d_region, region_len, s.as<uint64_t>(), stream));
+  return static_cast<size_t>(read_back(s.as<uint64_t>(), stream));
+}
+
+// ---- the coder plugins (fixedlen.hpp:22-42, huffman.hpp:38-70), device spans.  Return values
+// follow the reference: encoders return the payload size (0 when it does not fit), decoders
+// whether the payload decoded.
+inline size_t fixedlen_encode(const int32_t* d_syms, size_t n, uint8_t* d_dst, size_t cap, unsigned* width,
+                              void* stream = nullptr) {
+  DeviceScratch s(16);
+  check(zc_fixedlen_encode(d_syms, n, d_dst, cap, s.as<uint64_t>(), s.as<uint32_t>(8), stream));
+  if (width) *width = read_back(s.as<uint32_t>(8), stream);
+  return static_cast<size_t>(read_back(s.as<uint64_t>(), stream));
+}
+inline bool fixedlen_decode_into(const FrameHeader& h, const uint8_t* d_payload, size_t payload_len, uint8_t* d_dst,
+                                 size_t dst_len, void* stream = nullptr) {
+  DeviceScratch s(4);
+  check(zc_fixedlen_decode(&h, d_payload, payload_len, d_dst, dst_len, s.as<int32_t>(), stream));
+  return read_back(s.as<int32_t>(), stream) == 1;
+}
+// huffman_encode: with embed, the payload starts with the 256 code lengths (huffman.cpp:216-246).
+// d_index (optional, ZC_HUFF_INDEX_ENTRIES u32): the companion index for the chunk-parallel decode.
+inline size_t huffman_encode(const uint8_t* d_raw, size_t n, const HuffmanContext& ctx, uint8_t* d_dst, size_t cap,
+                             bool embed, uint32_t* d_index = nullptr, void* stream = nullptr) {
+  DeviceScratch s(8);
+  check(zc_huffman_encode(d_raw, n, ctx.get(), d_dst, cap, embed ? 1 : 0, s.as<uint64_t>(), d_index, stream));
+  return static_cast<size_t>(read_back(s.as<uint64_t>(), stream));
+}
+inline bool huffman_decode_into(const FrameHeader& h, const uint8_t* d_payload, size_t payload_len,
+                                const HuffmanContext* shared, uint8_t* d_dst, size_t dst_len,
+                                const uint32_t* d_index = nullptr, void* stream = nullptr) {
+  DeviceScratch s(4);
+  check(zc_huffman_decode(&h, d_payload, payload_len, shared ? shared->get() : nullptr, d_index, d_dst, dst_len,
+                          s.as<int32_t>(), stream));
+  return read_back(s.as<int32_t>(), stream) == 1;
+}
+
+// ---- rea.cpp:93-118: profile_sample of a device span (the sample window is the first 64 KiB).
+inline SampleStats profile_sample(const uint8_t* d_raw, size_t n, const HuffmanContext* ctx, void* stream = nullptr) {
+  DeviceScratch s(sizeof(SampleStats));
+  check(zc_profile_sample(d_raw, n, ctx ? ctx->get() : nullptr, s.as<SampleStats>(), stream));
+  return read_back(s.as<SampleStats>(), stream);
+}
+
+// ---- collectives.hpp:48-110: the per-rank face of a communicator (non-owning).  Every call runs
+// on the rank's own stream after the caller's `stream` work and returns when complete, like the
+// reference's blocking RankCtx methods.  Buffers are device pointers.
+class RankCtx {
+ public:
+  explicit RankCtx(zc_comm* c) : c_(c) {}
+  int rank() const { return zc_comm_rank(c_); }
+  int nranks() const { return zc_comm_nranks(c_); }
+  // point-to-point (collectives.cpp:350-364): batched, framed per send_batch, decoded per recv_batch
+  void send_encoded(int peer, const void* d_raw, size_t bytes, void* stream = nullptr) {
+    check(zc_comm_send_encoded(c_, peer, d_raw, bytes, stream));
+  }
+  void recv_decoded(int peer, void* d_dst, size_t bytes, void* stream = nullptr) {
+    check(zc_comm_recv_decoded(c_, peer, d_dst, bytes, stream));
+  }
+  // RankCtx::allreduce(QuantizedStream&): symbols in place; returns the reconciled scale.
+  double allreduce(int32_t* d_sym, size_t count, double scale, int32_t mode = ZC_QUANT_ERROR_BOUNDED,
+                   uint32_t levels = 0, void* stream = nullptr) {
+    check(zc_comm_allreduce_sym(c_, d_sym, count, mode, &scale, levels, stream));
+    return scale;
+  }
+  void allreduce_eb(const float* d_x, float* d_out, size_t count, double rel, void* stream = nullptr) {
+    check(zc_comm_allreduce_eb_f32(c_, d_x, d_out, 0, count, rel, stream));
+  }
+  void allreduce_eb(const float* d_x, double* d_out, size_t count, double rel, void* stream = nullptr) {
+    check(zc_comm_allreduce_eb_f32(c_, d_x, d_out, 1, count, rel, stream));
+  }
+  void reduce_scatter(int32_t* d_sym, size_t count, void* stream = nullptr) {
+    check(zc_comm_reduce_scatter_sym(c_, d_sym, count, stream));
+  }
+  void allgather(int32_t* d_all, size_t block, void* stream = nullptr) {
+    check(zc_comm_allgather_sym(c_, d_all, block, stream));
+  }
+  void alltoall(const int32_t* d_send, int32_t* d_recv, size_t block, void* stream = nullptr) {
+    check(zc_comm_alltoall_sym(c_, d_send, d_recv, block, stream));
+  }
+  void broadcast(int32_t* d_data, size_t count, int root, void* stream = nullptr) {
+    check(zc_comm_broadcast_sym(c_, d_data, count, root, stream));
+  }
+  void group_execute(std::vector<zc_coll_request>& reqs, void* stream = nullptr) {
+    check(zc_comm_group_execute(c_, reqs.data(), static_cast<int32_t>(reqs.size()), stream));
+  }
+  double allreduce_max(double v, void* stream = nullptr) {
+    double o = 0;
+    check(zc_comm_allreduce_max(c_, v, &o, stream));
+    return o;
+  }
+  zc_comm* get() const { return c_; }
+
+ private:
+  zc_comm* c_;
+};
+
+// ---- collectives.hpp:111-153, single process: Communicator(n, cfg) + run(fn) with one thread per
+// rank (ranks on local devices; several may share one GPU).  A rank whose body throws poisons
+// every link (zc_comm_abort), so peers blocked on it fail with PeerError; run() then resets the
+// communicator and rethrows the root cause (the first exception that is not a PeerError).
+class LocalCommunicator {
+ public:
+  LocalCommunicator(int nranks, const std::vector<int>& devices, const CollectiveConfig& cfg) : cs_(nranks, nullptr) {
+    check(zc_comm_create_group(nranks, devices.data(), &cfg, cs_.data()));
+  }
+  LocalCommunicator(int nranks, int device, const CollectiveConfig& cfg)
+      : LocalCommunicator(nranks, std::vector<int>(static_cast<size_t>(nranks), device), cfg) {}
+  ~LocalCommunicator() {
+    for (zc_comm* c : cs_) zc_comm_destroy(c);
+  }
+  LocalCommunicator(const LocalCommunicator&) = delete;
+  LocalCommunicator& operator=(const LocalCommunicator&) = delete;
+  int nranks() const { return static_cast<int>(cs_.size()); }
+  void set_shared_huffman(const HuffmanContext& ctx) {
+    for (zc_comm* c : cs_) check(zc_comm_set_shared_huffman(c, ctx.get()));
+  }
+  template <class F>
+  void run(F&& fn) {
+    const int n = nranks();
+    std::vector<std::exception_ptr> errs(static_cast<size_t>(n));
+    std::vector<std::thread> th;
+    for (int r = 0; r < n; ++r)
+      th.emplace_back([&, r] {
+        try {
+          RankCtx ctx(cs_[static_cast<size_t>(r)]);
+          fn(ctx);
+        } catch (...) {
+          errs[static_cast<size_t>(r)] = std::current_exception();
+          zc_comm_abort(cs_[static_cast<size_t>(r)]);
+        }
+      });
+    for (auto& t : th) t.join();
+    std::exception_ptr root, any;
+    for (auto& e : errs) {
+      if (!e) continue;
+      if (!any) any = e;
+      if (!root) {
+        try {
+          std::rethrow_exception(e);
+        } catch (const PeerError&) {
+        } catch (...) {
+          root = e;
+        }
+      }
+    }
+    if (!any) return;
+    for (zc_comm* c : cs_) zc_comm_reset(c);
+    std::rethrow_exception(root ? root : any);
+  }
+  // Communicator::wire_stats (collectives.cpp:175-186): summed over ranks.
+  WireStats wire_stats() const {
+    WireStats s{};
+    for (zc_comm* c : cs_) {
+      WireStats w;
+      check(zc_comm_wire_stats(c, &w));
+      for (int i = 0; i < 3; ++i) s.frames_by_codec[i] += w.frames_by_codec[i];
+      s.raw_bytes += w.raw_bytes;
+      s.payload_bytes += w.payload_bytes;
+      s.total_bytes += w.total_bytes;
+      s.index_bytes += w.index_bytes;
+      s.wall_codec_sec += w.wall_codec_sec;
+    }
+    return s;
+  }
+  void reset_stats() {
+    for (zc_comm* c : cs_) check(zc_comm_reset_stats(c));
+  }
+  RankCtx rank_ctx(int r) const { return RankCtx(cs_.at(static_cast<size_t>(r))); }
+
+ private:
+  std::vector<zc_comm*> cs_;
+};
+
 // ---- collectives.hpp:48-153: one rank of a multi-process communicator (RAII)
 class Communicator {
  public:
@@ -190,6 +398,15 @@ class Communicator {
     check(zc_comm_connect(c, all.data()));
   }
   void set_shared_huffman(const HuffmanContext& ctx) { check(zc_comm_set_shared_huffman(h_.get(), ctx.get())); }
+  // Communicator::run for this process's rank: fn(RankCtx&).
+  template <class F>
+  void run(F&& fn) {
+    RankCtx ctx(h_.get());
+    fn(ctx);
+  }
+  RankCtx rank_ctx() const { return RankCtx(h_.get()); }
+  void send_encoded(int peer, const void* d_raw, size_t bytes) { rank_ctx().send_encoded(peer, d_raw, bytes); }
+  void recv_decoded(int peer, void* d_dst, size_t bytes) { rank_ctx().recv_decoded(peer, d_dst, bytes); }
   // RankCtx::allreduce(QuantizedStream&): symbols in place; returns the reconciled scale.
   double allreduce(int32_t* d_sym, size_t count, double scale, int32_t mode = ZC_QUANT_ERROR_BOUNDED,
                    uint32_t levels = 0) {

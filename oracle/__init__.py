@@ -98,6 +98,7 @@ class Port:
              P(abi.ArbConfig), C.c_uint64, P(abi.WireStats))
         _sig(L, "zo_ring_allgather", C.c_int, C.c_int, i32p, C.c_uint64, C.c_int, P(abi.TransportHint), H,
              P(abi.ArbConfig), i32p, P(abi.WireStats))
+        _sig(L, "zo_set_per_slot_framing", None, C.c_int)
         _sig(L, "zo_gen_data", C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, f64p)
 
     # --- convenience wrappers (numpy in, numpy out) ---
@@ -162,14 +163,18 @@ class Port:
         p = self.lib.zo_huffman_encode(raw, len(raw), C.byref(ctx), out, len(out), 1 if embed else 0)
         return out[:p].copy()
 
-    def ring_allgather(self, blocks, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None):
+    def ring_allgather(self, blocks, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None, per_slot=False):
         blocks = np.ascontiguousarray(blocks, np.int32)
         n, block = blocks.shape
         out = np.zeros((n, n * block), np.int32)  # every rank's gathered copy
         w = abi.WireStats()
-        rc = self.lib.zo_ring_allgather(n, blocks.ravel(), block, pin, C.byref(hint or abi.make_hint()),
-                                        C.byref(ctx) if ctx is not None else None,
-                                        C.byref(cfg or abi.default_arb_config()), out.ravel(), C.byref(w))
+        self.lib.zo_set_per_slot_framing(1 if per_slot else 0)
+        try:
+            rc = self.lib.zo_ring_allgather(n, blocks.ravel(), block, pin, C.byref(hint or abi.make_hint()),
+                                            C.byref(ctx) if ctx is not None else None,
+                                            C.byref(cfg or abi.default_arb_config()), out.ravel(), C.byref(w))
+        finally:
+            self.lib.zo_set_per_slot_framing(0)
         return rc, out, w
 
     def encode_batches(self, raw, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None, stage_len=abi.STAGE_BANK_BYTES):
@@ -200,14 +205,18 @@ class Port:
         return st
 
     def ring_allreduce(self, syms, scales, pin=abi.PIN_AUTO, hint=None, ctx=None, cfg=None,
-                       fused_min=abi.BATCH_RAW_BYTES):
+                       fused_min=abi.BATCH_RAW_BYTES, per_slot=False):
         syms = np.ascontiguousarray(syms, np.int32).copy()
         n, count = syms.shape
         sc = np.ascontiguousarray(scales, np.float64).copy()
         w = abi.WireStats()
-        rc = self.lib.zo_ring_allreduce(n, syms.ravel(), count, sc, pin, C.byref(hint or abi.make_hint()),
-                                        C.byref(ctx) if ctx is not None else None,
-                                        C.byref(cfg or abi.default_arb_config()), fused_min, C.byref(w))
+        self.lib.zo_set_per_slot_framing(1 if per_slot else 0)
+        try:
+            rc = self.lib.zo_ring_allreduce(n, syms.ravel(), count, sc, pin, C.byref(hint or abi.make_hint()),
+                                            C.byref(ctx) if ctx is not None else None,
+                                            C.byref(cfg or abi.default_arb_config()), fused_min, C.byref(w))
+        finally:
+            self.lib.zo_set_per_slot_framing(0)
         return rc, syms, sc, w
 
 

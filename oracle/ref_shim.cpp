@@ -141,6 +141,7 @@ CollectiveConfig to_ccfg(const zc_collective_config* c) {
   cc.pin = static_cast<CodecPin>(c->pin);
   cc.overlap = c->serialized ? OverlapMode::Serialized : OverlapMode::Pipelined;
   cc.fusedCodecMinMsgBytes = c->fused_codec_min_msg_bytes;
+  cc.perSlotFraming = c->per_slot_framing != 0;
   return cc;
 }
 

@@ -824,21 +824,28 @@ static void wire_add(zc_wire_stats* w, const zc_encode_result* r, uint64_t raw) 
 }
 
 /* One lockstep exchange of `bytes` per rank (collectives.cpp:366-396): each rank's outgoing span is
- * cut into 4 MiB batches, encoded, and decoded by the successor into scratch.  src[r] is rank r's
+ * cut into chunk_raw_bytes batches (4 MiB, or 512 KiB slots), encoded, and decoded by the successor into scratch.  src[r] is rank r's
  * outgoing span; dst[r] receives what rank r gets from its predecessor.  add != 0 selects the RS
  * sink (int64-checked add into dst). */
+/* RankCtx::chunk_raw_bytes (collectives.cpp:197-199): 512 KiB slots under
+ * CollectiveConfig::perSlotFraming, else 4 MiB batches.  Every exchange of the ring simulation cuts
+ * its spans at this size; the stage capacity stays one bank (kStageBankBytes). */
+static uint64_t g_chunk_raw = ZC_BATCH_RAW_BYTES;
+void zo_set_per_slot_framing(int on) { g_chunk_raw = on ? ZC_SLOT_BYTES : ZC_BATCH_RAW_BYTES; }
+
 static int ring_exchange(int n, uint8_t** src, uint8_t** dst, uint64_t bytes, int pin, int add,
                          const zc_transport_hint* hint, const zo_huff* ctx, const zc_arb_config* cfg,
                          zc_wire_stats* wire) {
   if (bytes == 0) return 0;
+  const uint64_t step = g_chunk_raw;
   uint8_t* stage = (uint8_t*)malloc(ZC_STAGE_BANK_BYTES);
   uint8_t* scratch = (uint8_t*)malloc(ZC_BATCH_RAW_BYTES);
   uint8_t** frames = (uint8_t**)calloc((size_t)n, sizeof(uint8_t*));
   uint64_t* flen = (uint64_t*)calloc((size_t)n, sizeof(uint64_t));
   int rc = 0;
   for (int r = 0; r < n; ++r) frames[r] = (uint8_t*)malloc(ZC_STAGE_BANK_BYTES);
-  for (uint64_t off = 0; off < bytes && rc == 0; off += ZC_BATCH_RAW_BYTES) {
-    uint64_t len = bytes - off < ZC_BATCH_RAW_BYTES ? bytes - off : ZC_BATCH_RAW_BYTES;
+  for (uint64_t off = 0; off < bytes && rc == 0; off += step) {
+    uint64_t len = bytes - off < step ? bytes - off : step;
     for (int r = 0; r < n; ++r) {
       zc_encode_result er;
       zo_send_batch(src[r] + off, len, frames[r], ZC_STAGE_BANK_BYTES, pin, hint, ctx, cfg, &er);

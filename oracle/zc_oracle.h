@@ -91,6 +91,9 @@ int zo_recv_batch(const uint8_t* frame, uint64_t frame_len, const zo_huff* ctx, 
 /* Serial simulation of the ring algorithms (collectives.cpp:423-503, 525-544) over all ranks.
  * syms: nranks*count, in/out.  Returns 0, or ZC_ERR_OVERFLOW / ZC_ERR_RUNTIME.  wire accumulates
  * exactly what WireStats counts (meta frames included).  scales: per-rank in/out (reconciled). */
+/* CollectiveConfig::perSlotFraming (collectives.hpp:33): the ring functions below batch at 512 KiB
+ * (RankCtx::chunk_raw_bytes, collectives.cpp:197-199) while on.  Process-wide; tests only. */
+void zo_set_per_slot_framing(int on);
 int zo_ring_allreduce(int nranks, int32_t* syms, uint64_t count, double* scales, int pin,
                       const zc_transport_hint* hint, const zo_huff* ctx, const zc_arb_config* cfg,
                       uint64_t fused_min_msg_bytes, zc_wire_stats* wire);

@@ -100,7 +100,8 @@ class TimelineRow(C.Structure):          # zc_timeline_row (measured BatchTimeli
 
 class CollectiveConfig(C.Structure):     # collectives.hpp:24-34
     _fields_ = [("arb", ArbConfig), ("hint", TransportHint), ("pin", C.c_int32),
-                ("serialized", C.c_int32), ("fused_codec_min_msg_bytes", C.c_uint64)]
+                ("serialized", C.c_int32), ("fused_codec_min_msg_bytes", C.c_uint64),
+                ("per_slot_framing", C.c_int32), ("_pad", C.c_int32)]
 
 
 def default_arb_config() -> ArbConfig:

@@ -52,30 +52,53 @@ uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // piece (stage stride as in zcomm.py's Frames), their Huffman companion index and EncodeResults.
 constexpr uint32_t kRegions = 3;
 
+// Point-to-point channels (RankCtx::send_encoded / recv_decoded, collectives.cpp:350-364): every
+// directed pair s -> d owns kP2PRegions regions of kP2PUnits frames in d's block, so any rank may
+// send to any rank at any time without the ring's piece counters.
+constexpr uint32_t kP2PRegions = 2;
+constexpr uint32_t kP2PUnits = 4;
+
 struct Layout {
-  uint32_t nbanks, runits;
+  uint32_t nbanks, runits, nranks;
+  uint64_t ub, fstride;  // unit (batch) raw bytes; frame stride inside a piece region
   uint64_t bank_stride, idx_off;
   uint64_t reg_stride, reg_idx, reg_res;  // region size; index / results offsets inside a region
-  uint64_t off_banks, off_reg, off_ready, off_len, off_credit, off_sready, off_scredit, off_err, off_mbox, off_mflag,
-      off_wire, off_errall, off_scal, off_peers, total;
+  uint64_t p2p_stride, p2p_idx, p2p_res;  // the same for a point-to-point region (kP2PUnits frames)
+  uint64_t off_banks, off_reg, off_p2p, off_ready, off_len, off_credit, off_sready, off_scredit, off_pready, off_pcons,
+      off_err, off_mbox, off_mflag, off_wire, off_errall, off_scal, off_peers, total;
 };
 
 constexpr uint64_t kStageStride = (ZC_STAGE_BANK_BYTES + 255) / 256 * 256;
+// Per-slot framing (CollectiveConfig::perSlotFraming, collectives.cpp:197-199, 289-290): 512 KiB
+// batches.  A frame keeps a whole bank of capacity (the encoders' stage_len, so every decision is
+// the reference's), but no frame of a 512 KiB batch can exceed header + codebook + 32 bits per raw
+// byte (Huffman codes are <= 32 bits; FixedLen and RAW payloads are <= the raw bytes), so the
+// frames sit at this smaller stride inside a piece region.
+constexpr uint64_t kSlotFrameStride =
+    (ZC_HEADER_BYTES + ZC_HUFF_CODEBOOK_BYTES + 4 * ZC_SLOT_BYTES + 1024 + 255) / 256 * 256;
 
-Layout make_layout(uint32_t nbanks, uint32_t runits) {
+Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nranks) {
   Layout L;
   L.nbanks = nbanks;
   L.runits = runits;
+  L.nranks = nranks;
+  L.ub = per_slot ? ZC_SLOT_BYTES : ZC_BATCH_RAW_BYTES;
+  L.fstride = per_slot ? kSlotFrameStride : kStageStride;
   L.idx_off = align_up(ZC_STAGE_BANK_BYTES, kAlign);
   L.bank_stride = L.idx_off + align_up(ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
-  L.reg_idx = runits * kStageStride;
+  L.reg_idx = runits * L.fstride;
   L.reg_res = L.reg_idx + align_up(runits * ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
   L.reg_stride = L.reg_res + align_up(runits * sizeof(zc_encode_result), kAlign);
+  L.p2p_idx = kP2PUnits * L.fstride;
+  L.p2p_res = L.p2p_idx + align_up(kP2PUnits * ZC_HUFF_INDEX_ENTRIES * 4ull, kAlign);
+  L.p2p_stride = L.p2p_res + align_up(kP2PUnits * sizeof(zc_encode_result), kAlign);
   uint64_t o = 0;
   L.off_banks = o;
   o += nbanks * L.bank_stride;
   L.off_reg = o;
   o += kRegions * L.reg_stride;
+  L.off_p2p = o;  // [sender][kP2PRegions] regions (none for a single rank)
+  o += nranks > 1 ? static_cast<uint64_t>(nranks) * kP2PRegions * L.p2p_stride : 0;
   L.off_ready = o;
   o += align_up(8ull * nbanks, kAlign);
   L.off_len = o;
@@ -85,6 +108,10 @@ Layout make_layout(uint32_t nbanks, uint32_t runits) {
   L.off_sready = o;  // [kRegions] pieces received in region i (written by the predecessor)
   o += kAlign;
   L.off_scredit = o;  // [r]: pieces rank r has consumed from its regions (written by rank r)
+  o += align_up(8ull * kMaxRanks, kAlign);
+  L.off_pready = o;  // [s][kP2PRegions]: point-to-point piece count in region i from sender s
+  o += align_up(8ull * kMaxRanks * kP2PRegions, kAlign);
+  L.off_pcons = o;  // [d]: point-to-point pieces rank d has consumed from this rank (written by d)
   o += align_up(8ull * kMaxRanks, kAlign);
   L.off_err = o;
   o += kAlign;
@@ -346,7 +373,7 @@ __global__ void wait_geq_kernel(const unsigned long long* flag, unsigned long lo
 
 // After a piece's frames are in the successor's region: count them into this rank's WireStats
 // (send_batch's accounting, collectives.cpp:285-296) and publish the piece (system-scope release).
-__global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, uint64_t raw_total,
+__global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, uint64_t raw_total, uint64_t ub,
                                   zc_wire_stats* wire, unsigned long long* remote_ready, unsigned long long v,
                                   zc_encode_result* log) {
   unsigned long long f[3] = {0, 0, 0}, raw = 0, pay = 0, tot = 0, idx = 0;
@@ -354,7 +381,7 @@ __global__ void piece_sent_kernel(const zc_encode_result* res, uint32_t nunits, 
     const zc_encode_result r = res[u];
     if (log) log[u] = r;
     if (r.total_bytes == 0) continue;  // capacity failure: reported through the error word
-    const uint64_t R = (raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES < ZC_BATCH_RAW_BYTES ? raw_total - static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES : static_cast<uint64_t>(ZC_BATCH_RAW_BYTES));
+    const uint64_t R = raw_total - static_cast<uint64_t>(u) * ub < ub ? raw_total - static_cast<uint64_t>(u) * ub : ub;
     f[r.codec < 3 ? r.codec : 0] += 1;
     raw += R;
     pay += r.payload_bytes;
@@ -388,6 +415,12 @@ __global__ void piece_done_kernel(uint8_t* const* peers, uint64_t off, int rank,
     st_rel(reinterpret_cast<unsigned long long*>(peers[r] + off) + rank, v);
 }
 
+// Fallback of a single credit write (no stream memory operations).
+__global__ void flag_store_kernel(unsigned long long* flag, unsigned long long v) {
+  __threadfence_system();
+  st_rel(flag, v);
+}
+
 int sm_count(int dev) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -412,6 +445,7 @@ struct zc_comm {
   zc_huff_ctx* shared = nullptr;   // installed shared Huffman context (owned)
   uint64_t tx_seq = 0, rx_seq = 0;
   uint64_t ptx = 0, prx = 0;       // pieces sent to the successor / received from the predecessor
+  std::vector<uint64_t> p2p_tx, p2p_rx;  // point-to-point pieces sent to / received from each rank
   unsigned long long epoch = 0;
   zc_wire_stats host_wire{};       // control frames (meta / max) counted on the host
   int share = 1;                   // ranks sharing this device (loopback groups)
@@ -479,7 +513,8 @@ Link make_link(zc_comm* c) {
 }
 
 uint64_t chunk_lo(uint64_t count, int n, int c) { return static_cast<uint64_t>(c) * count / static_cast<uint64_t>(n); }
-uint64_t nbatches(uint64_t bytes) { return (bytes + ZC_BATCH_RAW_BYTES - 1) / ZC_BATCH_RAW_BYTES; }
+uint64_t nbatches(uint64_t bytes, uint64_t ub) { return (bytes + ub - 1) / ub; }
+uint64_t nbatches(const zc_comm* c, uint64_t bytes) { return nbatches(bytes, c->lay.ub); }
 
 EncParams ring_enc(zc_comm* c, const int32_t* src, uint64_t bytes, int pin, int rx_add, int tx) {
   EncParams p;
@@ -490,8 +525,8 @@ EncParams ring_enc(zc_comm* c, const int32_t* src, uint64_t bytes, int pin, int 
   p.pin = pin;
   p.scale = p.rcp = 1.0;
   p.total_bytes = bytes;
-  p.unit_bytes = ZC_BATCH_RAW_BYTES;
-  p.nunits = static_cast<uint32_t>(nbatches(bytes));
+  p.unit_bytes = c->lay.ub;
+  p.nunits = static_cast<uint32_t>(nbatches(c, bytes));
   p.stage_len = ZC_STAGE_BANK_BYTES;
   p.hint = c->cfg.hint;
   p.cfg = c->cfg.arb;
@@ -699,7 +734,7 @@ int exchange_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx,
   p.rx_store = store ? 1 : 0;
   p.rx_dst = rx;
   p.rx_total_bytes = rx_bytes;
-  p.rx_nunits = static_cast<uint32_t>(nbatches(rx_bytes));
+  p.rx_nunits = static_cast<uint32_t>(nbatches(c, rx_bytes));
   if (p.nunits == 0 && p.rx_nunits == 0) return ZC_OK;
   if (int rc = cuda_err(launch_encode(p, c->stream), what)) return rc;
   c->tx_seq += p.nunits;
@@ -743,7 +778,7 @@ int post_credit(zc_comm* c, unsigned long long v) {
 // Timeline records (no-ops unless zc_comm_timeline_enable): events around a piece.
 zc_comm::TlPiece* tl_begin(zc_comm* c, int kind, int peer, uint64_t seq, uint64_t bytes) {
   if (c->tl_cap == 0 || static_cast<int>(c->tl.size()) >= c->tl_cap) return nullptr;
-  zc_comm::TlPiece t{seq, bytes, kind, peer, static_cast<uint32_t>(nbatches(bytes)), nullptr, nullptr, nullptr};
+  zc_comm::TlPiece t{seq, bytes, kind, peer, static_cast<uint32_t>(nbatches(c, bytes)), nullptr, nullptr, nullptr};
   cudaEventCreate(&t.e0);
   cudaEventCreate(&t.e1);
   cudaEventCreate(&t.e2);
@@ -764,13 +799,13 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
   if (tl) cudaEventRecord(tl->e0, c->stream);
   uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
   auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
-  if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, dst, kStageStride, ZC_STAGE_BANK_BYTES, pin, &c->cfg.hint,
-                                   c->shared, &c->cfg.arb, res, reinterpret_cast<uint32_t*>(dst + y.reg_idx),
-                                   c->err_word(), c->stream))
+  if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, y.ub, dst, y.fstride, ZC_STAGE_BANK_BYTES, pin,
+                                   &c->cfg.hint, c->shared, &c->cfg.arb, res,
+                                   reinterpret_cast<uint32_t*>(dst + y.reg_idx), c->err_word(), c->stream))
     return rc;
   post_signal(reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg, seq + 1);
   note_launch();
-  piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(bytes)), bytes,
+  piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(c, bytes)), bytes, y.ub,
                                              reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire),
                                              reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg,
                                              seq + 1, log);
@@ -792,7 +827,7 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
     return rc;
   if (tl) cudaEventRecord(tl->e1, c->stream);
   const uint8_t* region = c->block + y.off_reg + reg * y.reg_stride;
-  if (int rc = zc_i_decode_batches(region, kStageStride, ZC_STAGE_BANK_BYTES,
+  if (int rc = zc_i_decode_batches(region, y.ub, y.fstride, ZC_STAGE_BANK_BYTES,
                                    reinterpret_cast<const zc_encode_result*>(region + y.reg_res), bytes, c->shared,
                                    reinterpret_cast<const uint32_t*>(region + y.reg_idx), store ? OUT_BYTES : OUT_ADD_I32,
                                    dst, 1.0, nullptr, c->err_word(), c->stream, own ? 1 : 0))
@@ -806,7 +841,7 @@ int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
 // sends to this rank, in pieces; sends run one piece ahead of receives.
 int staged_xfer(zc_comm* c, int to, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin,
                 bool store) {
-  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * ZC_BATCH_RAW_BYTES;
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
   const uint64_t ns = (tx_bytes + pb - 1) / pb, nr = (rx_bytes + pb - 1) / pb;
   const uint64_t steps = std::max(ns, nr) + 1;
   for (uint64_t k = 0; k < steps; ++k) {
@@ -822,7 +857,73 @@ int staged_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, u
   return staged_xfer(c, (c->rank + 1) % c->nranks, tx, tx_bytes, rx, rx_bytes, pin, store);
 }
 
-bool use_staged() { return std::getenv("ZC_RING_KERNEL") == nullptr; }
+// The single-kernel step (ZC_RING_KERNEL=1) stages 4 MiB batches only.
+// ---- point-to-point (RankCtx::send_encoded / recv_decoded, collectives.cpp:350-364): the message
+// in pieces of kP2PUnits batches, each encoded (send_batch per batch, cfg.pin) straight into the
+// pair's region in the receiver's block and published like a ring piece; the receiver decodes it
+// (recv_batch) and returns the region.  A send runs kP2PRegions pieces ahead of its receiver,
+// the analogue of the reference's per-connection credit window.
+int p2p_send(zc_comm* c, int to, const uint8_t* src, uint64_t bytes) {
+  const Layout& y = c->lay;
+  const uint64_t pb = static_cast<uint64_t>(kP2PUnits) * y.ub;
+  for (uint64_t off = 0; off < bytes; off += pb) {
+    const uint64_t len = std::min(pb, bytes - off);
+    const uint64_t k = c->p2p_tx[to]++;
+    const uint32_t reg = static_cast<uint32_t>(k % kP2PRegions);
+    if (k >= kP2PRegions)  // the receiver has consumed the piece that last used this region
+      if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_pcons) + to,
+                               k - kP2PRegions + 1))
+        return rc;
+    uint8_t* dst = c->peer[to] + y.off_p2p + (static_cast<uint64_t>(c->rank) * kP2PRegions + reg) * y.p2p_stride;
+    auto* res = reinterpret_cast<zc_encode_result*>(dst + y.p2p_res);
+    if (int rc = zc_i_encode_batches(src + off, SRC_BYTES, len, 1.0, y.ub, dst, y.fstride, ZC_STAGE_BANK_BYTES,
+                                     c->cfg.pin, &c->cfg.hint, c->shared, &c->cfg.arb, res,
+                                     reinterpret_cast<uint32_t*>(dst + y.p2p_idx), c->err_word(), c->stream))
+      return rc;
+    auto* ready = reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_pready) +
+                  static_cast<uint64_t>(c->rank) * kP2PRegions + reg;
+    post_signal(ready, k + 1);
+    note_launch();
+    piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(c, len)), len, y.ub,
+                                               reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire), ready, k + 1,
+                                               nullptr);
+    if (int rc = cuda_err(cudaGetLastError(), "p2p send")) return rc;
+  }
+  return ZC_OK;
+}
+
+int p2p_recv(zc_comm* c, int from, uint8_t* dst, uint64_t bytes) {
+  const Layout& y = c->lay;
+  const uint64_t pb = static_cast<uint64_t>(kP2PUnits) * y.ub;
+  const int pin = c->cfg.pin;
+  const bool own = pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN || (c->shared == nullptr && !c->cfg.arb.embed_codebook);
+  for (uint64_t off = 0; off < bytes; off += pb) {
+    const uint64_t len = std::min(pb, bytes - off);
+    const uint64_t k = c->p2p_rx[from]++;
+    const uint32_t reg = static_cast<uint32_t>(k % kP2PRegions);
+    const uint64_t slot = static_cast<uint64_t>(from) * kP2PRegions + reg;
+    if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_pready) + slot, k + 1))
+      return rc;
+    const uint8_t* region = c->block + y.off_p2p + slot * y.p2p_stride;
+    if (int rc = zc_i_decode_batches(region, y.ub, y.fstride, ZC_STAGE_BANK_BYTES,
+                                     reinterpret_cast<const zc_encode_result*>(region + y.p2p_res), len, c->shared,
+                                     reinterpret_cast<const uint32_t*>(region + y.p2p_idx), OUT_BYTES, dst + off, 1.0,
+                                     nullptr, c->err_word(), c->stream, own ? 1 : 0))
+      return rc;
+    auto* cons = reinterpret_cast<unsigned long long*>(c->peer[from] + y.off_pcons) + c->rank;
+    if (c->memops) {
+      if (int rc = stream_write(c, cons, k + 1)) return rc;
+    } else {
+      post_signal(cons, k + 1);
+      note_launch();
+      flag_store_kernel<<<1, 1, 0, c->stream>>>(cons, k + 1);
+      if (int rc = cuda_err(cudaGetLastError(), "p2p credit")) return rc;
+    }
+  }
+  return ZC_OK;
+}
+
+bool use_staged(const zc_comm* c) { return c->cfg.per_slot_framing || std::getenv("ZC_RING_KERNEL") == nullptr; }
 
 // Reduce-scatter then (optionally) all-gather over the ring (collectives.cpp:460-502).  RS frames
 // use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.  An AG step re-encodes the
@@ -843,7 +944,7 @@ int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
   for (int t = 0; t < n - 1; ++t) {
     chunk(r - t, &sb, &sby);
     chunk(r - t - 1, &rb, &rby);
-    if (use_staged()) {
+    if (use_staged(c)) {
       if (int rc = staged_step(c, sb, sby, rb, rby, fused_pin, false)) return rc;
     } else if (int rc = exchange_step(c, sb, sby, rb, rby, fused_pin, false, "rs-step")) {
       return rc;
@@ -853,7 +954,7 @@ int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
   for (int t = 0; t < n - 1; ++t) {
     chunk(r + 1 - t, &sb, &sby);
     chunk(r - t, &rb, &rby);
-    if (use_staged()) {
+    if (use_staged(c)) {
       if (int rc = staged_step(c, sb, sby, rb, rby, c->cfg.pin, true)) return rc;
     } else if (int rc = exchange_step(c, sb, sby, rb, rby, c->cfg.pin, true, "ag-step")) {
       return rc;
@@ -871,7 +972,7 @@ int enqueue_allgather(zc_comm* c, int32_t* d_all, uint64_t block) {
     const int si = ((r - t) % n + n) % n, ri = ((r - t - 1) % n + n) % n;
     int32_t* sb = d_all + static_cast<uint64_t>(si) * block;
     int32_t* rb = d_all + static_cast<uint64_t>(ri) * block;
-    if (use_staged()) {
+    if (use_staged(c)) {
       if (int rc = staged_step(c, sb, by, rb, by, c->cfg.pin, true)) return rc;
     } else if (int rc = exchange_step(c, sb, by, rb, by, c->cfg.pin, true, "ag-step")) {
       return rc;
@@ -927,7 +1028,7 @@ int enqueue_broadcast(zc_comm* c, int32_t* d_data, uint64_t count, int root) {
   const int pin = c->cfg.pin;
   if (pos == 0) return staged_xfer(c, next, d_data, by, nullptr, 0, pin, true);
   if (pos == n - 1) return staged_xfer(c, next, nullptr, 0, d_data, by, pin, true);
-  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * ZC_BATCH_RAW_BYTES;
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
   for (uint64_t off = 0; off < by; off += pb) {
     const uint64_t len = std::min(pb, by - off);
     if (int rc = recv_piece(c, d_data + off / 4, len, true, pin)) return rc;
@@ -1090,6 +1191,13 @@ int drain(zc_comm* c) {
       last = now();
       continue;
     }
+    // a peer poisoned the link (its abort or its own timeout): no need to wait out our timeout
+    uint32_t pe = 0;
+    cudaMemcpy(&pe, c->err_word(), 4, cudaMemcpyDeviceToHost);
+    if ((pe & (ZC_DERR_ABORT | ZC_DERR_TIMEOUT)) && now() - last > 50ull * 1000 * 1000) {
+      release_rank(c, 0);
+      return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+    }
     if (now() - last < c->timeout_ns) continue;
     for (int r = 0; r < c->nranks; ++r) {  // poison every rank (link poisoning), release our waits
       uint32_t e = 0;
@@ -1125,8 +1233,12 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
   const char* to = std::getenv("ZC_COMM_TIMEOUT_MS");
   if (to) c->timeout_ns = static_cast<unsigned long long>(std::atoll(to)) * 1000000ull;
   const char* ru = std::getenv("ZC_COMM_REGION_UNITS");
-  const uint32_t runits = ru ? static_cast<uint32_t>(std::max(1, std::min(256, std::atoi(ru)))) : 16u;
-  c->lay = make_layout(nbanks, runits);
+  // a piece region holds 64 MiB of 4 MiB batches, or 16 MiB of 512 KiB slots (per-slot framing)
+  const bool per_slot = c->cfg.per_slot_framing != 0;
+  const uint32_t runits = ru ? static_cast<uint32_t>(std::max(1, std::min(256, std::atoi(ru)))) : (per_slot ? 32u : 16u);
+  c->lay = make_layout(nbanks, runits, per_slot, static_cast<uint32_t>(nranks));
+  c->p2p_tx.assign(nranks, 0);
+  c->p2p_rx.assign(nranks, 0);
   int rc = cuda_err(cudaSetDevice(device), "cudaSetDevice");
   if (!rc) {
     preload_encode_kernels();
@@ -1145,6 +1257,7 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     cudaFuncGetAttributes(&fa, wait_geq_kernel);
     cudaFuncGetAttributes(&fa, piece_sent_kernel);
     cudaFuncGetAttributes(&fa, piece_done_kernel);
+    cudaFuncGetAttributes(&fa, flag_store_kernel);
     cudaGetLastError();
   }
   if (!rc) rc = cuda_err(cudaMalloc(&c->block, c->lay.total), "cudaMalloc block");
@@ -1246,6 +1359,8 @@ int reset_state(zc_comm* c) {
   forget_signals(c->block + y.off_ready, c->block + y.off_wire);
   c->tx_seq = c->rx_seq = 0;
   c->ptx = c->prx = 0;
+  std::fill(c->p2p_tx.begin(), c->p2p_tx.end(), 0);
+  std::fill(c->p2p_rx.begin(), c->p2p_rx.end(), 0);
   c->epoch = 0;
   return rc;
 }
@@ -1528,9 +1643,9 @@ int zc_comm_timeline_rows(zc_comm* c, zc_timeline_row* rows, int32_t cap, int32_
       r.batch = u;
       if (t.kind == 0) {
         const zc_encode_result& e = log[i * c->lay.runits + u];
-        const uint64_t off = static_cast<uint64_t>(u) * ZC_BATCH_RAW_BYTES;
+        const uint64_t off = static_cast<uint64_t>(u) * c->lay.ub;
         r.codec = e.codec;
-        r.raw_bytes = std::min<uint64_t>(ZC_BATCH_RAW_BYTES, t.bytes - off);
+        r.raw_bytes = std::min<uint64_t>(c->lay.ub, t.bytes - off);
         r.total_bytes = e.total_bytes;
         r.start_sec = a;
         r.ready_sec = a;
@@ -1564,6 +1679,41 @@ int zc_comm_sync(zc_comm* c) {
 }
 
 int zc_comm_reset(zc_comm* c) { return reset_state(c); }
+
+int zc_comm_send_encoded(zc_comm* c, int32_t peer, const void* d_raw, uint64_t raw_bytes, void* stream) {
+  if (peer < 0 || peer >= c->nranks || peer == c->rank) return set_err(ZC_ERR_INVALID_ARGUMENT, "send_encoded: bad peer");
+  if (raw_bytes == 0) return ZC_OK;  // zero-length batches never reach the receiver (collectives.cpp:202)
+  if (int rc = dev_guard(c)) return rc;
+  if (!c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = order_after(c, stream)) return rc;
+  if (int rc = p2p_send(c, peer, static_cast<const uint8_t*>(d_raw), raw_bytes)) return rc;
+  return finish(c);
+}
+
+int zc_comm_recv_decoded(zc_comm* c, int32_t peer, void* d_dst, uint64_t dst_bytes, void* stream) {
+  if (peer < 0 || peer >= c->nranks || peer == c->rank) return set_err(ZC_ERR_INVALID_ARGUMENT, "recv_decoded: bad peer");
+  if (dst_bytes == 0) return ZC_OK;
+  if (int rc = dev_guard(c)) return rc;
+  if (!c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
+  if (int rc = order_after(c, stream)) return rc;
+  if (int rc = p2p_recv(c, peer, static_cast<uint8_t*>(d_dst), dst_bytes)) return rc;
+  return finish(c);
+}
+
+// Link poisoning from the host (Communicator::run when a rank's body throws, transport.cpp:90-95):
+// every rank's error word gets ZC_DERR_ABORT, and this rank's pending waits are released.
+int zc_comm_abort(zc_comm* c) {
+  if (int rc = dev_guard(c)) return rc;
+  for (int r = 0; r < c->nranks; ++r) {
+    if (c->peer[r] == nullptr) continue;
+    uint32_t e = 0;
+    cudaMemcpy(&e, c->peer[r] + c->lay.off_err, 4, cudaMemcpyDeviceToHost);
+    e |= ZC_DERR_ABORT;
+    cudaMemcpy(c->peer[r] + c->lay.off_err, &e, 4, cudaMemcpyHostToDevice);
+  }
+  release_rank(c, ZC_DERR_ABORT);
+  return cuda_err(cudaGetLastError(), "abort");
+}
 
 // Diagnostics: ready[nb], len[nb], credit[nb], err, mailbox flags[nranks], tx_seq, rx_seq, epoch.
 int zc_comm_debug_state(zc_comm* c, uint64_t* out, int cap) {

@@ -33,7 +33,12 @@ constexpr int ET = ET_WARPS * 32;
 constexpr int STAGES = 3;                // tiles in flight per warp
 constexpr uint32_t TILE_ELEMS = 1024;    // 32 x 32 fp32
 constexpr uint32_t TILE_BYTES = TILE_ELEMS * 4;
-constexpr uint32_t UNIT_TILES = ZC_BATCH_RAW_BYTES / TILE_BYTES;  // 1024
+// A unit (batch) is 2^ush tiles: 1024 for 4 MiB batches, 128 for 512 KiB slots (per-slot framing).
+__host__ __device__ __forceinline__ uint32_t unit_tile_shift(uint64_t unit_bytes) {
+  uint32_t s = 0;
+  while ((static_cast<uint64_t>(TILE_BYTES) << s) < unit_bytes) ++s;
+  return s;
+}
 constexpr size_t EMIT_SMEM = static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES + 1024 + ET_WARPS * STAGES * 8;
 
 __device__ __forceinline__ float fmin_nan(float a, float b) {
@@ -418,17 +423,8 @@ __device__ __forceinline__ void store_row(uint32_t codec, uint32_t width, const 
   }
 }
 
-// Warp tile order: warp gw owns chunks gw, gw + tw, ... of CHUNK consecutive tiles (chunks never
-// straddle a unit), so consecutive tiles of a warp share the unit's state and payload rows.
+// Grid sizing: a warp's contiguous share of the tiles is at least about CHUNK tiles.
 constexpr uint64_t CHUNK = 4;
-__device__ __forceinline__ uint64_t tile_adv(uint64_t c, uint64_t tw) {
-  return ((c + 1) % CHUNK) != 0 ? c + 1 : c + 1 + (tw - 1) * CHUNK;
-}
-// The warp's first tile at or past tile `ue` (a unit boundary), given its current tile c.
-__device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64_t tw) {
-  const uint64_t j = c / CHUNK, je = ue / CHUNK;
-  return (j + ((je - j + tw - 1) / tw) * tw) * CHUNK;
-}
 
 constexpr uint32_t kForeign = 0xFEu;  // unit owned by the general kernels
 
@@ -485,9 +481,10 @@ __device__ __noinline__ void spec_flush(const EncParams& p, BUnit* us, uint32_t 
   BUnit& U = us[u];
   atomicMax(&U.maxzz, mz);
   const uint32_t ntu = static_cast<uint32_t>((unit_R(p, u) / 4 + TILE_ELEMS - 1) / TILE_ELEMS);
-  uint32_t old;  // release: this warp's range is in before its tiles count; acquire: the decider sees all
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&U.tdone), "r"(ntiles) : "memory");
+  uint32_t old;  // release: this warp's range is in before its tiles count
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&U.tdone), "r"(ntiles) : "memory");
   if (old + ntiles != ntu) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the decider (last arriver) sees every warp's range
   uint32_t e = 0;
   decide_unit<SRC>(p, U, u, true, false, e);  // from the symbols' max zig-zag (U.maxzz)
   *err |= e;
@@ -529,32 +526,37 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   __syncwarp();
 
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * ET_WARPS + warp, tw = static_cast<uint64_t>(gridDim.x) * ET_WARPS;
-  // The warp's tile sequence: tiles gw, gw+tw, ... of owned units, full tiles only.
+  const uint32_t ush = unit_tile_shift(p.unit_bytes);
+  const uint64_t umask = (1ull << ush) - 1;
+  // The warp's tile sequence: its contiguous share [t_beg, t_end) of the full tiles, owned units
+  // only — a warp crosses at most a couple of unit boundaries, so the per-unit view (global loads
+  // of the unit's plan / decision) and the speculative range flush happen a few times per warp.
+  const uint64_t t_beg = nfull * gw / tw, t_end = nfull * (gw + 1) / tw;
   uint32_t iss_u = 0xffffffffu;
   bool iss_owned = false;
   auto next_tile = [&](uint64_t c) -> uint64_t {
-    while (c < nfull) {
-      const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    while (c < t_end) {
+      const uint32_t u = static_cast<uint32_t>(c >> ush);
       if (u != iss_u) {
         iss_u = u;
         iss_owned = owned(unit_view_m<kMode>(p, us, u, ctx_ok).codec);
       }
       if (iss_owned) return c;
-      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
+      c = static_cast<uint64_t>(u + 1) << ush;
     }
-    return nfull;
+    return t_end;
   };
-  uint64_t c_issue = next_tile(gw * CHUNK);
+  uint64_t c_issue = next_tile(t_beg);
   if (lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      if (c_issue < nfull) {
+      if (c_issue < t_end) {
         tma::mbar_arrive_expect_tx(&bars[i], TILE_BYTES);
         tma::load_2d(my + i * TILE_BYTES, &tmap, &bars[i], 0, static_cast<int32_t>(c_issue * 32));
       }
-      c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
+      c_issue = c_issue < t_end ? next_tile(c_issue + 1) : t_end;
     }
   } else {
-    for (int i = 0; i < STAGES; ++i) c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
+    for (int i = 0; i < STAGES; ++i) c_issue = c_issue < t_end ? next_tile(c_issue + 1) : t_end;
   }
   uint32_t k = 0, cur_u = 0xffffffffu;
   UnitView v;
@@ -564,7 +566,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   uint64_t c_first = gw;
   {  // the processing sequence restarts from the first tile (its own unit cache)
     iss_u = 0xffffffffu;
-    c_first = next_tile(gw * CHUNK);
+    c_first = next_tile(t_beg);
     iss_u = 0xffffffffu;
   }
   uint32_t sp_mz = 0, sp_u = 0xffffffffu, sp_n = 0;
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     sp_mz = 0;
     sp_n = 0;
   };
-  for (uint64_t c = c_first; c < nfull; c = next_tile(tile_adv(c, tw)), ++k) {
+  for (uint64_t c = c_first; c < t_end; c = next_tile(c + 1), ++k) {
     const uint32_t st = k % STAGES;
     tma::mbar_wait(&bars[st], (k / STAGES) & 1u);
     const uint8_t* tile = my + st * TILE_BYTES;
@@ -586,13 +588,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
                    : "=f"(x[4 * m]), "=f"(x[4 * m + 1]), "=f"(x[4 * m + 2]), "=f"(x[4 * m + 3])
                    : "r"(row + ((m ^ (lane & 7)) << 4)));
     }
-    __syncwarp();
-    if (lane == 0 && c_issue < nfull) {  // refill this stage
-      tma::mbar_arrive_expect_tx(&bars[st], TILE_BYTES);
-      tma::load_2d(my + st * TILE_BYTES, &tmap, &bars[st], 0, static_cast<int32_t>(c_issue * 32));
-    }
-    c_issue = c_issue < nfull ? next_tile(tile_adv(c_issue, tw)) : nfull;
-    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    const uint32_t u = static_cast<uint32_t>(c >> ush);
     if (u != cur_u) {
       cur_u = u;
       v = unit_view_m<kMode>(p, us, u, ctx_ok);
@@ -612,19 +608,28 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       sp_u = u;
       ++sp_n;
     }
-    store_row(v.codec, v.width, s, payload, (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
+    store_row(v.codec, v.width, s, payload, (c & umask) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
+    // Refill this stage only now: the row's values have been consumed (stored), so every lane's
+    // shared-memory reads of the tile have completed before the async proxy overwrites it (a
+    // refill right after the loads raced them when the row work is short, e.g. RAW symbols).
+    __syncwarp();
+    if (lane == 0 && c_issue < t_end) {
+      tma::mbar_arrive_expect_tx(&bars[st], TILE_BYTES);
+      tma::load_2d(my + st * TILE_BYTES, &tmap, &bars[st], 0, static_cast<int32_t>(c_issue * 32));
+    }
+    c_issue = c_issue < t_end ? next_tile(c_issue + 1) : t_end;
   }
 
   if (kMode == 1 && sp_n) spec_run_flush();
   // the message's last, partial tile (direct guarded loads / byte-exact tail stores)
-  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
+  if (nfull < ntiles && gw == tw - 1) {
     const uint64_t c = nfull;
-    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    const uint32_t u = static_cast<uint32_t>(c >> ush);
     v = unit_view_m<kMode>(p, us, u, ctx_ok);
     if (owned(v.codec)) {
       const uint64_t R = unit_R(p, u);
       const uint64_t n = R / 4;  // symbols of the unit
-      const uint64_t e0 = (c % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
+      const uint64_t e0 = (c & umask) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
       const float* src = static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4);
       uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
       uint32_t s[32];
@@ -771,21 +776,21 @@ __device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t 
   }
 }
 
-struct DecSeq {  // a warp's tile sequence over owned units, with the view of the current unit
-  uint64_t nfull, tw;
-  uint32_t cu;
+struct DecSeq {  // a warp's contiguous tile range over owned units, with the current unit's view
+  uint64_t end;
+  uint32_t ush, cu;
   DecView cv;
   __device__ __forceinline__ uint64_t next(const DecParams& p, uint64_t c) {
-    while (c < nfull) {
-      const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    while (c < end) {
+      const uint32_t u = static_cast<uint32_t>(c >> ush);
       if (u != cu) {
         cu = u;
         cv = dec_view(p, u);
       }
       if (cv.codec != kFallback) return c;
-      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) * UNIT_TILES, tw);
+      c = static_cast<uint64_t>(u + 1) << ush;
     }
-    return nfull;
+    return end;
   }
 };
 
@@ -812,33 +817,36 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   __syncwarp();
   const uint64_t tw = static_cast<uint64_t>(gridDim.x) * DT_WARPS;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * DT_WARPS + warp;
-  DecSeq iss{nfull, tw, 0xffffffffu, {kFallback, 0}}, prc{nfull, tw, 0xffffffffu, {kFallback, 0}};
+  const uint32_t ush = unit_tile_shift(p.unit_bytes);
+  const uint64_t umask = (1ull << ush) - 1;
+  const uint64_t t_beg = nfull * gw / tw, t_end = nfull * (gw + 1) / tw;
+  DecSeq iss{t_end, ush, 0xffffffffu, {kFallback, 0}}, prc{t_end, ush, 0xffffffffu, {kFallback, 0}};
   auto issue = [&](uint32_t st, uint64_t c) {  // lane 0: the packed rows of tile c into stage st
-    const uint32_t u = static_cast<uint32_t>(c / UNIT_TILES);
+    const uint32_t u = static_cast<uint32_t>(c >> ush);
     const uint32_t bytes = 128u * iss.cv.width;
-    const uint8_t* src = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes + (c % UNIT_TILES) * bytes;
+    const uint8_t* src = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes + (c & umask) * bytes;
     tma::mbar_arrive_expect_tx(&bars[st], bytes);
     tma::load_1d(my + st * TILE_BYTES, src, bytes, &bars[st]);
   };
-  uint64_t c_issue = iss.next(p, gw * CHUNK);
+  uint64_t c_issue = iss.next(p, t_beg);
   for (int i = 0; i < DSTAGES - 1; ++i) {
-    if (c_issue < nfull) {
+    if (c_issue < t_end) {
       if (lane == 0) issue(i, c_issue);
-      c_issue = iss.next(p, tile_adv(c_issue, tw));
+      c_issue = iss.next(p, c_issue + 1);
     }
   }
   uint32_t k = 0;
-  for (uint64_t c = prc.next(p, gw * CHUNK); c < nfull; c = prc.next(p, tile_adv(c, tw)), ++k) {
+  for (uint64_t c = prc.next(p, t_beg); c < t_end; c = prc.next(p, c + 1), ++k) {
     const uint32_t st = k % DSTAGES;
     // refill the stage that tile k-1 used once its store has read the buffer (the ring keeps
     // DSTAGES-1 loads in flight while this tile is decoded)
-    if (c_issue < nfull) {
+    if (c_issue < t_end) {
       const uint32_t rs = (k + DSTAGES - 1) % DSTAGES;
       if (lane == 0) {
         tma::bulk_wait_read<0>();
         issue(rs, c_issue);
       }
-      c_issue = iss.next(p, tile_adv(c_issue, tw));
+      c_issue = iss.next(p, c_issue + 1);
     }
     tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
     const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
@@ -852,8 +860,8 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     }
   }
   // the message's last, partial tile: symbol by symbol with byte-exact bounds
-  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
-    const uint32_t u = static_cast<uint32_t>(nfull / UNIT_TILES);
+  if (nfull < ntiles && gw == tw - 1) {
+    const uint32_t u = static_cast<uint32_t>(nfull >> ush);
     const DecView v = dec_view(p, u);
     if (v.codec != kFallback) {
       const uint64_t off = static_cast<uint64_t>(u) * p.unit_bytes;
@@ -861,7 +869,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
       const uint8_t* payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
       const uint64_t P = v.codec == ZC_CODEC_RAW ? 4 * n : packed_bytes(n, v.width);
       float* out = static_cast<float*>(p.out) + off / 4;
-      const uint64_t e0 = (nfull % UNIT_TILES) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
+      const uint64_t e0 = (nfull & umask) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
       for (uint64_t e = e0; e < e0 + 32 && e < n; ++e) {
         int32_t sym;
         if (v.codec == ZC_CODEC_RAW) {
@@ -917,9 +925,14 @@ bool make_row_tensor_map(CUtensorMap* map, const void* base, uint64_t rows) {  /
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Units of 2^k whole tiles, up to one bank: 4 MiB batches and 512 KiB slots.
+static bool tiled_unit(uint64_t ub) {
+  return ub >= TILE_BYTES && ub <= ZC_BATCH_RAW_BYTES && (ub & (ub - 1)) == 0;
+}
+
 bool fixed_path_ok(const EncParams& p) {
   const bool src_ok = p.src_kind == SRC_F32 || (p.src_kind == SRC_BYTES && p.total_bytes % 4 == 0);
-  return src_ok && (reinterpret_cast<uintptr_t>(p.src) & 15u) == 0 && p.unit_bytes == ZC_BATCH_RAW_BYTES &&
+  return src_ok && (reinterpret_cast<uintptr_t>(p.src) & 15u) == 0 && tiled_unit(p.unit_bytes) &&
          p.mode == ENC_SEND && !p.link_tx && !p.link_rx_add && !p.cfg.embed_codebook;
 }
 
@@ -959,8 +972,9 @@ cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t tota
   const uint64_t rows = count / 32;
   // tiles of the message (the last unit's may be partial) and the full ones before it
   const uint64_t last_n = (p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes) / 4;
-  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
-  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + last_n / TILE_ELEMS;
+  const uint64_t unit_tiles = p.unit_bytes / TILE_BYTES;
+  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * unit_tiles + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
+  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * unit_tiles + last_n / TILE_ELEMS;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (rows > 0 && !make_row_tensor_map(&map, p.src, rows)) return cudaErrorInvalidValue;
@@ -992,7 +1006,7 @@ cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_
 
 bool fixed_decode_ok(const DecParams& p) {
   return !p.bare && (p.out_kind == OUT_F32 || p.out_kind == OUT_ADD_I32 || p.out_kind == OUT_BYTES) &&
-         p.unit_bytes == ZC_BATCH_RAW_BYTES && (p.total_bytes % 4) == 0 &&
+         tiled_unit(p.unit_bytes) && (p.total_bytes % 4) == 0 &&
          (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0 && (p.stride % 16) == 0 &&
          (reinterpret_cast<uintptr_t>(p.stages) & 15u) == 0;
 }
@@ -1010,8 +1024,9 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
   const uint64_t count = p.total_bytes / 4;
   const uint64_t rows = count / 32;
   const uint64_t last_n = (p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes) / 4;
-  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
-  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * UNIT_TILES + last_n / TILE_ELEMS;
+  const uint64_t unit_tiles = p.unit_bytes / TILE_BYTES;
+  const uint64_t ntiles = static_cast<uint64_t>(p.nunits - 1) * unit_tiles + (last_n + TILE_ELEMS - 1) / TILE_ELEMS;
+  const uint64_t nfull = static_cast<uint64_t>(p.nunits - 1) * unit_tiles + last_n / TILE_ELEMS;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (rows > 0 && !make_row_tensor_map(&map, p.out, rows)) return cudaErrorInvalidValue;

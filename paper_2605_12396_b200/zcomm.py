@@ -70,6 +70,11 @@ def lib():
     _sig(L, "zc_version", C.c_char_p)
     _sig(L, "zc_launch_count", C.c_uint64)
     _sig(L, "zc_device_count", C.c_int, P(C.c_int))
+    _sig(L, "zc_device_malloc", C.c_int, u64, P(vp))
+    _sig(L, "zc_device_free", None, vp)
+    _sig(L, "zc_memcpy", C.c_int, vp, vp, u64)
+    _sig(L, "zc_memset", C.c_int, vp, C.c_int, u64)
+    _sig(L, "zc_stream_synchronize", C.c_int, vp)
     _sig(L, "zc_default_arb_config", None, P(abi.ArbConfig))
     _sig(L, "zc_default_transport_hint", None, P(abi.TransportHint))
     _sig(L, "zc_default_collective_config", None, P(abi.CollectiveConfig))
@@ -135,6 +140,9 @@ def lib():
     _sig(L, "zc_comm_allreduce_max", C.c_int, vp, dbl, P(dbl), vp)
     _sig(L, "zc_comm_sync", C.c_int, vp)
     _sig(L, "zc_comm_reset", C.c_int, vp)
+    _sig(L, "zc_comm_send_encoded", C.c_int, vp, i32, vp, u64, vp)
+    _sig(L, "zc_comm_recv_decoded", C.c_int, vp, i32, vp, u64, vp)
+    _sig(L, "zc_comm_abort", C.c_int, vp)
     _sig(L, "zc_comm_wire_stats", C.c_int, vp, P(abi.WireStats))
     _sig(L, "zc_comm_reset_stats", C.c_int, vp)
     _sig(L, "zc_group_allreduce_sym", C.c_int, P(vp), C.c_int, P(vp), u64, i32, P(dbl), u32)
@@ -635,6 +643,36 @@ class Group:
         for r in range(self.nranks):
             check(lib().zc_comm_set_shared_huffman(self._h[r], ctx.handle))
 
+    def run(self, fn):
+        """Communicator::run (collectives.cpp:137-173): fn(RankCtx) on one thread per rank.  A rank
+        whose body raises poisons every link (zc_comm_abort; peers blocked on it fail with
+        LinkPoisoned), the communicator is reset, and the root cause is re-raised.  Returns the
+        per-rank results."""
+        import threading
+        n = self.nranks
+        res, errs = [None] * n, [None] * n
+
+        def body(r):
+            torch.cuda.set_device(self.devices[r])
+            try:
+                res[r] = fn(RankCtx(self, r))
+            except BaseException as e:  # noqa: BLE001 - every rank's failure is collected
+                errs[r] = e
+                lib().zc_comm_abort(self._h[r])
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(n)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        failed = [e for e in errs if e is not None]
+        if failed:
+            for r in range(n):
+                lib().zc_comm_reset(self._h[r])
+            root = next((e for e in failed if not isinstance(e, LinkPoisoned)), failed[0])
+            raise root
+        return res
+
     def set_shared_huffman_from_bytes(self, sample) -> None:
         self.set_shared_huffman(HuffmanContext.from_bytes(sample))
 
@@ -775,6 +813,49 @@ class Group:
         self.close()
 
 
+class RankCtx:
+    """The per-rank face of a single-process Group inside Group.run (collectives.hpp:48-110): the
+    rank's collectives and point-to-point calls, each on the rank's own communicator (the calls of
+    different ranks run concurrently on their own threads, like the reference's rank threads)."""
+
+    def __init__(self, group: "Group", rank: int):
+        self._g, self._h, self._rank = group, group._h[rank], rank
+
+    def rank(self) -> int:
+        return self._rank
+
+    def nranks(self) -> int:
+        return self._g.nranks
+
+    def send_encoded(self, peer: int, raw: torch.Tensor):
+        check(lib().zc_comm_send_encoded(self._h, peer, _ptr(raw), raw.numel() * raw.element_size(), None))
+
+    def recv_decoded(self, peer: int, dst: torch.Tensor):
+        check(lib().zc_comm_recv_decoded(self._h, peer, _ptr(dst), dst.numel() * dst.element_size(), None))
+
+    def allreduce(self, sym: torch.Tensor, scale: float, mode: int = abi.QUANT_ERROR_BOUNDED, levels: int = 0) -> float:
+        s = C.c_double(scale)
+        check(lib().zc_comm_allreduce_sym(self._h, _ptr(sym), sym.numel(), mode, C.byref(s), levels, None))
+        return s.value
+
+    def allreduce_eb(self, x: torch.Tensor, rel: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        out = out if out is not None else torch.empty(x.numel(), dtype=torch.float32, device=x.device)
+        check(lib().zc_comm_allreduce_eb_f32(self._h, _ptr(x), _ptr(out), 1 if out.dtype == torch.float64 else 0,
+                                             x.numel(), float(rel), None))
+        return out
+
+    def allgather(self, all_blocks: torch.Tensor, block: int):
+        check(lib().zc_comm_allgather_sym(self._h, _ptr(all_blocks), block, None))
+
+    def broadcast(self, data: torch.Tensor, root: int):
+        check(lib().zc_comm_broadcast_sym(self._h, _ptr(data), data.numel(), root, None))
+
+    def allreduce_max(self, v: float) -> float:
+        o = C.c_double(0.0)
+        check(lib().zc_comm_allreduce_max(self._h, float(v), C.byref(o), None))
+        return o.value
+
+
 class Communicator:
     """One rank of a multi-process communicator (one process per GPU).  The peers' IPC blobs are
     exchanged with torch.distributed (any backend; the data path never uses it)."""
@@ -834,6 +915,14 @@ class Communicator:
 
     def broadcast(self, data: torch.Tensor, root: int):
         check(lib().zc_comm_broadcast_sym(self._h, _ptr(data), data.numel(), root, _stream()))
+
+    def send_encoded(self, peer: int, raw: torch.Tensor):
+        """RankCtx::send_encoded (collectives.cpp:350-356): the tensor's bytes, framed per batch."""
+        check(lib().zc_comm_send_encoded(self._h, peer, _ptr(raw), raw.numel() * raw.element_size(), _stream()))
+
+    def recv_decoded(self, peer: int, dst: torch.Tensor):
+        """RankCtx::recv_decoded (collectives.cpp:358-364): fills dst's bytes from peer's frames."""
+        check(lib().zc_comm_recv_decoded(self._h, peer, _ptr(dst), dst.numel() * dst.element_size(), _stream()))
 
     def group_execute(self, requests: Sequence[dict]):
         k = len(requests)

@@ -229,6 +229,22 @@ def main():
                 "n": n, "count": count, "pin": pin, "out_sha256": sha(s[0]), "out_head": s[0][:8].tolist(),
                 "wire": {"frames_by_codec": list(w.frames_by_codec), "raw_bytes": int(w.raw_bytes),
                          "payload_bytes": int(w.payload_bytes), "total_bytes": int(w.total_bytes)}}
+        # per-slot framing (CollectiveConfig::perSlotFraming, collectives.cpp:197-199): every
+        # exchange batches at 512 KiB, so frames, decisions and WireStats all change
+        for pin in (abi.PIN_AUTO, abi.PIN_RAW, abi.PIN_FIXEDLEN, abi.PIN_HUFFMAN):
+            s = base.copy()
+            sc = np.full(n, 2e-4)
+            w = abi.WireStats()
+            c = abi.default_collective_config(pin)
+            c.per_slot_framing = 1
+            sample = np.ascontiguousarray(base[0].view(np.uint8)[: abi.BATCH_RAW_BYTES])
+            rc = R.lib.zr_allreduce_sym(n, C.byref(c), s.ravel(), count, abi.QUANT_ERROR_BOUNDED, sc, 0,
+                                        sample.ctypes.data_as(C.POINTER(C.c_uint8)), len(sample), C.byref(w), None)
+            assert rc == 0, R.error()
+            col[f"ring{n}_{abi.PIN_NAMES[pin]}_slot"] = {
+                "n": n, "count": count, "pin": pin, "per_slot_framing": 1, "out_sha256": sha(s[0]),
+                "wire": {"frames_by_codec": list(w.frames_by_codec), "raw_bytes": int(w.raw_bytes),
+                         "payload_bytes": int(w.payload_bytes), "total_bytes": int(w.total_bytes)}}
         # allgather (collectives.cpp:525-544) of ragged-free blocks
         blk = base[:, :300_000].copy()
         out = np.zeros(n * n * 300_000, np.int32)  # every rank's gathered copy

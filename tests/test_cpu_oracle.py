@@ -169,6 +169,24 @@ def test_ring_allreduce_matches_reference(port, n, pin):
 
 
 @pytest.mark.parametrize("n", [2, 3, 4])
+@pytest.mark.parametrize("pin", ["auto", "raw", "fixedlen", "huffman"])
+def test_ring_allreduce_per_slot_matches_reference(port, n, pin):
+    """CollectiveConfig::perSlotFraming: the same ring with 512 KiB batches (collectives.cpp:197-199,
+    366-396): symbols and WireStats identical to the reference Communicator's, and the frame count
+    is the per-slot one (not the 4 MiB batches')."""
+    k = GOLDEN["collectives"][f"ring{n}_{pin}_slot"]
+    base = ring_input(n)
+    ctx = port.huff_from_bytes(np.ascontiguousarray(base[0].view(np.uint8)[: abi.BATCH_RAW_BYTES]))
+    rc, out, _, w = port.ring_allreduce(base, np.full(n, 2e-4), pin=k["pin"], ctx=ctx, per_slot=True)
+    assert rc == 0
+    assert sha(out[0]) == k["out_sha256"]
+    assert list(w.frames_by_codec) == k["wire"]["frames_by_codec"]
+    assert (w.raw_bytes, w.payload_bytes, w.total_bytes) == (k["wire"]["raw_bytes"], k["wire"]["payload_bytes"],
+                                                              k["wire"]["total_bytes"])
+    assert sum(w.frames_by_codec) > sum(GOLDEN["collectives"][f"ring{n}_{pin}"]["wire"]["frames_by_codec"])
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
 def test_ring_allgather_matches_reference(port, n):
     """RankCtx::allgather (collectives.cpp:525-544)."""
     k = GOLDEN["collectives"][f"allgather{n}"]

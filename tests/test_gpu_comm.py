@@ -295,3 +295,69 @@ def test_embedded_codebook_ring_without_shared_ctx(zc, port):
     w = _ring_check(zc, port, g, syms, abi.PIN_AUTO, None, cfg)
     assert w.frames_by_codec[abi.CODEC_HUFFMAN] > 0
     g.close()
+
+
+# ------------------------------------------------------------------ per-slot framing
+@pytest.mark.parametrize("n,count", [(2, (3 << 20) // 4 + 777), (3, (5 << 20) // 4 + 3)])
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_RAW, abi.PIN_FIXEDLEN, abi.PIN_HUFFMAN])
+def test_allreduce_per_slot_framing_vs_reference(zc, port, ref, n, count, pin):
+    """CollectiveConfig::perSlotFraming (collectives.hpp:33): every exchange batches at 512 KiB
+    (RankCtx::chunk_raw_bytes, collectives.cpp:197-199).  Symbols and WireStats equal to the
+    compiled reference Communicator's and to the oracle ring's; more frames than 4 MiB batching."""
+    import ctypes as C
+    rng = np.random.default_rng(40 + n * 5 + pin)
+    syms = [np.clip(rng.laplace(0, 40 * (r + 1), count), -2**20, 2**20).astype(np.int32) for r in range(n)]
+    sample = np.ascontiguousarray(syms[0].view(np.uint8)[: 1 << 20])
+    cfg = zc.collective_config(pin, per_slot_framing=1)
+    exp = np.stack(syms).copy()
+    sc = np.ones(n)
+    w_ref = abi.WireStats()
+    assert ref.lib.zr_allreduce_sym(n, C.byref(cfg), exp.ravel(), count, abi.QUANT_ERROR_BOUNDED, sc, 0,
+                                    sample.ctypes.data_as(C.POINTER(C.c_uint8)), len(sample), C.byref(w_ref),
+                                    None) == 0
+    o = port.huff_from_bytes(sample)
+    rc, exp_p, _, w_p = port.ring_allreduce(np.stack(syms), [1.0] * n, pin, cfg.hint, o, cfg.arb,
+                                            cfg.fused_codec_min_msg_bytes, per_slot=True)
+    assert rc == 0 and np.array_equal(exp_p, exp)
+    assert list(w_p.frames_by_codec) == list(w_ref.frames_by_codec) and w_p.payload_bytes == w_ref.payload_bytes
+    g = zc.Group(n, cfg=cfg)
+    g.set_shared_huffman(zc.HuffmanContext.from_bytes(sample))
+    ts = [t(s) for s in syms]
+    g.allreduce(ts, [1.0] * n)
+    for r in range(n):
+        assert np.array_equal(npy(ts[r]), exp[r])
+    w = g.wire_stats()
+    assert list(w.frames_by_codec) == list(w_ref.frames_by_codec)
+    assert (w.raw_bytes, w.payload_bytes, w.total_bytes) == (w_ref.raw_bytes, w_ref.payload_bytes, w_ref.total_bytes)
+    g4 = zc.Group(n, cfg=zc.collective_config(pin))  # 4 MiB batches: fewer frames on the same data
+    g4.set_shared_huffman(zc.HuffmanContext.from_bytes(sample))
+    g4.allreduce([t(s) for s in syms], [1.0] * n)
+    assert sum(g4.wire_stats().frames_by_codec) < sum(w.frames_by_codec)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_allgather_and_broadcast_per_slot_framing(zc, port, ref, n):
+    """allgather under per-slot framing: outputs exact, WireStats equal to the compiled reference's
+    (collectives.cpp:525-544); broadcast's store-and-forward at slot granularity (:569-591) exact."""
+    import ctypes as C
+    block = (3 << 20) // 4 + 11
+    rng = np.random.default_rng(n + 900)
+    blocks = [rng.integers(-3000, 3000, block).astype(np.int32) for _ in range(n)]
+    cfg = zc.collective_config(abi.PIN_AUTO, per_slot_framing=1)
+    out = np.zeros(n * n * block, np.int32)
+    w_ref = abi.WireStats()
+    assert ref.lib.zr_allgather_sym(n, C.byref(cfg), np.stack(blocks).ravel(), block, None, 0, out,
+                                    C.byref(w_ref)) == 0
+    g = zc.Group(n, cfg=cfg)
+    outs = g.allgather([t(b) for b in blocks])
+    full = np.concatenate(blocks)
+    for o in outs:
+        assert np.array_equal(npy(o), full)
+    w = g.wire_stats()
+    assert list(w.frames_by_codec) == list(w_ref.frames_by_codec)
+    assert (w.raw_bytes, w.payload_bytes, w.total_bytes) == (w_ref.raw_bytes, w_ref.payload_bytes, w_ref.total_bytes)
+    data = rng.integers(-2**20, 2**20, (5 << 20) // 4 + 9).astype(np.int32)
+    ds = [t(data) if r == 1 else torch.zeros(len(data), dtype=torch.int32, device=DEV) for r in range(n)]
+    g.broadcast(ds, 1)
+    for d in ds:
+        assert np.array_equal(npy(d), data)
