@@ -425,6 +425,16 @@ __device__ __forceinline__ void store_row(uint32_t codec, uint32_t width, const 
 
 // Grid sizing: a warp's contiguous share of the tiles is at least about CHUNK tiles.
 constexpr uint64_t CHUNK = 4;
+// The decoder's warp tile order: warp gw owns chunks gw, gw + tw, ... of CHUNK consecutive tiles
+// (chunks never straddle a unit), so the warps in flight write one advancing window of the output.
+__device__ __forceinline__ uint64_t tile_adv(uint64_t c, uint64_t tw) {
+  return ((c + 1) % CHUNK) != 0 ? c + 1 : c + 1 + (tw - 1) * CHUNK;
+}
+// The warp's first tile at or past tile `ue` (a unit boundary), given its current tile c.
+__device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64_t tw) {
+  const uint64_t j = c / CHUNK, je = ue / CHUNK;
+  return (j + ((je - j + tw - 1) / tw) * tw) * CHUNK;
+}
 
 constexpr uint32_t kForeign = 0xFEu;  // unit owned by the general kernels
 
@@ -674,7 +684,10 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
 constexpr int DT_WARPS = 16;
 constexpr int DT = DT_WARPS * 32;
 constexpr int DSTAGES = 3;
-constexpr size_t DEC_SMEM = static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES + 1024 + DT_WARPS * DSTAGES * 8;
+// Per-unit views (codec, width) cached in shared memory for the first DEC_VIEWS units: one byte
+// each, 0 = not this kernel's, 33 = RAW, else the FixedLen width.
+constexpr uint32_t DEC_VIEWS = 4096;
+constexpr size_t DEC_SMEM = static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES + 1024 + DT_WARPS * DSTAGES * 8 + DEC_VIEWS;
 
 struct DecView {
   uint32_t codec;  // ZC_CODEC_RAW / ZC_CODEC_FIXEDLEN when this kernel owns the unit, else kFallback
@@ -776,21 +789,32 @@ __device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t 
   }
 }
 
-struct DecSeq {  // a warp's contiguous tile range over owned units, with the current unit's view
-  uint64_t end;
+__device__ __forceinline__ uint8_t pack_view(const DecView& v) {
+  return v.codec == kFallback ? 0 : v.codec == ZC_CODEC_RAW ? 33 : static_cast<uint8_t>(v.width);
+}
+__device__ __forceinline__ DecView unpack_view(uint8_t b) {
+  DecView v;
+  v.codec = b == 0 ? kFallback : b == 33 ? ZC_CODEC_RAW : ZC_CODEC_FIXEDLEN;
+  v.width = b == 33 ? 32u : b;
+  return v;
+}
+
+struct DecSeq {  // a warp's tile sequence over owned units, with the view of the current unit
+  uint64_t nfull, tw;
   uint32_t ush, cu;
   DecView cv;
+  const uint8_t* views;  // shared-memory view table (units < DEC_VIEWS)
   __device__ __forceinline__ uint64_t next(const DecParams& p, uint64_t c) {
-    while (c < end) {
+    while (c < nfull) {
       const uint32_t u = static_cast<uint32_t>(c >> ush);
       if (u != cu) {
         cu = u;
-        cv = dec_view(p, u);
+        cv = u < DEC_VIEWS ? unpack_view(views[u]) : dec_view(p, u);
       }
       if (cv.codec != kFallback) return c;
-      c = static_cast<uint64_t>(u + 1) << ush;
+      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) << ush, tw);
     }
-    return end;
+    return nfull;
   }
 };
 
@@ -803,13 +827,20 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* my = s_tiles + static_cast<size_t>(warp) * DSTAGES * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES) + warp * DSTAGES;
+  uint8_t* views = reinterpret_cast<uint8_t*>(bars + DT_WARPS * DSTAGES - warp * DSTAGES);
   const double scale = p.scale;
   uint32_t err = 0;
-  // decoded codec per owned unit (recv_batch's dispatch result)
-  for (uint32_t u = blockIdx.x * DT + tid; u < p.nunits; u += gridDim.x * DT) {
+  // every unit's view (recv_batch's dispatch result), once per CTA; the decoded codec per owned unit
+  for (uint32_t u = tid; u < p.nunits && u < DEC_VIEWS; u += DT) {
+    const DecView v = dec_view(p, u);
+    views[u] = pack_view(v);
+    if (v.codec != kFallback && p.codec_out && u % gridDim.x == blockIdx.x) p.codec_out[u] = v.codec;
+  }
+  for (uint32_t u = DEC_VIEWS + blockIdx.x * DT + tid; u < p.nunits; u += gridDim.x * DT) {
     const DecView v = dec_view(p, u);
     if (v.codec != kFallback && p.codec_out) p.codec_out[u] = v.codec;
   }
+  __syncthreads();
   if (lane == 0) {
     for (int i = 0; i < DSTAGES; ++i) tma::mbar_init(&bars[i], 1);
     tma::fence_barrier_init();
@@ -819,8 +850,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * DT_WARPS + warp;
   const uint32_t ush = unit_tile_shift(p.unit_bytes);
   const uint64_t umask = (1ull << ush) - 1;
-  const uint64_t t_beg = nfull * gw / tw, t_end = nfull * (gw + 1) / tw;
-  DecSeq iss{t_end, ush, 0xffffffffu, {kFallback, 0}}, prc{t_end, ush, 0xffffffffu, {kFallback, 0}};
+  DecSeq iss{nfull, tw, ush, 0xffffffffu, {kFallback, 0}, views}, prc{nfull, tw, ush, 0xffffffffu, {kFallback, 0}, views};
   auto issue = [&](uint32_t st, uint64_t c) {  // lane 0: the packed rows of tile c into stage st
     const uint32_t u = static_cast<uint32_t>(c >> ush);
     const uint32_t bytes = 128u * iss.cv.width;
@@ -828,25 +858,25 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     tma::mbar_arrive_expect_tx(&bars[st], bytes);
     tma::load_1d(my + st * TILE_BYTES, src, bytes, &bars[st]);
   };
-  uint64_t c_issue = iss.next(p, t_beg);
+  uint64_t c_issue = iss.next(p, gw * CHUNK);
   for (int i = 0; i < DSTAGES - 1; ++i) {
-    if (c_issue < t_end) {
+    if (c_issue < nfull) {
       if (lane == 0) issue(i, c_issue);
-      c_issue = iss.next(p, c_issue + 1);
+      c_issue = iss.next(p, tile_adv(c_issue, tw));
     }
   }
   uint32_t k = 0;
-  for (uint64_t c = prc.next(p, t_beg); c < t_end; c = prc.next(p, c + 1), ++k) {
+  for (uint64_t c = prc.next(p, gw * CHUNK); c < nfull; c = prc.next(p, tile_adv(c, tw)), ++k) {
     const uint32_t st = k % DSTAGES;
     // refill the stage that tile k-1 used once its store has read the buffer (the ring keeps
     // DSTAGES-1 loads in flight while this tile is decoded)
-    if (c_issue < t_end) {
+    if (c_issue < nfull) {
       const uint32_t rs = (k + DSTAGES - 1) % DSTAGES;
       if (lane == 0) {
         tma::bulk_wait_read<0>();
         issue(rs, c_issue);
       }
-      c_issue = iss.next(p, c_issue + 1);
+      c_issue = iss.next(p, tile_adv(c_issue, tw));
     }
     tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
     const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
@@ -860,7 +890,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     }
   }
   // the message's last, partial tile: symbol by symbol with byte-exact bounds
-  if (nfull < ntiles && gw == tw - 1) {
+  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
     const uint32_t u = static_cast<uint32_t>(nfull >> ush);
     const DecView v = dec_view(p, u);
     if (v.codec != kFallback) {
