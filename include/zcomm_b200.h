@@ -188,6 +188,10 @@ void zc_device_free(void* d_ptr);
 int zc_memcpy(void* dst, const void* src, uint64_t bytes);
 int zc_memset(void* d_ptr, int value, uint64_t bytes);
 int zc_stream_synchronize(void* stream); /* NULL = the legacy default stream */
+/* Device memory released while a collective is in flight (a communicator, Huffman context or
+ * zc_device_free buffer dropped on a rank thread) is freed at the next quiescent point; this
+ * performs those frees now when no collective is in flight. */
+void zc_flush_deferred(void);
 /* Reference defaults: ArbitrationConfig{} (rea.hpp:64-79), TransportHint{} (rea.hpp:33-36),
  * CollectiveConfig{} (collectives.hpp:24-34). */
 void zc_default_arb_config(zc_arb_config* h_cfg);

@@ -341,6 +341,7 @@ class LocalCommunicator {
         }
       });
     for (auto& t : th) t.join();
+    zc_flush_deferred();
     std::exception_ptr root, any;
     for (auto& e : errs) {
       if (!e) continue;

@@ -13,6 +13,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <vector>
 
 #include "zc_api_internal.h"
 #include "zc_huffman_host.hpp"
@@ -33,6 +34,48 @@ std::atomic<uint64_t>& launch_counter() {
   return n;
 }
 void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+std::atomic<int> g_inflight{0};
+std::mutex g_dead_mu;
+struct Dead {
+  int device;
+  void* p;
+  bool ipc;
+};
+std::vector<Dead> g_dead;
+void free_now(const Dead& d) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(d.device);
+  if (d.ipc) cudaIpcCloseMemHandle(d.p);
+  else cudaFree(d.p);
+  cudaSetDevice(cur);
+}
+}  // namespace
+
+InFlight::InFlight() { g_inflight.fetch_add(1); }
+InFlight::~InFlight() { g_inflight.fetch_sub(1); }
+
+void release_device_memory(int device, void* p, bool ipc_handle) {
+  if (p == nullptr) return;
+  if (g_inflight.load() > 0) {
+    std::lock_guard<std::mutex> g(g_dead_mu);
+    g_dead.push_back(Dead{device, p, ipc_handle});
+    return;
+  }
+  free_now(Dead{device, p, ipc_handle});
+}
+
+void flush_deferred_if_idle() {
+  std::vector<Dead> v;
+  {
+    std::lock_guard<std::mutex> g(g_dead_mu);
+    if (g_inflight.load() > 0) return;
+    v.swap(g_dead);
+  }
+  for (const Dead& d : v) free_now(d);
+}
 
 int set_err(int code, const std::string& msg) {
   g_err = msg;
@@ -187,8 +230,12 @@ int zc_device_malloc(uint64_t bytes, void** d_out) {
   return cuda_err(cudaMalloc(d_out, bytes ? bytes : 1), "cudaMalloc");
 }
 void zc_device_free(void* d) {
-  if (d) cudaFree(d);
+  if (!d) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  zc::release_device_memory(dev, d, false);
 }
+void zc_flush_deferred(void) { zc::flush_deferred_if_idle(); }
 int zc_memcpy(void* dst, const void* src, uint64_t bytes) {
   return cuda_err(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault), "cudaMemcpy");
 }
@@ -495,13 +542,7 @@ int zc_huff_ctx_codes(const zc_huff_ctx* c, uint32_t* code, uint32_t* rev) {
 
 void zc_huff_ctx_destroy(zc_huff_ctx* c) {
   if (!c) return;
-  for (auto& kv : c->dev) {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    cudaSetDevice(kv.first);
-    cudaFree(kv.second);
-    cudaSetDevice(cur);
-  }
+  for (auto& kv : c->dev) zc::release_device_memory(kv.first, kv.second, false);
   delete c;
 }
 
@@ -635,7 +676,7 @@ __attribute__((visibility("hidden"))) int zc_i_reserve_scratch(void* stream, uin
   return reserve_scratch(static_cast<cudaStream_t>(stream), nunits);
 }
 
-__attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, int kind, uint64_t total, double scale, uint64_t unit_bytes, uint8_t* d_stages, uint64_t stride,
+__attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, int kind, uint64_t total, double scale, const zc_i_batch_opts* o, uint8_t* d_stages, uint64_t stride,
                           uint64_t stage_len, int32_t pin, const zc_transport_hint* hint, const zc_huff_ctx* ctx,
                           const zc_arb_config* cfg, zc_encode_result* d_results, uint32_t* d_index, uint32_t* d_err,
                           void* stream) {
@@ -649,9 +690,12 @@ __attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, i
   p.pin = pin;
   p.scale = scale;
   p.rcp = 1.0 / scale;
+  const uint64_t unit_bytes = o && o->unit_bytes ? o->unit_bytes : ZC_BATCH_RAW_BYTES;
   p.total_bytes = total;
   p.unit_bytes = unit_bytes;
   p.nunits = static_cast<uint32_t>((total + unit_bytes - 1) / unit_bytes);
+  p.dscale = o ? o->dscale : nullptr;
+  p.maxzz_in = o ? o->maxzz_in : nullptr;
   p.stages = d_stages;
   p.stride = stride;
   p.stage_len = stage_len;
@@ -666,7 +710,7 @@ int zc_encode_batches_sym(const int32_t* d_sym, uint64_t raw_bytes, uint8_t* d_s
                           uint64_t stage_len, int32_t pin, const zc_transport_hint* hint, const zc_huff_ctx* ctx,
                           const zc_arb_config* cfg, zc_encode_result* d_results, uint32_t* d_index, uint32_t* d_err,
                           void* stream) {
-  return zc_i_encode_batches(d_sym, SRC_BYTES, raw_bytes, 1.0, ZC_BATCH_RAW_BYTES, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
+  return zc_i_encode_batches(d_sym, SRC_BYTES, raw_bytes, 1.0, nullptr, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
                         d_index, d_err, stream);
 }
 
@@ -676,11 +720,11 @@ int zc_encode_batches_f32(const float* d_x, uint64_t count, double scale, uint8_
                           void* stream) {
   if (int rc = check_scale(scale, "eb_quantize_chunk")) return rc;
   if (!aligned16(d_x)) return set_err(ZC_ERR_INVALID_ARGUMENT, "input must be 16-byte aligned");
-  return zc_i_encode_batches(d_x, SRC_F32, count * 4, scale, ZC_BATCH_RAW_BYTES, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
+  return zc_i_encode_batches(d_x, SRC_F32, count * 4, scale, nullptr, d_stages, stride, stage_len, pin, hint, ctx, cfg, d_results,
                         d_index, d_err, stream);
 }
 
-__attribute__((visibility("hidden"))) int zc_i_decode_batches(const uint8_t* d_stages, uint64_t unit_bytes, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
+__attribute__((visibility("hidden"))) int zc_i_decode_batches(const uint8_t* d_stages, const zc_i_batch_opts* o, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t total, const zc_huff_ctx* ctx, const uint32_t* d_index, int out_kind, void* out,
                           double scale, uint32_t* d_codec, uint32_t* d_err, void* stream, int own_frames) {
   if (total == 0) return ZC_OK;
@@ -691,9 +735,13 @@ __attribute__((visibility("hidden"))) int zc_i_decode_batches(const uint8_t* d_s
   p.stride = stride;
   p.region = stage_len;
   p.frame_len = d_sent;
+  const uint64_t unit_bytes = o && o->unit_bytes ? o->unit_bytes : ZC_BATCH_RAW_BYTES;
   p.total_bytes = total;
   p.unit_bytes = unit_bytes;
   p.nunits = static_cast<uint32_t>((total + unit_bytes - 1) / unit_bytes);
+  p.dscale = o ? o->dscale : nullptr;
+  p.acc_f32 = o ? o->acc_f32 : nullptr;
+  p.maxzz_out = o ? o->maxzz_out : nullptr;
   p.out_kind = out_kind;
   p.out = out;
   p.scale = scale;
@@ -709,21 +757,21 @@ __attribute__((visibility("hidden"))) int zc_i_decode_batches(const uint8_t* d_s
 int zc_decode_batches_sym(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t raw_bytes, const zc_huff_ctx* ctx, const uint32_t* d_index, int32_t* d_sym,
                           uint32_t* d_codec_out, void* stream) {
-  return zc_i_decode_batches(d_stages, ZC_BATCH_RAW_BYTES, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_BYTES, d_sym, 1.0, d_codec_out,
+  return zc_i_decode_batches(d_stages, nullptr, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_BYTES, d_sym, 1.0, d_codec_out,
                         nullptr, stream, 0);
 }
 
 int zc_decode_batches_f32(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len, const zc_encode_result* d_sent,
                           uint64_t count, double scale, const zc_huff_ctx* ctx, const uint32_t* d_index, float* d_out,
                           uint32_t* d_codec_out, void* stream) {
-  return zc_i_decode_batches(d_stages, ZC_BATCH_RAW_BYTES, stride, stage_len, d_sent, count * 4, ctx, d_index, OUT_F32, d_out, scale,
+  return zc_i_decode_batches(d_stages, nullptr, stride, stage_len, d_sent, count * 4, ctx, d_index, OUT_F32, d_out, scale,
                         d_codec_out, nullptr, stream, 0);
 }
 
 int zc_decode_batches_add_sym(const uint8_t* d_stages, uint64_t stride, uint64_t stage_len,
                               const zc_encode_result* d_sent, uint64_t raw_bytes, const zc_huff_ctx* ctx,
                               const uint32_t* d_index, int32_t* d_acc, uint32_t* d_err, void* stream) {
-  return zc_i_decode_batches(d_stages, ZC_BATCH_RAW_BYTES, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_ADD_I32, d_acc, 1.0, nullptr,
+  return zc_i_decode_batches(d_stages, nullptr, stride, stage_len, d_sent, raw_bytes, ctx, d_index, OUT_ADD_I32, d_acc, 1.0, nullptr,
                         d_err, stream, 0);
 }
 
@@ -796,12 +844,12 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
     if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, pp->h2d), "H2D")) return rc;
     if (int rc = cuda_err(cudaEventRecord(in, pp->h2d), "H2D event")) return rc;
     if (int rc = cuda_err(cudaStreamWaitEvent(pp->work, in, 0), "H2D wait")) return rc;
-    if (int rc = zc_i_encode_batches(d_work + e0, SRC_F32, n * 4, scale, ZC_BATCH_RAW_BYTES, d_stages + b0 * stride, stride, stage_len, pin, hint,
+    if (int rc = zc_i_encode_batches(d_work + e0, SRC_F32, n * 4, scale, nullptr, d_stages + b0 * stride, stride, stage_len, pin, hint,
                                 ctx, cfg, d_results + b0, d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr,
                                 d_err, pp->work))
       return rc;
     // decoded in place: the group's encode has consumed its input (stream order)
-    if (int rc = zc_i_decode_batches(d_stages + b0 * stride, ZC_BATCH_RAW_BYTES, stride, stage_len, d_results + b0, n * 4, ctx,
+    if (int rc = zc_i_decode_batches(d_stages + b0 * stride, nullptr, stride, stage_len, d_results + b0, n * 4, ctx,
                                 d_index ? d_index + b0 * ZC_HUFF_INDEX_ENTRIES : nullptr, OUT_F32, d_work + e0, scale,
                                 nullptr, d_err, pp->work, own))
       return rc;

@@ -120,7 +120,7 @@ __device__ void decide_unit(const EncParams& p, BUnit& U, uint32_t u, bool want_
           mn = dkey_inv(~__ldcg(&U.dmin_c));
           mx = dkey_inv(__ldcg(&U.dmax_k));
         }
-        maxzz = max(zigzag32(quantize_one(mx, p.scale, p.rcp, err)), zigzag32(quantize_one(mn, p.scale, p.rcp, err)));
+        maxzz = max(zigzag32(quantize_one(mx, enc_scale(p), enc_rcp(p), err)), zigzag32(quantize_one(mn, enc_scale(p), enc_rcp(p), err)));
       }
     }
     if (R >= 4 && R % 4 == 0) {

@@ -57,15 +57,26 @@ constexpr uint32_t kRegions = 3;
 // send to any rank at any time without the ring's piece counters.
 constexpr uint32_t kP2PRegions = 2;
 constexpr uint32_t kP2PUnits = 4;
+// Relay lane (all-gather hops after the first, broadcast hops after the first): a received piece is
+// forwarded verbatim — frames, companion index and results copied into the successor's relay
+// regions — since AG frames are a pure function of the bytes, so re-encoding them would ship the
+// same frames (collectives.cpp:494-502).  Its own regions and counters keep its sequence apart
+// from the encoded pieces of the main lane.  The all-gather wavefront needs n relay regions per
+// rank to be deadlock-free for any number of pieces per chunk (a rank's forward waits for the
+// region its successor freed n-1 forwards earlier; checked by simulating the flag protocol over
+// n <= 16 ranks and up to 24 pieces per chunk); with more than kMaxRelayRanks ranks the hops
+// re-encode instead.
+constexpr uint32_t kMaxRelayRanks = 16;
+uint32_t relay_regions(uint32_t nranks) { return nranks >= 3 && nranks <= kMaxRelayRanks ? nranks : 0u; }
 
 struct Layout {
-  uint32_t nbanks, runits, nranks;
+  uint32_t nbanks, runits, nranks, nrelay;
   uint64_t ub, fstride;  // unit (batch) raw bytes; frame stride inside a piece region
   uint64_t bank_stride, idx_off;
   uint64_t reg_stride, reg_idx, reg_res;  // region size; index / results offsets inside a region
   uint64_t p2p_stride, p2p_idx, p2p_res;  // the same for a point-to-point region (kP2PUnits frames)
-  uint64_t off_banks, off_reg, off_p2p, off_ready, off_len, off_credit, off_sready, off_scredit, off_pready, off_pcons,
-      off_err, off_mbox, off_mflag, off_wire, off_errall, off_scal, off_peers, total;
+  uint64_t off_banks, off_reg, off_rly, off_p2p, off_ready, off_len, off_credit, off_sready, off_scredit, off_rready,
+      off_rcons, off_pready, off_pcons, off_err, off_mbox, off_mflag, off_wire, off_errall, off_scal, off_peers, total;
 };
 
 constexpr uint64_t kStageStride = (ZC_STAGE_BANK_BYTES + 255) / 256 * 256;
@@ -97,6 +108,9 @@ Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nra
   o += nbanks * L.bank_stride;
   L.off_reg = o;
   o += kRegions * L.reg_stride;
+  L.off_rly = o;  // relay regions (written by the predecessor's forwards)
+  L.nrelay = relay_regions(nranks);
+  o += static_cast<uint64_t>(L.nrelay) * L.reg_stride;
   L.off_p2p = o;  // [sender][kP2PRegions] regions (none for a single rank)
   o += nranks > 1 ? static_cast<uint64_t>(nranks) * kP2PRegions * L.p2p_stride : 0;
   L.off_ready = o;
@@ -109,6 +123,10 @@ Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nra
   o += kAlign;
   L.off_scredit = o;  // [r]: pieces rank r has consumed from its regions (written by rank r)
   o += align_up(8ull * kMaxRanks, kAlign);
+  L.off_rready = o;  // [nrelay]: relay pieces received in relay region i (written by the predecessor)
+  o += kAlign;
+  L.off_rcons = o;  // relay pieces the successor has consumed (written by the successor)
+  o += kAlign;
   L.off_pready = o;  // [s][kP2PRegions]: point-to-point piece count in region i from sender s
   o += align_up(8ull * kMaxRanks * kP2PRegions, kAlign);
   L.off_pcons = o;  // [d]: point-to-point pieces rank d has consumed from this rank (written by d)
@@ -135,6 +153,7 @@ Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nra
 struct Scal {
   double absmax;      // local max|x|
   double scale;       // shared bin width
+  double rcp;         // 1 / scale (with `scale`, the device quantizer pair of the fused encoders)
   double requant_f;   // llround(s * f) factor when this rank's scale differs
   uint32_t requant;   // 1 when requantization is needed
   uint32_t _p;
@@ -234,7 +253,10 @@ __device__ void mail_reduce(const MailArgs& a) {
     }
     s->gmax = m;
     s->out = m;
-    if (a.op == MAIL_EB_SCALE) s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, a.rel), m);
+    if (a.op == MAIL_EB_SCALE) {
+      s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, a.rel), m);
+      s->rcp = 1.0 / s->scale;
+    }
   } else {
     // StreamMeta {mode u8 @0, levels u32 @4, count u64 @8, scale f64 @16} (collectives.cpp:29-58)
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(mb + a.rank * 32);
@@ -254,6 +276,7 @@ __device__ void mail_reduce(const MailArgs& a) {
     }
     s->my_scale = my_scale;
     s->scale = shared;
+    s->rcp = 1.0 / shared;
     s->requant = (shared != my_scale && my_scale > 0.0) ? 1u : 0u;
     s->requant_f = my_scale / shared;
   }
@@ -351,6 +374,7 @@ __global__ void set_scale_kernel(Scal* s, double rel, int from_absmax) {
   if (from_absmax) {
     double m = s->absmax;
     s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, rel), m);
+    s->rcp = 1.0 / s->scale;
   }
 }
 
@@ -415,6 +439,29 @@ __global__ void piece_done_kernel(uint8_t* const* peers, uint64_t off, int rank,
     st_rel(reinterpret_cast<unsigned long long*>(peers[r] + off) + rank, v);
 }
 
+// Copies a received piece (frames of total_bytes each, the Huffman companion index of Huffman
+// frames, the EncodeResults) from this rank's region into a peer's relay region: one CTA per
+// frame, 16-byte vectors (frames sit at 256-byte-aligned strides).
+__global__ void forward_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t fstride,
+                               uint64_t reg_idx, uint64_t reg_res, uint32_t nunits, uint64_t bytes, uint64_t ub) {
+  const uint32_t u = blockIdx.x;
+  if (u >= nunits) return;
+  const zc_encode_result* res = reinterpret_cast<const zc_encode_result*>(src + reg_res);
+  const zc_encode_result r = res[u];
+  const uint64_t total = r.total_bytes;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + u * fstride);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + u * fstride);
+  for (uint64_t v = threadIdx.x; v * 16 < total; v += blockDim.x) d4[v] = __ldcg(s4 + v);
+  if (r.codec == ZC_CODEC_HUFFMAN) {
+    const uint64_t R = bytes - static_cast<uint64_t>(u) * ub < ub ? bytes - static_cast<uint64_t>(u) * ub : ub;
+    const uint64_t ne = (R + ZC_HUFF_INDEX_GRAIN - 1) / ZC_HUFF_INDEX_GRAIN;
+    const uint32_t* si = reinterpret_cast<const uint32_t*>(src + reg_idx) + static_cast<uint64_t>(u) * ZC_HUFF_INDEX_ENTRIES;
+    uint32_t* di = reinterpret_cast<uint32_t*>(dst + reg_idx) + static_cast<uint64_t>(u) * ZC_HUFF_INDEX_ENTRIES;
+    for (uint64_t i = threadIdx.x; i < ne; i += blockDim.x) di[i] = __ldcg(si + i);
+  }
+  if (threadIdx.x == 0) reinterpret_cast<zc_encode_result*>(dst + reg_res)[u] = r;
+}
+
 // Fallback of a single credit write (no stream memory operations).
 __global__ void flag_store_kernel(unsigned long long* flag, unsigned long long v) {
   __threadfence_system();
@@ -445,6 +492,9 @@ struct zc_comm {
   zc_huff_ctx* shared = nullptr;   // installed shared Huffman context (owned)
   uint64_t tx_seq = 0, rx_seq = 0;
   uint64_t ptx = 0, prx = 0;       // pieces sent to the successor / received from the predecessor
+  uint64_t rtx = 0, rrx = 0;       // relay pieces forwarded to the successor / received from the predecessor
+  uint32_t* mz = nullptr;          // [2][mz_cap] per-unit max zig-zag of reduced chunks (RS sink -> next send)
+  uint64_t mz_cap = 0;
   std::vector<uint64_t> p2p_tx, p2p_rx;  // point-to-point pieces sent to / received from each rank
   unsigned long long epoch = 0;
   zc_wire_stats host_wire{};       // control frames (meta / max) counted on the host
@@ -786,8 +836,33 @@ zc_comm::TlPiece* tl_begin(zc_comm* c, int kind, int peer, uint64_t seq, uint64_
   return &c->tl.back();
 }
 
-int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) {
+// What a piece send encodes: int32 symbols (SRC_BYTES) or, for allreduce_eb's first reduce-
+// scatter step, the rank's fp32 input quantized on the fly with the device-agreed scale.
+struct SendSpec {
+  const void* src;            // chunk base
+  int kind;                   // SRC_BYTES / SRC_F32
+  uint64_t bytes;             // chunk raw bytes (symbols)
+  int pin;
+  const uint32_t* mz_in;      // per unit of the chunk: max zig-zag known from the reduce sink (or null)
+};
+// Where a received piece goes: the sink kind, its destination, and whether the piece is forwarded
+// to the successor's relay lane before its region is returned.
+struct RecvSpec {
+  void* dst;                  // chunk base (OUT_BYTES / OUT_ADD_*: int32; OUT_F32 / OUT_F64: floats)
+  uint64_t bytes;             // chunk raw bytes (symbols)
+  int out_kind;
+  const float* acc;           // OUT_ADD_Q: the local fp32 chunk
+  uint32_t* mz_out;           // OUT_ADD_*: per unit of the chunk, the sums' max zig-zag (or null)
+  bool fwd;                   // forward verbatim to the successor (relay lane)
+  bool relay;                 // the piece arrives on the relay lane
+  int pin;
+};
+uint32_t out_elem_bytes(int kind) { return kind == OUT_F64 ? 8u : 4u; }
+
+int send_piece(zc_comm* c, int to, const SendSpec& sp, uint64_t k) {
   const Layout& y = c->lay;
+  const uint64_t pb = static_cast<uint64_t>(y.runits) * y.ub, off = k * pb;
+  const uint64_t bytes = std::min(pb, sp.bytes - off);
   zc_comm::TlPiece* tl = tl_begin(c, 0, to, c->ptx, bytes);
   zc_encode_result* log = tl ? c->tl_res + (c->tl.size() - 1) * y.runits : nullptr;
   const uint64_t seq = c->ptx++;
@@ -799,8 +874,12 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
   if (tl) cudaEventRecord(tl->e0, c->stream);
   uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
   auto* res = reinterpret_cast<zc_encode_result*>(dst + y.reg_res);
-  if (int rc = zc_i_encode_batches(src, SRC_BYTES, bytes, 1.0, y.ub, dst, y.fstride, ZC_STAGE_BANK_BYTES, pin,
-                                   &c->cfg.hint, c->shared, &c->cfg.arb, res,
+  zc_i_batch_opts o{};
+  o.unit_bytes = y.ub;
+  o.dscale = sp.kind == SRC_F32 ? &c->scal()->scale : nullptr;
+  o.maxzz_in = sp.mz_in ? sp.mz_in + k * y.runits : nullptr;
+  if (int rc = zc_i_encode_batches(static_cast<const uint8_t*>(sp.src) + off, sp.kind, bytes, 1.0, &o, dst, y.fstride,
+                                   ZC_STAGE_BANK_BYTES, sp.pin, &c->cfg.hint, c->shared, &c->cfg.arb, res,
                                    reinterpret_cast<uint32_t*>(dst + y.reg_idx), c->err_word(), c->stream))
     return rc;
   post_signal(reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + reg, seq + 1);
@@ -813,51 +892,113 @@ int send_piece(zc_comm* c, int to, const int32_t* src, uint64_t bytes, int pin) 
   return cuda_err(cudaGetLastError(), "piece send");
 }
 
-int recv_piece(zc_comm* c, int32_t* dst, uint64_t bytes, bool store, int pin) {
+// Forwards the piece in `region` (this rank's block) to the successor's relay lane: a send_batch
+// per frame in the reference (counted in WireStats like one), a bulk copy here.
+int forward_piece(zc_comm* c, const uint8_t* region, uint64_t bytes) {
+  const Layout& y = c->lay;
+  const int to = (c->rank + 1) % c->nranks;
+  zc_comm::TlPiece* tl = tl_begin(c, 0, to, c->rtx, bytes);
+  zc_encode_result* log = tl ? c->tl_res + (c->tl.size() - 1) * y.runits : nullptr;
+  const uint64_t seq = c->rtx++;
+  const uint32_t reg = static_cast<uint32_t>(seq % y.nrelay);
+  if (seq >= y.nrelay)
+    if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_rcons), seq - y.nrelay + 1))
+      return rc;
+  if (tl) cudaEventRecord(tl->e0, c->stream);
+  uint8_t* dst = c->peer[to] + y.off_rly + reg * y.reg_stride;
+  const uint32_t nu = static_cast<uint32_t>(nbatches(c, bytes));
+  note_launch();
+  forward_kernel<<<nu, 512, 0, c->stream>>>(region, dst, y.fstride, y.reg_idx, y.reg_res, nu, bytes, y.ub);
+  if (int rc = cuda_err(cudaGetLastError(), "forward")) return rc;
+  auto* ready = reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_rready) + reg;
+  post_signal(ready, seq + 1);
+  note_launch();
+  piece_sent_kernel<<<1, 32, 0, c->stream>>>(reinterpret_cast<const zc_encode_result*>(region + y.reg_res), nu, bytes,
+                                             y.ub, reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire), ready,
+                                             seq + 1, log);
+  if (tl) cudaEventRecord(tl->e1, c->stream);
+  return cuda_err(cudaGetLastError(), "forward publish");
+}
+
+int recv_piece(zc_comm* c, const RecvSpec& rs, uint64_t k) {
+  const Layout& y = c->lay;
+  const uint64_t pb = static_cast<uint64_t>(y.runits) * y.ub, off = k * pb;
+  const uint64_t bytes = std::min(pb, rs.bytes - off);
+  const int pin = rs.pin;
   // frames of our own batched encoder: without a Huffman context (or with a FixedLen / RAW pin)
   // all are FixedLen / RAW and the general decode kernels are skipped.  Embedded codebooks let
   // Auto pick Huffman with no shared context (rea.cpp:160), so those frames take the general path.
   const bool own = pin == ZC_PIN_RAW || pin == ZC_PIN_FIXEDLEN || (c->shared == nullptr && !c->cfg.arb.embed_codebook);
-  const Layout& y = c->lay;
-  zc_comm::TlPiece* tl = tl_begin(c, 1, -1, c->prx, bytes);
+  zc_comm::TlPiece* tl = tl_begin(c, 1, -1, rs.relay ? c->rrx : c->prx, bytes);
   if (tl) cudaEventRecord(tl->e0, c->stream);
-  const uint64_t seq = c->prx++;
-  const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
-  if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + reg, seq + 1))
-    return rc;
+  const uint64_t seq = rs.relay ? c->rrx++ : c->prx++;
+  const uint32_t reg = static_cast<uint32_t>(seq % (rs.relay ? y.nrelay : kRegions));
+  const unsigned long long* ready =
+      reinterpret_cast<const unsigned long long*>(c->block + (rs.relay ? y.off_rready : y.off_sready)) + reg;
+  if (int rc = launch_wait(c, ready, seq + 1)) return rc;
   if (tl) cudaEventRecord(tl->e1, c->stream);
-  const uint8_t* region = c->block + y.off_reg + reg * y.reg_stride;
-  if (int rc = zc_i_decode_batches(region, y.ub, y.fstride, ZC_STAGE_BANK_BYTES,
+  const uint8_t* region = c->block + (rs.relay ? y.off_rly : y.off_reg) + reg * y.reg_stride;
+  zc_i_batch_opts o{};
+  o.unit_bytes = y.ub;
+  o.dscale = (rs.out_kind == OUT_F32 || rs.out_kind == OUT_F64 || rs.out_kind == OUT_ADD_Q) ? &c->scal()->scale : nullptr;
+  o.acc_f32 = rs.acc ? rs.acc + off / 4 : nullptr;
+  o.maxzz_out = rs.mz_out ? rs.mz_out + k * y.runits : nullptr;
+  void* dst = static_cast<uint8_t*>(rs.dst) + off / 4 * out_elem_bytes(rs.out_kind);
+  if (int rc = zc_i_decode_batches(region, &o, y.fstride, ZC_STAGE_BANK_BYTES,
                                    reinterpret_cast<const zc_encode_result*>(region + y.reg_res), bytes, c->shared,
-                                   reinterpret_cast<const uint32_t*>(region + y.reg_idx), store ? OUT_BYTES : OUT_ADD_I32,
-                                   dst, 1.0, nullptr, c->err_word(), c->stream, own ? 1 : 0))
+                                   reinterpret_cast<const uint32_t*>(region + y.reg_idx), rs.out_kind, dst, 1.0, nullptr,
+                                   c->err_word(), c->stream, own ? 1 : 0))
     return rc;
-  if (int rc = post_credit(c, seq + 1)) return rc;
+  if (rs.fwd)
+    if (int rc = forward_piece(c, region, bytes)) return rc;
+  if (rs.relay) {  // return the relay region to the predecessor
+    auto* cons = reinterpret_cast<unsigned long long*>(c->peer[(c->rank - 1 + c->nranks) % c->nranks] + y.off_rcons);
+    if (c->memops) {
+      if (int rc = stream_write(c, cons, seq + 1)) return rc;
+    } else {
+      post_signal(cons, seq + 1);
+      note_launch();
+      flag_store_kernel<<<1, 1, 0, c->stream>>>(cons, seq + 1);
+    }
+  } else if (int rc = post_credit(c, seq + 1)) {
+    return rc;
+  }
   if (tl) cudaEventRecord(tl->e2, c->stream);
   return cuda_err(cudaGetLastError(), "piece recv");
 }
 
-// One exchange (BatchIo::exchange, collectives.cpp:366-396): `tx` to rank `to`, `rx` from whoever
+// One exchange (BatchIo::exchange, collectives.cpp:366-396): `sp` to rank `to`, `rs` from whoever
 // sends to this rank, in pieces; sends run one piece ahead of receives.
-int staged_xfer(zc_comm* c, int to, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin,
-                bool store) {
+int staged_xfer(zc_comm* c, int to, const SendSpec& sp, const RecvSpec& rs) {
   const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
-  const uint64_t ns = (tx_bytes + pb - 1) / pb, nr = (rx_bytes + pb - 1) / pb;
+  const uint64_t ns = (sp.bytes + pb - 1) / pb, nr = (rs.bytes + pb - 1) / pb;
   const uint64_t steps = std::max(ns, nr) + 1;
   for (uint64_t k = 0; k < steps; ++k) {
     if (k < ns)
-      if (int rc = send_piece(c, to, tx + k * (pb / 4), std::min(pb, tx_bytes - k * pb), pin)) return rc;
+      if (int rc = send_piece(c, to, sp, k)) return rc;
     if (k >= 1 && k - 1 < nr)
-      if (int rc = recv_piece(c, rx + (k - 1) * (pb / 4), std::min(pb, rx_bytes - (k - 1) * pb), store, pin)) return rc;
+      if (int rc = recv_piece(c, rs, k - 1)) return rc;
   }
   return ZC_OK;
 }
 
-int staged_step(zc_comm* c, const int32_t* tx, uint64_t tx_bytes, int32_t* rx, uint64_t rx_bytes, int pin, bool store) {
-  return staged_xfer(c, (c->rank + 1) % c->nranks, tx, tx_bytes, rx, rx_bytes, pin, store);
+// Receives every piece of a relay-lane hop (the sends of this hop were the forwards of the
+// previous one).
+int relay_recv(zc_comm* c, const RecvSpec& rs) {
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
+  for (uint64_t k = 0; k * pb < rs.bytes; ++k)
+    if (int rc = recv_piece(c, rs, k)) return rc;
+  return ZC_OK;
 }
 
-// The single-kernel step (ZC_RING_KERNEL=1) stages 4 MiB batches only.
+SendSpec sym_send(const int32_t* src, uint64_t bytes, int pin, const uint32_t* mz_in = nullptr) {
+  return SendSpec{src, SRC_BYTES, bytes, pin, mz_in};
+}
+RecvSpec sym_recv(int32_t* dst, uint64_t bytes, int kind, int pin, uint32_t* mz_out = nullptr) {
+  return RecvSpec{dst, bytes, kind, nullptr, mz_out, false, false, pin};
+}
+
+
 // ---- point-to-point (RankCtx::send_encoded / recv_decoded, collectives.cpp:350-364): the message
 // in pieces of kP2PUnits batches, each encoded (send_batch per batch, cfg.pin) straight into the
 // pair's region in the receiver's block and published like a ring piece; the receiver decodes it
@@ -876,7 +1017,9 @@ int p2p_send(zc_comm* c, int to, const uint8_t* src, uint64_t bytes) {
         return rc;
     uint8_t* dst = c->peer[to] + y.off_p2p + (static_cast<uint64_t>(c->rank) * kP2PRegions + reg) * y.p2p_stride;
     auto* res = reinterpret_cast<zc_encode_result*>(dst + y.p2p_res);
-    if (int rc = zc_i_encode_batches(src + off, SRC_BYTES, len, 1.0, y.ub, dst, y.fstride, ZC_STAGE_BANK_BYTES,
+    zc_i_batch_opts o{};
+    o.unit_bytes = y.ub;
+    if (int rc = zc_i_encode_batches(src + off, SRC_BYTES, len, 1.0, &o, dst, y.fstride, ZC_STAGE_BANK_BYTES,
                                      c->cfg.pin, &c->cfg.hint, c->shared, &c->cfg.arb, res,
                                      reinterpret_cast<uint32_t*>(dst + y.p2p_idx), c->err_word(), c->stream))
       return rc;
@@ -905,7 +1048,9 @@ int p2p_recv(zc_comm* c, int from, uint8_t* dst, uint64_t bytes) {
     if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_pready) + slot, k + 1))
       return rc;
     const uint8_t* region = c->block + y.off_p2p + slot * y.p2p_stride;
-    if (int rc = zc_i_decode_batches(region, y.ub, y.fstride, ZC_STAGE_BANK_BYTES,
+    zc_i_batch_opts o{};
+    o.unit_bytes = y.ub;
+    if (int rc = zc_i_decode_batches(region, &o, y.fstride, ZC_STAGE_BANK_BYTES,
                                      reinterpret_cast<const zc_encode_result*>(region + y.p2p_res), len, c->shared,
                                      reinterpret_cast<const uint32_t*>(region + y.p2p_idx), OUT_BYTES, dst + off, 1.0,
                                      nullptr, c->err_word(), c->stream, own ? 1 : 0))
@@ -925,42 +1070,114 @@ int p2p_recv(zc_comm* c, int from, uint8_t* dst, uint64_t bytes) {
 
 bool use_staged(const zc_comm* c) { return c->cfg.per_slot_framing || std::getenv("ZC_RING_KERNEL") == nullptr; }
 
+// The fused ring (default; ZC_RING_UNFUSED=1 restores the re-encoding hops for A/B runs):
+//  - a reduce sink records each unit's max zig-zag of the sums it writes, so the next send of that
+//    chunk decides its FixedLen width without a range pass over the sums (decode -> reduce ->
+//    range in one kernel; the encode then reads the sums once, from L2 when they are still there);
+//  - all-gather hops after the first forward the received frames verbatim (relay lane).
+bool fuse_ring() { return std::getenv("ZC_RING_UNFUSED") == nullptr; }
+
+// Two per-unit max zig-zag arrays (by reduce-scatter step parity), allocated with the communicator
+// (kMzUnits units each: chunks up to 256 GiB of 4 MiB batches); a chunk with more units takes the
+// range pass instead.  Nothing is allocated on a collective's path: cudaMalloc / cudaFree may wait
+// for the whole device, i.e. for a peer rank's queued waits in a single-process group.
+constexpr uint64_t kMzUnits = 65536;
+bool use_mz(zc_comm* c, uint64_t units) { return c->mz != nullptr && units <= c->mz_cap; }
+uint32_t* mz_buf(zc_comm* c, int t) { return c->mz + static_cast<uint64_t>(t & 1) * c->mz_cap; }
+uint64_t max_chunk_units(zc_comm* c, uint64_t count) {
+  return nbatches(c, ((count + c->nranks - 1) / c->nranks + 1) * 4);
+}
+
+struct Chunks {  // the ring's chunk bounds c * count / n (collectives.cpp:465-467)
+  uint64_t count;
+  int n;
+  uint64_t lo(int ci) const {
+    ci = ((ci % n) + n) % n;
+    return chunk_lo(count, n, ci);
+  }
+  uint64_t bytes(int ci) const {
+    ci = ((ci % n) + n) % n;
+    return (chunk_lo(count, n, ci + 1) - chunk_lo(count, n, ci)) * 4;
+  }
+};
+
+// The all-gather phase: hop 0 sends `first` (the chunk this rank owns) and receives chunk r; hop t
+// receives chunk r - t.  `recv_of(ci)` gives the sink of chunk ci.
+// Fused: every received piece but the last hop's is forwarded verbatim to the successor's relay
+// lane (hop t's sends are hop t-1's forwards).  The hops run as one wavefront — at time k: hop 0
+// sends piece k, then hop h receives (and forwards) piece k-1-h — so a rank consumes its relay
+// pieces at the pace its predecessor forwards them: a forward only ever waits for relay pieces
+// forwarded at earlier times, and two relay regions suffice.  (Running the hops one after another
+// would deadlock: a rank's forwards of hop 0 would wait for a successor still in its own hop 0.)
+template <class RecvOf>
+int allgather_hops(zc_comm* c, const SendSpec& first, RecvOf recv_of) {
+  const int n = c->nranks, r = c->rank, next = (r + 1) % n;
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
+  if (!(fuse_ring() && c->lay.nrelay > 0)) {  // each hop re-encodes the chunk received at the previous hop
+    if (int rc = staged_xfer(c, next, first, recv_of(r))) return rc;
+    for (int t = 1; t < n - 1; ++t) {
+      const RecvSpec prev = recv_of(r + 1 - t);
+      if (int rc = staged_xfer(c, next, sym_send(static_cast<const int32_t*>(prev.dst), prev.bytes, first.pin),
+                               recv_of(r - t)))
+        return rc;
+    }
+    return ZC_OK;
+  }
+  std::vector<RecvSpec> hop(n - 1);
+  std::vector<uint64_t> np(n - 1);
+  uint64_t kmax = (first.bytes + pb - 1) / pb;
+  for (int h = 0; h < n - 1; ++h) {
+    hop[h] = recv_of(r - h);
+    hop[h].relay = h > 0;
+    hop[h].fwd = h < n - 2;
+    np[h] = (hop[h].bytes + pb - 1) / pb;
+    kmax = std::max<uint64_t>(kmax, np[h] + 1 + h);
+  }
+  const uint64_t ns = (first.bytes + pb - 1) / pb;
+  for (uint64_t k = 0; k < kmax; ++k) {
+    if (k < ns)
+      if (int rc = send_piece(c, next, first, k)) return rc;
+    for (int h = 0; h < n - 1; ++h) {
+      if (k < 1ull + h) break;
+      const uint64_t j = k - 1 - h;
+      if (j < np[h])
+        if (int rc = recv_piece(c, hop[h], j)) return rc;
+    }
+  }
+  return ZC_OK;
+}
+
 // Reduce-scatter then (optionally) all-gather over the ring (collectives.cpp:460-502).  RS frames
-// use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.  An AG step re-encodes the
-// chunk it received in the previous step: frames are a pure function of the bytes, so every hop
-// ships the frame the reference would.
+// use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.
 int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
   const int n = c->nranks, r = c->rank;
   const uint64_t msg = count * 4;
   const int fused_pin = msg >= c->cfg.fused_codec_min_msg_bytes ? c->cfg.pin : ZC_PIN_RAW;
-  auto chunk = [&](int ci, int32_t** base, uint64_t* bytes) {
-    ci = ((ci % n) + n) % n;
-    uint64_t lo = chunk_lo(count, n, ci), hi = chunk_lo(count, n, ci + 1);
-    *base = d_sym + lo;
-    *bytes = (hi - lo) * 4;
-  };
-  int32_t *sb, *rb;
-  uint64_t sby, rby;
+  const Chunks ch{count, n};
+  if (!use_staged(c)) {  // the single-kernel steps (ZC_RING_KERNEL=1)
+    for (int t = 0; t < n - 1; ++t)
+      if (int rc = exchange_step(c, d_sym + ch.lo(r - t), ch.bytes(r - t), d_sym + ch.lo(r - t - 1), ch.bytes(r - t - 1),
+                                 fused_pin, false, "rs-step"))
+        return rc;
+    if (!allgather) return ZC_OK;
+    for (int t = 0; t < n - 1; ++t)
+      if (int rc = exchange_step(c, d_sym + ch.lo(r + 1 - t), ch.bytes(r + 1 - t), d_sym + ch.lo(r - t), ch.bytes(r - t),
+                                 c->cfg.pin, true, "ag-step"))
+        return rc;
+    return ZC_OK;
+  }
+  const bool fz = fuse_ring() && use_mz(c, max_chunk_units(c, count));
   for (int t = 0; t < n - 1; ++t) {
-    chunk(r - t, &sb, &sby);
-    chunk(r - t - 1, &rb, &rby);
-    if (use_staged(c)) {
-      if (int rc = staged_step(c, sb, sby, rb, rby, fused_pin, false)) return rc;
-    } else if (int rc = exchange_step(c, sb, sby, rb, rby, fused_pin, false, "rs-step")) {
+    uint32_t* mo = fz ? mz_buf(c, t) : nullptr;
+    if (mo)
+      if (int rc = cuda_err(cudaMemsetAsync(mo, 0, max_chunk_units(c, count) * 4, c->stream), "unit ranges")) return rc;
+    if (int rc = staged_xfer(c, (r + 1) % n, sym_send(d_sym + ch.lo(r - t), ch.bytes(r - t), fused_pin, fz && t > 0 ? mz_buf(c, t - 1) : nullptr),
+                             sym_recv(d_sym + ch.lo(r - t - 1), ch.bytes(r - t - 1), OUT_ADD_I32, fused_pin, mo)))
       return rc;
-    }
   }
   if (!allgather) return ZC_OK;
-  for (int t = 0; t < n - 1; ++t) {
-    chunk(r + 1 - t, &sb, &sby);
-    chunk(r - t, &rb, &rby);
-    if (use_staged(c)) {
-      if (int rc = staged_step(c, sb, sby, rb, rby, c->cfg.pin, true)) return rc;
-    } else if (int rc = exchange_step(c, sb, sby, rb, rby, c->cfg.pin, true, "ag-step")) {
-      return rc;
-    }
-  }
-  return ZC_OK;
+  return allgather_hops(c, sym_send(d_sym + ch.lo(r + 1), ch.bytes(r + 1), c->cfg.pin, fz ? mz_buf(c, n - 2) : nullptr),
+                        [&](int ci) { return sym_recv(d_sym + ch.lo(ci), ch.bytes(ci), OUT_BYTES, c->cfg.pin); });
 }
 
 // All-gather of equal blocks (collectives.cpp:525-544): step t sends block (r-t), receives (r-t-1).
@@ -968,17 +1185,15 @@ int enqueue_allgather(zc_comm* c, int32_t* d_all, uint64_t block) {
   const int n = c->nranks, r = c->rank;
   if (n == 1 || block == 0) return ZC_OK;
   const uint64_t by = block * 4;
-  for (int t = 0; t < n - 1; ++t) {
-    const int si = ((r - t) % n + n) % n, ri = ((r - t - 1) % n + n) % n;
-    int32_t* sb = d_all + static_cast<uint64_t>(si) * block;
-    int32_t* rb = d_all + static_cast<uint64_t>(ri) * block;
-    if (use_staged(c)) {
-      if (int rc = staged_step(c, sb, by, rb, by, c->cfg.pin, true)) return rc;
-    } else if (int rc = exchange_step(c, sb, by, rb, by, c->cfg.pin, true, "ag-step")) {
-      return rc;
-    }
+  auto blk = [&](int i) { return d_all + static_cast<uint64_t>(((i % n) + n) % n) * block; };
+  if (!use_staged(c)) {
+    for (int t = 0; t < n - 1; ++t)
+      if (int rc = exchange_step(c, blk(r - t), by, blk(r - t - 1), by, c->cfg.pin, true, "ag-step")) return rc;
+    return ZC_OK;
   }
-  return ZC_OK;
+  // allgather_hops numbers chunks like the allreduce AG (hop t receives r - t): shift by one
+  const int pin = c->cfg.pin;
+  return allgather_hops(c, sym_send(blk(r), by, pin), [&](int ci) { return sym_recv(blk(ci - 1), by, OUT_BYTES, pin); });
 }
 
 // Every rank's piece counters back to zero (the all-to-all's precondition: any rank may send to any
@@ -991,6 +1206,9 @@ int resync_pieces(zc_comm* c) {
     return rc;
   forget_signals(c->block + y.off_sready, c->block + y.off_err);
   c->ptx = c->prx = 0;
+  c->rtx = c->rrx = 0;
+  std::fill(c->p2p_tx.begin(), c->p2p_tx.end(), 0);
+  std::fill(c->p2p_rx.begin(), c->p2p_rx.end(), 0);
   return launch_mail(c, MAIL_BARRIER, nullptr, 0, 0.0);
 }
 
@@ -1008,8 +1226,8 @@ int enqueue_alltoall(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_
   if (int rc = resync_pieces(c)) return rc;
   for (int t = 1; t < n; ++t) {
     const int to = (r + t) % n, from = (r - t + n) % n;
-    if (int rc = staged_xfer(c, to, d_send + static_cast<uint64_t>(to) * block, by,
-                             d_recv + static_cast<uint64_t>(from) * block, by, c->cfg.pin, true))
+    if (int rc = staged_xfer(c, to, sym_send(d_send + static_cast<uint64_t>(to) * block, by, c->cfg.pin),
+                             sym_recv(d_recv + static_cast<uint64_t>(from) * block, by, OUT_BYTES, c->cfg.pin)))
       return rc;
   }
   return ZC_OK;
@@ -1017,24 +1235,42 @@ int enqueue_alltoall(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_
 
 // Broadcast along the ring from `root` (collectives.cpp:569-591): the root sends the message, the
 // last rank of the chain receives it, every rank in between stores each piece and forwards it
-// (store-and-forward per piece keeps the chain pipelined).  Forwarded frames are re-encoded from
-// the stored bytes, so every hop ships the frame the reference would.  Only ring edges carry
-// pieces, so the piece counters stay consistent for the ring collectives.
+// (store-and-forward per piece keeps the chain pipelined).  Forwarded frames are the received ones,
+// copied verbatim into the successor's relay lane: the frame the reference's re-encode would ship.
+// Only ring edges carry pieces, so the piece counters stay consistent for the ring collectives.
 int enqueue_broadcast(zc_comm* c, int32_t* d_data, uint64_t count, int root) {
   const int n = c->nranks;
   if (n == 1 || count == 0) return ZC_OK;
   const int pos = (c->rank - root + n) % n, next = (c->rank + 1) % n;
   const uint64_t by = count * 4;
   const int pin = c->cfg.pin;
-  if (pos == 0) return staged_xfer(c, next, d_data, by, nullptr, 0, pin, true);
-  if (pos == n - 1) return staged_xfer(c, next, nullptr, 0, d_data, by, pin, true);
-  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
-  for (uint64_t off = 0; off < by; off += pb) {
-    const uint64_t len = std::min(pb, by - off);
-    if (int rc = recv_piece(c, d_data + off / 4, len, true, pin)) return rc;
-    if (int rc = send_piece(c, next, d_data + off / 4, len, pin)) return rc;
+  const SendSpec none{nullptr, SRC_BYTES, 0, pin, nullptr};
+  if (pos == 0) return staged_xfer(c, next, sym_send(d_data, by, pin), RecvSpec{nullptr, 0, OUT_BYTES, nullptr, nullptr, false, false, pin});
+  if (!fuse_ring()) {
+    if (pos == n - 1) return staged_xfer(c, next, none, sym_recv(d_data, by, OUT_BYTES, pin));
+    const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
+    const RecvSpec rs = sym_recv(d_data, by, OUT_BYTES, pin);
+    const SendSpec sp = sym_send(d_data, by, pin);
+    for (uint64_t k = 0; k * pb < by; ++k) {
+      if (int rc = recv_piece(c, rs, k)) return rc;
+      if (int rc = send_piece(c, next, sp, k)) return rc;
+    }
+    return ZC_OK;
   }
-  return ZC_OK;
+  RecvSpec rs = sym_recv(d_data, by, OUT_BYTES, pin);
+  if (c->lay.nrelay == 0) {  // no relay lane (more than kMaxRelayRanks ranks): store and re-encode
+    const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
+    const SendSpec sp = sym_send(d_data, by, pin);
+    for (uint64_t k = 0; k * pb < by; ++k) {
+      if (int rc = recv_piece(c, rs, k)) return rc;
+      if (pos < n - 1)
+        if (int rc = send_piece(c, next, sp, k)) return rc;
+    }
+    return ZC_OK;
+  }
+  rs.relay = pos >= 2;
+  rs.fwd = pos < n - 1;
+  return relay_recv(c, rs);
 }
 
 int enqueue_meta(zc_comm* c, uint64_t count, int mode, double scale, uint32_t levels) {
@@ -1061,22 +1297,26 @@ int enqueue_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int mode, 
   return enqueue_ring(c, d_sym, count, true);
 }
 
+// The allreduce_eb symbol scratch, grown with the stream-ordered allocator (no device-wide sync).
 int ensure_sym(zc_comm* c, uint64_t count) {
   if (c->sym_cap >= count) return ZC_OK;
-  cudaStreamSynchronize(c->stream);
-  if (c->sym) cudaFree(c->sym);
+  if (c->sym) cudaFreeAsync(c->sym, c->stream);
   c->sym = nullptr;
   c->sym_cap = 0;
-  if (int rc = cuda_err(cudaMalloc(&c->sym, std::max<uint64_t>(count, 1) * 4), "malloc symbols")) return rc;
+  if (int rc = cuda_err(cudaMallocAsync(reinterpret_cast<void**>(&c->sym), std::max<uint64_t>(count, 1) * 4, c->stream),
+                        "malloc symbols"))
+    return rc;
   c->sym_cap = count;
   return ZC_OK;
 }
 
 int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64, uint64_t count, double rel) {
   if (int rc = ensure_sym(c, count)) return rc;
+  const int n = c->nranks, r = c->rank;
+  const bool fz = n > 1 && count > 0 && use_staged(c) && fuse_ring() && use_mz(c, max_chunk_units(c, count));
   Scal* s = c->scal();
   if (int rc = cuda_err(launch_absmax(d_x, SRC_F32, count, &s->absmax, c->err_word(), c->stream), "absmax")) return rc;
-  if (c->nranks > 1) {
+  if (n > 1) {
     count_ctrl_frames(c, 8);
     if (int rc = launch_mail(c, MAIL_EB_SCALE, nullptr, 1, rel)) return rc;
   } else {
@@ -1084,17 +1324,51 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
     set_scale_kernel<<<1, 1, 0, c->stream>>>(s, rel, 1);
   }
   const int g = sm_count(c->device) * 4;
-  note_launch();
-  quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
-  if (c->nranks > 1 && count > 0) {
+  if (n > 1 && count > 0) {
     // allreduce(q) with the shared scale: the meta ring still runs (and checks the counts)
     uint32_t rec[8] = {0};
     rec[0] = ZC_QUANT_ERROR_BOUNDED;
     rec[2] = static_cast<uint32_t>(count);
     rec[3] = static_cast<uint32_t>(count >> 32);
     count_ctrl_frames(c, 24);
-    if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
-    if (int rc = enqueue_ring(c, c->sym, count, true)) return rc;
+    if (!fz) {
+      note_launch();
+      quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
+      if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
+      if (int rc = enqueue_ring(c, c->sym, count, true)) return rc;
+    } else {
+      if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
+      // Fused: nothing is quantized or dequantized in a pass of its own.  RS step 0 encodes the
+      // rank's own chunk straight from fp32; every RS receive quantizes the local fp32 chunk into
+      // the sum (OUT_ADD_Q) and records the sums' range for the next send; AG receives dequantize
+      // into the output; only the chunk this rank reduced is dequantized from its symbols.
+      const Chunks ch{count, n};
+      const int fused_pin = count * 4 >= c->cfg.fused_codec_min_msg_bytes ? c->cfg.pin : ZC_PIN_RAW;
+      for (int t = 0; t < n - 1; ++t) {
+        uint32_t* mo = mz_buf(c, t);
+        if (int rc = cuda_err(cudaMemsetAsync(mo, 0, max_chunk_units(c, count) * 4, c->stream), "unit ranges")) return rc;
+        const int sc = r - t, rcv = r - t - 1;
+        const SendSpec sp = t == 0 ? SendSpec{d_x + ch.lo(sc), SRC_F32, ch.bytes(sc), fused_pin, nullptr}
+                                   : sym_send(c->sym + ch.lo(sc), ch.bytes(sc), fused_pin, mz_buf(c, t - 1));
+        const RecvSpec rs{c->sym + ch.lo(rcv), ch.bytes(rcv), OUT_ADD_Q, d_x + ch.lo(rcv), mo, false, false, fused_pin};
+        if (int rc = staged_xfer(c, (r + 1) % n, sp, rs)) return rc;
+      }
+      const int ok = OUT_F32 + (out_f64 ? 1 : 0);
+      const uint64_t esz = out_f64 ? 8 : 4;
+      if (int rc = allgather_hops(c, sym_send(c->sym + ch.lo(r + 1), ch.bytes(r + 1), c->cfg.pin, mz_buf(c, n - 2)),
+                                  [&](int ci) {
+                                    return RecvSpec{static_cast<uint8_t*>(d_out) + ch.lo(ci) * esz, ch.bytes(ci), ok,
+                                                    nullptr, nullptr, false, false, c->cfg.pin};
+                                  }))
+        return rc;
+      note_launch();
+      dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym + ch.lo(r + 1), ch.bytes(r + 1) / 4, s,
+                                                      static_cast<uint8_t*>(d_out) + ch.lo(r + 1) * esz, out_f64);
+      return cuda_err(cudaGetLastError(), "dequantize");
+    }
+  } else {
+    note_launch();
+    quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
   }
   note_launch();
   dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym, count, s, d_out, out_f64);
@@ -1258,9 +1532,14 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
     cudaFuncGetAttributes(&fa, piece_sent_kernel);
     cudaFuncGetAttributes(&fa, piece_done_kernel);
     cudaFuncGetAttributes(&fa, flag_store_kernel);
+    cudaFuncGetAttributes(&fa, forward_kernel);
     cudaGetLastError();
   }
   if (!rc) rc = cuda_err(cudaMalloc(&c->block, c->lay.total), "cudaMalloc block");
+  if (!rc && nranks > 1) {
+    rc = cuda_err(cudaMalloc(&c->mz, 2 * kMzUnits * 4), "cudaMalloc unit ranges");
+    if (!rc) c->mz_cap = kMzUnits;
+  }
   if (!rc) rc = cuda_err(cudaMemset(c->block + c->lay.off_ready, 0, c->lay.total - c->lay.off_ready), "memset");
   if (!rc) rc = cuda_err(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   if (!rc) {
@@ -1276,6 +1555,7 @@ int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg
   if (!rc) rc = zc_i_reserve_scratch(c->stream, runits);
   if (rc) {
     if (c->block) cudaFree(c->block);
+    if (c->mz) cudaFree(c->mz);
     delete c;
     return rc;
   }
@@ -1315,7 +1595,8 @@ void release_rank(zc_comm* c, uint32_t bit) {
 // Single-process group: every rank's collective is enqueued by its own host thread under the
 // baton (see baton_run), then each rank's stream is drained; on failure every rank is reset.
 template <typename F>
-int run_group(zc_comm* const* cs, int n, F enqueue) {
+int run_group_inner(zc_comm* const* cs, int n, F enqueue) {
+  InFlight inflight;
   std::vector<int> rcs;
   std::vector<std::string> msgs;
   baton_run(n, [&](int r) -> int {
@@ -1350,6 +1631,14 @@ int run_group(zc_comm* const* cs, int n, F enqueue) {
   return first;
 }
 
+template <typename F>
+int run_group(zc_comm* const* cs, int n, F enqueue) {
+  const int rc = run_group_inner(cs, n, enqueue);
+  flush_deferred_if_idle();
+  return rc;
+}
+
+
 int reset_state(zc_comm* c) {
   if (int rc = dev_guard(c)) return rc;
   if (std::getenv("ZC_DEBUG_NORESET")) return ZC_OK;  // keep the flag state for zc_comm_debug_state
@@ -1359,6 +1648,7 @@ int reset_state(zc_comm* c) {
   forget_signals(c->block + y.off_ready, c->block + y.off_wire);
   c->tx_seq = c->rx_seq = 0;
   c->ptx = c->prx = 0;
+  c->rtx = c->rrx = 0;
   std::fill(c->p2p_tx.begin(), c->p2p_tx.end(), 0);
   std::fill(c->p2p_rx.begin(), c->p2p_rx.end(), 0);
   c->epoch = 0;
@@ -1370,6 +1660,7 @@ int reset_state(zc_comm* c) {
 extern "C" {
 
 int zc_comm_create(int rank, int nranks, int device, const zc_collective_config* cfg, zc_comm** out) {
+  flush_deferred_if_idle();
   return alloc_comm(rank, nranks, device, cfg, out);
 }
 
@@ -1415,6 +1706,7 @@ int zc_comm_connect(zc_comm* c, const uint8_t* blobs) {
 }
 
 int zc_comm_create_group(int nranks, const int* devices, const zc_collective_config* cfg, zc_comm** out) {
+  flush_deferred_if_idle();
   std::vector<zc_comm*> cs(nranks, nullptr);
   for (int r = 0; r < nranks; ++r) {
     if (int rc = alloc_comm(r, nranks, devices[r], cfg, &cs[r])) {
@@ -1453,9 +1745,11 @@ void zc_comm_destroy(zc_comm* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int r = 0; r < c->nranks; ++r)
-    if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer[r]);
-  if (c->sym) cudaFree(c->sym);
-  if (c->block) cudaFree(c->block);
+    if (c->ipc_opened[r]) release_device_memory(c->device, c->peer[r], true);
+  if (c->sym) cudaFreeAsync(c->sym, c->stream);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  release_device_memory(c->device, c->mz, false);
+  release_device_memory(c->device, c->block, false);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->shared) zc_huff_ctx_destroy(c->shared);
@@ -1464,7 +1758,7 @@ void zc_comm_destroy(zc_comm* c) {
     cudaEventDestroy(t.e1);
     cudaEventDestroy(t.e2);
   }
-  if (c->tl_res) cudaFree(c->tl_res);
+  release_device_memory(c->device, c->tl_res, false);
   if (c->tl_t0) cudaEventDestroy(c->tl_t0);
   delete c;
 }
@@ -1487,6 +1781,7 @@ int zc_comm_set_shared_huffman(zc_comm* c, const zc_huff_ctx* ctx) {
 
 int zc_comm_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int32_t mode, double* h_scale, uint32_t levels,
                           void* stream) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
   if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
@@ -1498,6 +1793,7 @@ int zc_comm_allreduce_sym(zc_comm* c, int32_t* d_sym, uint64_t count, int32_t mo
 
 int zc_comm_allreduce_eb_f32(zc_comm* c, const float* d_x, void* d_out, int32_t out_f64, uint64_t count, double rel,
                              void* stream) {
+  InFlight inflight;
   if (!(rel > 0.0) || rel > 1.0) return set_err(ZC_ERR_INVALID_ARGUMENT, "eb_quantize: rel must be in (0, 1]");
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
@@ -1507,6 +1803,7 @@ int zc_comm_allreduce_eb_f32(zc_comm* c, const float* d_x, void* d_out, int32_t 
 }
 
 int zc_comm_reduce_scatter_sym(zc_comm* c, int32_t* d_sym, uint64_t count, void* stream) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
   if (c->nranks == 1 || count == 0) return ZC_OK;
@@ -1515,6 +1812,7 @@ int zc_comm_reduce_scatter_sym(zc_comm* c, int32_t* d_sym, uint64_t count, void*
 }
 
 int zc_comm_allgather_sym(zc_comm* c, int32_t* d_all, uint64_t block, void* stream) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
   if (c->nranks == 1 || block == 0) return ZC_OK;
@@ -1523,6 +1821,7 @@ int zc_comm_allgather_sym(zc_comm* c, int32_t* d_all, uint64_t block, void* stre
 }
 
 int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
+  InFlight inflight;
   (void)stream;  // host scalar in and out: nothing on the caller's stream to order after
   if (!std::isfinite(v)) return set_err(ZC_ERR_INVALID_ARGUMENT, "allreduce_max requires finite input");
   if (c->nranks == 1) {
@@ -1544,6 +1843,7 @@ int zc_comm_allreduce_max(zc_comm* c, double v, double* out, void* stream) {
 
 int zc_comm_allreduce_qsgd_f32(zc_comm* c, const float* d_x, void* d_out, int32_t out_f64, uint64_t count,
                                uint32_t levels, uint64_t seed, void* stream) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
   if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
@@ -1561,6 +1861,7 @@ int zc_comm_allreduce_qsgd_f32(zc_comm* c, const float* d_x, void* d_out, int32_
 }
 
 int zc_comm_alltoall_sym(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uint64_t block, void* stream) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   if (int rc = order_after(c, stream)) return rc;
   if (c->nranks > 1 && !c->connected) return set_err(ZC_ERR_LOGIC, "communicator not connected");
@@ -1569,6 +1870,7 @@ int zc_comm_alltoall_sym(zc_comm* c, const int32_t* d_send, int32_t* d_recv, uin
 }
 
 int zc_comm_broadcast_sym(zc_comm* c, int32_t* d_data, uint64_t count, int32_t root, void* stream) {
+  InFlight inflight;
   if (c->nranks == 1 || count == 0) return ZC_OK;
   if (root < 0 || root >= c->nranks) return set_err(ZC_ERR_INVALID_ARGUMENT, "broadcast root out of range");
   if (int rc = dev_guard(c)) return rc;
@@ -1579,6 +1881,7 @@ int zc_comm_broadcast_sym(zc_comm* c, int32_t* d_data, uint64_t count, int32_t r
 }
 
 int zc_comm_group_execute(zc_comm* c, zc_coll_request* reqs, int32_t nreqs, void* stream) {
+  InFlight inflight;
   if (nreqs < 0 || (nreqs > 0 && reqs == nullptr)) return set_err(ZC_ERR_INVALID_ARGUMENT, "bad request list");
   if (int rc = check_requests(c, reqs, nreqs)) return rc;
   if (int rc = dev_guard(c)) return rc;
@@ -1674,6 +1977,7 @@ int zc_comm_timeline_origin_delta(zc_comm* a, zc_comm* b, double* out) {
 }
 
 int zc_comm_sync(zc_comm* c) {
+  InFlight inflight;
   if (int rc = dev_guard(c)) return rc;
   return finish(c);
 }
@@ -1681,6 +1985,7 @@ int zc_comm_sync(zc_comm* c) {
 int zc_comm_reset(zc_comm* c) { return reset_state(c); }
 
 int zc_comm_send_encoded(zc_comm* c, int32_t peer, const void* d_raw, uint64_t raw_bytes, void* stream) {
+  InFlight inflight;
   if (peer < 0 || peer >= c->nranks || peer == c->rank) return set_err(ZC_ERR_INVALID_ARGUMENT, "send_encoded: bad peer");
   if (raw_bytes == 0) return ZC_OK;  // zero-length batches never reach the receiver (collectives.cpp:202)
   if (int rc = dev_guard(c)) return rc;
@@ -1691,6 +1996,7 @@ int zc_comm_send_encoded(zc_comm* c, int32_t peer, const void* d_raw, uint64_t r
 }
 
 int zc_comm_recv_decoded(zc_comm* c, int32_t peer, void* d_dst, uint64_t dst_bytes, void* stream) {
+  InFlight inflight;
   if (peer < 0 || peer >= c->nranks || peer == c->rank) return set_err(ZC_ERR_INVALID_ARGUMENT, "recv_decoded: bad peer");
   if (dst_bytes == 0) return ZC_OK;
   if (int rc = dev_guard(c)) return rc;

@@ -47,10 +47,11 @@ __device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameChec
   // reduction sink cannot be replayed after a partial add, so there the frame is reported corrupt.
   if (threadIdx.x == 0) {
     check_frame<false>(stage, unit_region(p, u), R, p.bare ? &p.hdr : nullptr, p.bare != 0, p.ctx, true, fc);
-    s_fail = ((f & 1u) == 0 || p.out_kind == OUT_ADD_I32) ? 1u : 0u;
+    s_fail = ((f & 1u) == 0 || is_add_sink(p.out_kind)) ? 1u : 0u;
   }
   __syncthreads();
-  Sink sink{p.out_kind, p.out, p.scale};
+  const double sc = dec_scale(p);
+  Sink sink{p.out_kind, p.out, sc, p.out_kind == OUT_ADD_Q ? 1.0 / sc : 0.0, p.acc_f32, 0u};
   if (!s_fail && fc.codec == ZC_CODEC_HUFFMAN) {
     const bool ok = load_huff_tables<false>(fc, payload, p.ctx, &s_t, &s_flag, s_lens);
     if (!ok) {
@@ -84,9 +85,9 @@ __device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameChec
       } else if (p.codec_out) {
         p.codec_out[u] = kFallback;
       }
-      if (p.out_kind == OUT_ADD_I32) err |= ZC_DERR_CORRUPT;
+      if (is_add_sink(p.out_kind)) err |= ZC_DERR_CORRUPT;
     }
-    if (!p.bare && p.out_kind != OUT_ADD_I32) {
+    if (!p.bare && !is_add_sink(p.out_kind)) {
       const uint64_t have = fc.region > kHeaderBytes ? fc.region - kHeaderBytes : 0;
       const uint64_t lim = R < have ? R : have;
       for (uint64_t v = threadIdx.x; v * 16 < lim; v += DT) {
@@ -137,9 +138,14 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
   }
   if (fc.codec == kFallback && p.bare) return;
   if (p.fast && (fc.codec == ZC_CODEC_RAW || fc.codec == ZC_CODEC_FIXEDLEN)) return;  // zc_fixed.cu decoded it
-  Sink sink{p.out_kind, p.out, p.scale};
+  const double sc = dec_scale(p);
+  Sink sink{p.out_kind, p.out, sc, p.out_kind == OUT_ADD_Q ? 1.0 / sc : 0.0, p.acc_f32, 0u};
   const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
   uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
+  if (p.maxzz_out != nullptr && is_add_sink(p.out_kind)) {  // the sums' range, for the next send
+    const uint32_t m = __reduce_max_sync(FULL, sink.mz);
+    if (lane == 0 && m) atomicMax(p.maxzz_out + u, m);
+  }
   f = __reduce_or_sync(FULL, f);
   if (lane == 0 && f) atomicOr(&p.flags[u], f);
   err = __reduce_or_sync(FULL, err);

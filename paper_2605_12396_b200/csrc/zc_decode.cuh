@@ -60,8 +60,12 @@ __device__ __forceinline__ double i2d(uint32_t s) {
 struct Sink {
   int kind;      // OutKind
   void* out;     // base of the whole message (raw byte offsets index it)
-  double scale;  // dequantization factor
+  double scale;  // dequantization factor; OUT_ADD_Q: the quantizer's bin width
+  double rcp;    // OUT_ADD_Q: 1 / scale
+  const float* acc;  // OUT_ADD_Q: the local fp32 chunk (indexed like `out`)
+  mutable uint32_t mz;  // OUT_ADD_*: running max zig-zag of the sums this thread wrote
 };
+__host__ __device__ __forceinline__ bool is_add_sink(int kind) { return kind == OUT_ADD_I32 || kind == OUT_ADD_Q; }
 
 // Writes 4 decoded symbol words (16 raw bytes; nb valid) at raw byte offset `ob` of the output.
 __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_t w[4], uint32_t nb, uint32_t& err) {
@@ -95,6 +99,21 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
       }
       break;
     }
+    case OUT_ADD_Q: {  // allreduce_eb's RS sink: q(local fp32) + decoded, int64-checked
+      int32_t* o = static_cast<int32_t*>(k.out) + ob / 4;
+      const float* x = k.acc + ob / 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (static_cast<uint32_t>(i) < nb / 4) {
+          const int32_t q = quantize_one(static_cast<double>(x[i]), k.scale, k.rcp, err);
+          const long long s = static_cast<long long>(q) + static_cast<int32_t>(w[i]);
+          if (s != static_cast<int32_t>(s)) err |= ZC_DERR_OVERFLOW;
+          o[i] = static_cast<int32_t>(s);
+          k.mz = max(k.mz, zigzag32(static_cast<int32_t>(s)));
+        }
+      }
+      break;
+    }
     case OUT_ADD_I32: {
       int32_t* o = static_cast<int32_t*>(k.out) + ob / 4;
       if (nb == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
@@ -108,6 +127,8 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
         if (ovf) err |= ZC_DERR_OVERFLOW;
         *reinterpret_cast<int4*>(o) = make_int4(static_cast<int32_t>(s0), static_cast<int32_t>(s1),
                                                 static_cast<int32_t>(s2), static_cast<int32_t>(s3));
+        k.mz = max(k.mz, max(max(zigzag32(static_cast<int32_t>(s0)), zigzag32(static_cast<int32_t>(s1))),
+                             max(zigzag32(static_cast<int32_t>(s2)), zigzag32(static_cast<int32_t>(s3)))));
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -115,6 +136,7 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
             long long s = static_cast<long long>(o[i]) + static_cast<int32_t>(w[i]);
             if (s != static_cast<int32_t>(s)) err |= ZC_DERR_OVERFLOW;
             o[i] = static_cast<int32_t>(s);
+            k.mz = max(k.mz, zigzag32(static_cast<int32_t>(s)));
           }
         }
       }

@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
           if (gbad) {
             err |= ZC_DERR_NONFINITE;
           } else {
-            const int32_t smax = quantize_one(gmx, p.scale, p.rcp, err);
-            const int32_t smin = quantize_one(gmn, p.scale, p.rcp, err);
+            const int32_t smax = quantize_one(gmx, enc_scale(p), enc_rcp(p), err);
+            const int32_t smin = quantize_one(gmn, enc_scale(p), enc_rcp(p), err);
             maxzz = max(zigzag32(smax), zigzag32(smin));
           }
         }
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(NT, 1) encode_kernel(const EncParams p) {
       if (go) {
         if (tid == 0) check_frame<true>(rx_stage, rlen, rR, nullptr, false, p.ctx, true, s_fc);
         __syncthreads();
-        Sink sink{p.rx_store ? OUT_BYTES : OUT_ADD_I32, p.rx_dst, 1.0};
+        Sink sink{p.rx_store ? OUT_BYTES : OUT_ADD_I32, p.rx_dst, 1.0, 0.0, nullptr, 0u};
         uint32_t f = decode_slice<true, 2>(s_fc, rx_stage + kHeaderBytes, rR, r0, r1, sink, uoff,
                                         reinterpret_cast<const uint32_t*>(rx_stage + p.L.idx_off), p.ctx, &s_x.dec.t,
                                         &s_flag, s_lens, s_x.dec.words, err);

@@ -135,7 +135,7 @@ __device__ __forceinline__ void load_vec(const EncParams& p, uint64_t uoff, uint
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       w[k] = (static_cast<uint32_t>(k) < nb / 4)
-                 ? static_cast<uint32_t>(quantize_one(static_cast<double>(f[k]), p.scale, p.rcp, err))
+                 ? static_cast<uint32_t>(quantize_one(static_cast<double>(f[k]), enc_scale(p), enc_rcp(p), err))
                  : 0u;
   } else {
     const double* s = static_cast<const double*>(p.src) + (uoff + b0) / 4;
@@ -154,7 +154,7 @@ __device__ __forceinline__ void load_vec(const EncParams& p, uint64_t uoff, uint
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      w[k] = (static_cast<uint32_t>(k) < nb / 4) ? static_cast<uint32_t>(quantize_one(f[k], p.scale, p.rcp, err)) : 0u;
+      w[k] = (static_cast<uint32_t>(k) < nb / 4) ? static_cast<uint32_t>(quantize_one(f[k], enc_scale(p), enc_rcp(p), err)) : 0u;
   }
 }
 
@@ -236,7 +236,7 @@ __device__ __forceinline__ void to_words(const EncParams& p, const RawVec& rv, u
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       w[k] = static_cast<uint32_t>(k) < rv.nb / 4
-                 ? static_cast<uint32_t>(quantize_one(element<SRC>(rv, k), p.scale, p.rcp, err))
+                 ? static_cast<uint32_t>(quantize_one(element<SRC>(rv, k), enc_scale(p), enc_rcp(p), err))
                  : 0u;
   }
 }
@@ -290,10 +290,10 @@ __device__ __forceinline__ void words_full(const EncParams& p, const RawVec& rv,
   } else {
     bool slow = false;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] = static_cast<uint32_t>(quantize_fast(element<SRC>(rv, k), p.rcp, slow));
+    for (int k = 0; k < 4; ++k) w[k] = static_cast<uint32_t>(quantize_fast(element<SRC>(rv, k), enc_rcp(p), slow));
     if (slow) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) w[k] = static_cast<uint32_t>(quantize_one(element<SRC>(rv, k), p.scale, p.rcp, err));
+      for (int k = 0; k < 4; ++k) w[k] = static_cast<uint32_t>(quantize_one(element<SRC>(rv, k), enc_scale(p), enc_rcp(p), err));
     }
   }
 }

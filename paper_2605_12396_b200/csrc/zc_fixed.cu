@@ -101,7 +101,7 @@ __device__ __forceinline__ void window_profile(const EncParams& p, BUnit& U, uin
         a.z = nb > 8 ? __ldg(fs + 2) : 0.f;
       }
       if (SRC == SRC_F32) {
-        quantize4(a, p.scale, p.rcp, w, err);
+        quantize4(a, enc_scale(p), enc_rcp(p), w, err);
       } else {  // symbols already
         w[0] = __float_as_uint(a.x);
         w[1] = __float_as_uint(a.y);
@@ -183,8 +183,11 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
   __shared__ uint32_t s_task;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool automode = p.pin == ZC_PIN_AUTO;
-  const uint32_t nprof = (automode || g.spec) ? p.nunits : 0u;
-  const uint64_t nchunks = g.spec ? 0 : (g.total + RCH - 1) / RCH;
+  // symbols whose per-unit max zig-zag the producer already knows (the ring's reduce sink): no
+  // slice is read; one task per unit profiles the window (Auto) and decides
+  const bool pre = SRC != SRC_F32 && p.maxzz_in != nullptr;
+  const uint32_t nprof = (automode || g.spec || pre) ? p.nunits : 0u;
+  const uint64_t nchunks = (g.spec || pre) ? 0 : (g.total + RCH - 1) / RCH;
   BGlobal* gl = bglobal(us, p.nunits);
   uint32_t err = 0;
   float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
       const uint64_t R = unit_R(p, u);
       if (R <= p.cfg.small_batch_threshold_bytes || p.stage_len <= kHeaderBytes) {
         if (tid == 0) us[u].plan = ZC_CODEC_RAW;
-      } else {
+      } else if (automode || g.spec) {
         const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(p.src) + static_cast<uint64_t>(u) * (p.unit_bytes / 4));
         window_profile<SRC>(p, us[u], u, src, R, ctx_ok, s_prof, err);
       }
@@ -254,6 +257,9 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
         if (g.spec) {  // the emit decides; here only the plan census and the width guess
           BUnit& U = us[u];
           if (automode && U.plan == ZC_CODEC_HUFFMAN) atomicAdd(&gl->n_huff, 1u);
+        } else if (pre) {  // the unit's range is known: complete it at once
+          atomicMax(&us[u].maxzz, __ldcg(p.maxzz_in + u));
+          finish(us[u], u, unit_slices(p, u) + (automode ? 1u : 0u));
         } else {
           finish(us[u], u, 1u);
         }
@@ -571,7 +577,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   uint32_t k = 0, cur_u = 0xffffffffu;
   UnitView v;
   uint8_t* payload = nullptr;
-  const double scale = p.scale, rcp = p.rcp;
+  const double scale = enc_scale(p), rcp = enc_rcp(p);
   const float xlim = fast_xlim(scale);
   uint64_t c_first = gw;
   {  // the processing sequence restarts from the first tile (its own unit cache)
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       uint32_t s[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        s[i] = e0 + i < n ? (SRC == SRC_F32 ? quantize_exact(__ldg(src + e0 + i), p.scale, p.rcp, &err)
+        s[i] = e0 + i < n ? (SRC == SRC_F32 ? quantize_exact(__ldg(src + e0 + i), enc_scale(p), enc_rcp(p), &err)
                                             : __float_as_uint(__ldg(src + e0 + i)))
                           : 0u;
       if (kMode == 1 && v.spec) {  // the partial tile's max zig-zag (its valid elements only)
@@ -724,7 +730,8 @@ __device__ __forceinline__ int32_t row_symbol(const uint32_t (&a)[W], int i) {
 
 // One tile in shared memory: packed rows in, swizzled fp32 tile out (same buffer).
 template <int W, bool kRaw, int OUT>
-__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, const int32_t* acc, int lane, uint32_t& err) {
+__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, double rcp, const void* accp, int lane,
+                                                 uint32_t& mz, uint32_t& err) {
   uint32_t a[W];
   const uint32_t row = buf + lane * W * 4;
   if (W % 4 == 0) {
@@ -746,17 +753,25 @@ __device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, con
   for (int m = 0; m < 8; ++m) {
     uint32_t o[4];
     int4 add = make_int4(0, 0, 0, 0);
-    if (OUT == OUT_ADD_I32) add = __ldcg(reinterpret_cast<const int4*>(acc + lane * 32) + m);
+    if (OUT == OUT_ADD_I32) add = __ldcg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(accp) + lane * 32) + m);
+    if (OUT == OUT_ADD_Q) {  // the local fp32 chunk, quantized on the fly (quant.cpp:22-27)
+      const float4 xf = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(accp) + lane * 32) + m);
+      add = make_int4(quantize_one(static_cast<double>(xf.x), scale, rcp, err),
+                      quantize_one(static_cast<double>(xf.y), scale, rcp, err),
+                      quantize_one(static_cast<double>(xf.z), scale, rcp, err),
+                      quantize_one(static_cast<double>(xf.w), scale, rcp, err));
+    }
     const int32_t ad[4] = {add.x, add.y, add.z, add.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int32_t sym = row_symbol<W, kRaw>(a, 4 * m + q);
       if (OUT == OUT_F32) {
         o[q] = __float_as_uint(__double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym)))));
-      } else if (OUT == OUT_ADD_I32) {  // RS sink: int64 sum range-checked to int32 (collectives.cpp:480-491)
+      } else if (OUT == OUT_ADD_I32 || OUT == OUT_ADD_Q) {  // RS sink: int64 sum range-checked (collectives.cpp:480-491)
         const long long sum = static_cast<long long>(ad[q]) + sym;
         if (sum != static_cast<int32_t>(sum)) err |= ZC_DERR_OVERFLOW;
         o[q] = static_cast<uint32_t>(static_cast<int32_t>(sum));
+        mz = max(mz, zigzag32(static_cast<int32_t>(o[q])));
       } else {
         o[q] = static_cast<uint32_t>(sym);
       }
@@ -768,16 +783,16 @@ __device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, con
 }
 
 template <int OUT>
-__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, const int32_t* acc,
-                                                     int lane, uint32_t& err) {
+__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, double rcp,
+                                                     const void* acc, int lane, uint32_t& mz, uint32_t& err) {
   if (v.codec == ZC_CODEC_RAW) {
-    decode_tile_smem<32, true, OUT>(buf, scale, acc, lane, err);
+    decode_tile_smem<32, true, OUT>(buf, scale, rcp, acc, lane, mz, err);
     return;
   }
   switch (v.width) {
-#define ZC_DC(W)                                                   \
-  case W:                                                          \
-    decode_tile_smem<W, false, OUT>(buf, scale, acc, lane, err); \
+#define ZC_DC(W)                                                               \
+  case W:                                                                      \
+    decode_tile_smem<W, false, OUT>(buf, scale, rcp, acc, lane, mz, err); \
     break;
     ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
     ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
@@ -828,8 +843,15 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   uint8_t* my = s_tiles + static_cast<size_t>(warp) * DSTAGES * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(DT_WARPS) * DSTAGES * TILE_BYTES) + warp * DSTAGES;
   uint8_t* views = reinterpret_cast<uint8_t*>(bars + DT_WARPS * DSTAGES - warp * DSTAGES);
-  const double scale = p.scale;
-  uint32_t err = 0;
+  const double scale = dec_scale(p), rcp = OUT == OUT_ADD_Q ? 1.0 / scale : 0.0;
+  uint32_t err = 0, mz = 0, mz_u = 0xffffffffu;
+  // the sums' max zig-zag per unit (the next send's FixedLen width without a range pass)
+  auto mz_flush = [&]() {
+    if (OUT != OUT_ADD_I32 && OUT != OUT_ADD_Q) return;
+    const uint32_t m = __reduce_max_sync(FULL, mz);
+    if (lane == 0 && p.maxzz_out != nullptr && mz_u != 0xffffffffu && m) atomicMax(p.maxzz_out + mz_u, m);
+    mz = 0;
+  };
   // every unit's view (recv_batch's dispatch result), once per CTA; the decoded codec per owned unit
   for (uint32_t u = tid; u < p.nunits && u < DEC_VIEWS; u += DT) {
     const DecView v = dec_view(p, u);
@@ -880,8 +902,14 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     }
     tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
     const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
-    const int32_t* acc = OUT == OUT_ADD_I32 ? static_cast<const int32_t*>(p.out) + c * TILE_ELEMS : nullptr;
-    decode_tile_dispatch<OUT>(prc.cv, buf, scale, acc, lane, err);
+    const void* acc = OUT == OUT_ADD_I32 ? static_cast<const void*>(static_cast<const int32_t*>(p.out) + c * TILE_ELEMS)
+                      : OUT == OUT_ADD_Q ? static_cast<const void*>(p.acc_f32 + c * TILE_ELEMS)
+                                         : nullptr;
+    if (static_cast<uint32_t>(c >> ush) != mz_u) {
+      mz_flush();
+      mz_u = static_cast<uint32_t>(c >> ush);
+    }
+    decode_tile_dispatch<OUT>(prc.cv, buf, scale, rcp, acc, lane, mz, err);
     tma::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -893,6 +921,10 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
     const uint32_t u = static_cast<uint32_t>(nfull >> ush);
     const DecView v = dec_view(p, u);
+    if (u != mz_u) {
+      mz_flush();
+      mz_u = u;
+    }
     if (v.codec != kFallback) {
       const uint64_t off = static_cast<uint64_t>(u) * p.unit_bytes;
       const uint64_t n = ((p.total_bytes - off) < p.unit_bytes ? (p.total_bytes - off) : p.unit_bytes) / 4;
@@ -912,18 +944,21 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
           sym = unzigzag32(z);
         }
         if (OUT == OUT_F32) {
-          out[e] = __double2float_rn(__dmul_rn(p.scale, i2d(static_cast<uint32_t>(sym))));
-        } else if (OUT == OUT_ADD_I32) {
+          out[e] = __double2float_rn(__dmul_rn(scale, i2d(static_cast<uint32_t>(sym))));
+        } else if (OUT == OUT_ADD_I32 || OUT == OUT_ADD_Q) {
           int32_t* o = reinterpret_cast<int32_t*>(out) + e;
-          const long long sum = static_cast<long long>(*o) + sym;
+          const int32_t a = OUT == OUT_ADD_I32 ? *o : quantize_one(static_cast<double>(p.acc_f32[off / 4 + e]), scale, rcp, err);
+          const long long sum = static_cast<long long>(a) + sym;
           if (sum != static_cast<int32_t>(sum)) err |= ZC_DERR_OVERFLOW;
           *o = static_cast<int32_t>(sum);
+          mz = max(mz, zigzag32(static_cast<int32_t>(sum)));
         } else {
           reinterpret_cast<int32_t*>(out)[e] = sym;
         }
       }
     }
   }
+  mz_flush();
   if (lane == 0) tma::bulk_wait<0>();
   __syncwarp();
   err = __reduce_or_sync(FULL, err);
@@ -974,7 +1009,7 @@ cudaError_t launch_fixed_range_m(const EncParams& p, void* scratch, uint64_t tot
   g.fast = 1;
   g.spec = mode == 1 ? 1u : 0u;
   note_launch();
-  const uint64_t tasks = mode == 1 ? p.nunits : total_slices + p.nunits;
+  const uint64_t tasks = (mode == 1 || (p.src_kind != SRC_F32 && p.maxzz_in != nullptr)) ? p.nunits : total_slices + p.nunits;
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(tasks, 2ull * sms)));
   if (p.src_kind == SRC_F32)
     range_kernel<SRC_F32><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
@@ -1035,7 +1070,8 @@ cudaError_t launch_fixed_emit(const EncParams& p, void* scratch, uint64_t total_
 }
 
 bool fixed_decode_ok(const DecParams& p) {
-  return !p.bare && (p.out_kind == OUT_F32 || p.out_kind == OUT_ADD_I32 || p.out_kind == OUT_BYTES) &&
+  return !p.bare && (p.out_kind == OUT_F32 || p.out_kind == OUT_ADD_I32 || p.out_kind == OUT_ADD_Q || p.out_kind == OUT_BYTES) &&
+         (p.out_kind != OUT_ADD_Q || (reinterpret_cast<uintptr_t>(p.acc_f32) & 15u) == 0) &&
          tiled_unit(p.unit_bytes) && (p.total_bytes % 4) == 0 &&
          (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0 && (p.stride % 16) == 0 &&
          (reinterpret_cast<uintptr_t>(p.stages) & 15u) == 0;
@@ -1047,6 +1083,7 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(fl_decode_kernel<OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
     cudaFuncSetAttribute(fl_decode_kernel<OUT_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
     cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+    cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1067,6 +1104,8 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
     fl_decode_kernel<OUT_F32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
   else if (p.out_kind == OUT_ADD_I32)
     fl_decode_kernel<OUT_ADD_I32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+  else if (p.out_kind == OUT_ADD_Q)
+    fl_decode_kernel<OUT_ADD_Q><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
   else
     fl_decode_kernel<OUT_BYTES><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
   return cudaGetLastError();
@@ -1081,6 +1120,7 @@ void preload_fixed_kernels() {
   cudaFuncSetAttribute(fl_decode_kernel<OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
   cudaFuncSetAttribute(fl_decode_kernel<OUT_BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
   cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
+  cudaFuncSetAttribute(fl_decode_kernel<OUT_ADD_Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(DEC_SMEM));
   cudaGetLastError();
 }
 

@@ -10,7 +10,9 @@
 namespace zc {
 
 enum SrcKind : int { SRC_BYTES = 0, SRC_F32 = 1, SRC_F64 = 2 };
-enum OutKind : int { OUT_BYTES = 0, OUT_F32 = 1, OUT_F64 = 2, OUT_ADD_I32 = 3 };
+// OUT_ADD_Q: the reduce-scatter sink of allreduce_eb — the local fp32 chunk (DecParams::acc_f32) is
+// quantized on the fly and added to the decoded symbols; the int32 sum goes to `out`.
+enum OutKind : int { OUT_BYTES = 0, OUT_F32 = 1, OUT_F64 = 2, OUT_ADD_I32 = 3, OUT_ADD_Q = 4 };
 
 // Encode modes.
 enum EncMode : int {
@@ -54,6 +56,8 @@ struct EncParams {
   int pin;
   int embed;           // bare huffman: prepend codebook
   double scale, rcp;   // float sources
+  const double* dscale;  // or, when set, {scale, 1/scale} in device memory (allreduce_eb's agreed scale)
+  const uint32_t* maxzz_in;  // SRC_BYTES: each unit's max zig-zag, known from the producer (or null)
   uint64_t total_bytes;
   uint64_t unit_bytes;
   uint32_t nunits;
@@ -94,6 +98,9 @@ struct DecParams {
   int out_kind;
   void* out;
   double scale;            // dequantization factor for OUT_F32 / OUT_F64
+  const double* dscale;    // or, when set, {scale, 1/scale} in device memory
+  const float* acc_f32;    // OUT_ADD_Q: the local fp32 chunk quantized into the sums
+  uint32_t* maxzz_out;     // OUT_ADD_*: per unit, atomicMax of the sums' zig-zag (or null)
   const DevHuff* ctx;
   const uint32_t* index;   // may be null
   uint64_t index_stride;
@@ -107,6 +114,12 @@ struct DecParams {
   int own_frames;          // the frames come from this library's batched encoder without a Huffman
                            // context: all valid FixedLen / RAW, so the general kernels are skipped
 };
+
+// Quantizer bin width of a float source / dequantization factor: the host value, or the device
+// pair {scale, 1/scale} (allreduce_eb: agreed on the device, never seen by the host).
+__device__ __forceinline__ double enc_scale(const EncParams& p) { return p.dscale ? p.dscale[0] : p.scale; }
+__device__ __forceinline__ double enc_rcp(const EncParams& p) { return p.dscale ? p.dscale[1] : p.rcp; }
+__device__ __forceinline__ double dec_scale(const DecParams& p) { return p.dscale ? p.dscale[0] : p.scale; }
 
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
 // can state how many of OUR kernels a region launched.

@@ -75,6 +75,7 @@ def lib():
     _sig(L, "zc_memcpy", C.c_int, vp, vp, u64)
     _sig(L, "zc_memset", C.c_int, vp, C.c_int, u64)
     _sig(L, "zc_stream_synchronize", C.c_int, vp)
+    _sig(L, "zc_flush_deferred", None)
     _sig(L, "zc_default_arb_config", None, P(abi.ArbConfig))
     _sig(L, "zc_default_transport_hint", None, P(abi.TransportHint))
     _sig(L, "zc_default_collective_config", None, P(abi.CollectiveConfig))
@@ -665,6 +666,7 @@ class Group:
             x.start()
         for x in th:
             x.join()
+        lib().zc_flush_deferred()  # frees queued while the rank threads were in collectives
         failed = [e for e in errs if e is not None]
         if failed:
             for r in range(n):

@@ -8,6 +8,10 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# A protocol bug must fail a test quickly rather than sit out the 20 s default per rank.
+os.environ.setdefault("ZC_COMM_TIMEOUT_MS", "8000")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running")

@@ -361,3 +361,32 @@ def test_allgather_and_broadcast_per_slot_framing(zc, port, ref, n):
     g.broadcast(ds, 1)
     for d in ds:
         assert np.array_equal(npy(d), data)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_HUFFMAN])
+def test_fused_ring_equals_unfused(zc, port, n, pin, monkeypatch):
+    """The fused ring (fp32 quantized inside the first RS send and the RS sinks, sums' range handed
+    to the next send, AG frames forwarded verbatim, dequantized inside the AG sinks) produces the
+    same outputs and WireStats as the unfused ring (quantize -> re-encoding hops -> dequantize),
+    and both equal the serial oracle."""
+    count = (11 << 20) // 4 + 5 * n + 1
+    rng = np.random.default_rng(70 + n + pin)
+    xs = [rng.laplace(0, 1e-2 * (r + 1), count).astype(np.float32) for r in range(n)]
+    gmax = max(float(np.abs(x).max()) for x in xs)
+    rel = 1e-4 / gmax
+    scale, syms, exp = _serial_eb(port, xs, rel)
+    outs, wires = [], []
+    for unfused in (False, True):
+        if unfused:
+            monkeypatch.setenv("ZC_RING_UNFUSED", "1")
+        g = zc.Group(n, cfg=zc.collective_config(pin))
+        g.set_shared_huffman_from_bytes(syms[0].view(np.uint8)[: 1 << 20])
+        o = g.allreduce_eb([t(x) for x in xs], rel, torch.float64)
+        outs.append([npy(v) for v in o])
+        wires.append(g.wire_stats())
+    for o in outs[0] + outs[1]:
+        assert np.array_equal(o.view(np.uint64), exp.view(np.uint64))
+    a, b = wires
+    assert list(a.frames_by_codec) == list(b.frames_by_codec)
+    assert (a.raw_bytes, a.payload_bytes, a.total_bytes) == (b.raw_bytes, b.payload_bytes, b.total_bytes)
