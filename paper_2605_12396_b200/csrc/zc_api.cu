@@ -696,6 +696,7 @@ __attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, i
   p.nunits = static_cast<uint32_t>((total + unit_bytes - 1) / unit_bytes);
   p.dscale = o ? o->dscale : nullptr;
   p.maxzz_in = o ? o->maxzz_in : nullptr;
+  p.no_spec = o ? o->no_spec : 0;
   p.stages = d_stages;
   p.stride = stride;
   p.stage_len = stage_len;

@@ -31,6 +31,7 @@ struct zc_i_batch_opts {
   const uint32_t* maxzz_in;   // encode of symbols: per-unit max zig-zag already known
   const float* acc_f32;       // decode OUT_ADD_Q: the local fp32 chunk
   uint32_t* maxzz_out;        // decode OUT_ADD_*: per-unit max zig-zag of the sums (atomicMax)
+  int no_spec;                // encode fp32: no speculative width (two reads of the input)
 };
 extern "C" {
 int zc_i_reserve_scratch(void* stream, uint32_t nunits);

@@ -47,8 +47,20 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
   const uint64_t R = unit_R(p, u);
   const uint64_t uoff = static_cast<uint64_t>(u) * p.unit_bytes;
   const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
+  // symbols whose per-unit max zig-zag the ring's reduce sink recorded: decided here, no range pass
+  auto decide_known = [&](uint32_t& e) {
+    if (SRC == SRC_BYTES && p.maxzz_in != nullptr) {
+      U.maxzz = __ldcg(p.maxzz_in + u);
+      if (target_codec(p, U, ctx_ok) == ZC_CODEC_FIXEDLEN) decide_unit<SRC>(p, U, u, true, true, e);
+    }
+  };
   if (R <= p.cfg.small_batch_threshold_bytes || p.stage_len <= kHeaderBytes) {
-    if (part == 0 && tid == 0) U.plan = ZC_CODEC_RAW;
+    if (part == 0 && tid == 0) {
+      U.plan = ZC_CODEC_RAW;
+      uint32_t e = 0;
+      decide_known(e);
+      if (e && p.err) atomicOr(p.err, e);
+    }
     return;
   }
   for (int i = tid; i < 256; i += PT) {
@@ -137,6 +149,7 @@ __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* u
       }
       U.plan = arbitrate_plan(R, pcap, st, p.hint, ctx_ok, p.cfg).choice;
       if (U.plan == ZC_CODEC_HUFFMAN) atomicAdd(&bglobal(us, p.nunits)->n_huff, 1u);
+      decide_known(err);
     }
   }
   err = __reduce_or_sync(FULL, err);
@@ -1001,7 +1014,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaMemsetAsync(scratch, 0, sizeof(BUnit) * p.nunits + sizeof(BGlobal), s);
   BUnit* us = static_cast<BUnit*>(scratch);
-  BGeom g;
+  BGeom g{};
   g.s_full = static_cast<uint32_t>((p.unit_bytes + BS - 1) / BS);
   const uint64_t last_R = p.total_bytes - static_cast<uint64_t>(p.nunits - 1) * p.unit_bytes;
   g.total = static_cast<uint64_t>(p.nunits - 1) * g.s_full + (last_R + BS - 1) / BS;
@@ -1011,7 +1024,7 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   // that hold any FixedLen payload of a unit (<= the unit's raw bytes); smaller stages take the
   // two-read path, whose decision (capacity check included) precedes every store.
   g.spec = (g.fast && SRC == SRC_F32 && (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) &&
-            p.stage_len >= kHeaderBytes + p.unit_bytes && std::getenv("ZC_NO_SPEC") == nullptr) ? 1u : 0u;
+            p.stage_len >= kHeaderBytes + p.unit_bytes && !p.no_spec && std::getenv("ZC_NO_SPEC") == nullptr) ? 1u : 0u;
   const int fmode = g.spec ? 1 : 0;
   if (p.pin == ZC_PIN_AUTO && !g.fast) {
     note_launch();
@@ -1022,10 +1035,18 @@ cudaError_t launch_batch_t(const EncParams& p, void* scratch, cudaStream_t s) {
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(sms)));
   if (g.fast) {
     // the range kernel also profiles the window and plans (Auto): no separate profile launch
-    if (g.spec) {  // window profiles (plan, width guess) only: the emit reads the input once
+    if (g.spec || (SRC == SRC_BYTES && p.maxzz_in != nullptr && (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN))) {
+      // window profiles only: the plan and the width guess (speculative fp32), or the plan and the
+      // decision from the ranges the ring's reduce sink recorded
       note_launch();
       profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
-    } else if (p.pin == ZC_PIN_AUTO || p.pin == ZC_PIN_FIXEDLEN) {
+    } else if (p.pin == ZC_PIN_AUTO) {
+      // the plans first (8 CTAs per window), then one HBM stream over the FixedLen-planned units
+      // only (a window profile as a single task of the range kernel is its critical path)
+      note_launch();
+      profile_kernel<SRC><<<p.nunits * PC, PT, 0, s>>>(p, us);
+      if (cudaError_t e = launch_fixed_range_m(p, scratch, g.total, g.s_full, sms, 3, s)) return e;
+    } else if (p.pin == ZC_PIN_FIXEDLEN) {
       if (cudaError_t e = launch_fixed_range_m(p, scratch, g.total, g.s_full, sms, fmode, s)) return e;
     }
     const bool fused = huff_possible && p.index != nullptr;  // one launch for the whole Huffman side

@@ -51,6 +51,7 @@ struct BGeom {
   uint64_t total;   // slices in the message
   uint32_t fast;    // zc_fixed.cu handles the FixedLen / RAW units (range + emit)
   uint32_t spec;    // speculative FixedLen: range pass = window profiles only, emit packs with the window's width
+  uint32_t planned;  // Auto: profile_kernel already profiled every window and stored the plans
   __device__ __forceinline__ void unit_of(uint64_t t, uint32_t nunits, uint32_t& u, uint32_t& s) const {
     const uint64_t head = static_cast<uint64_t>(nunits - 1) * s_full;
     if (t < head) {

@@ -878,6 +878,10 @@ int send_piece(zc_comm* c, int to, const SendSpec& sp, uint64_t k) {
   o.unit_bytes = y.ub;
   o.dscale = sp.kind == SRC_F32 ? &c->scal()->scale : nullptr;
   o.maxzz_in = sp.mz_in ? sp.mz_in + k * y.runits : nullptr;
+  // the ring's fp32 sends (allreduce_eb's first RS step) read their input twice rather than guess
+  // the width from a 64 KiB window: gradients are heavy-tailed (Laplacian), so the window's width
+  // is often one bit short of the batch's and the guess would cost a redo pass (measured).
+  o.no_spec = sp.kind == SRC_F32 && std::getenv("ZC_RING_SPEC") == nullptr;
   if (int rc = zc_i_encode_batches(static_cast<const uint8_t*>(sp.src) + off, sp.kind, bytes, 1.0, &o, dst, y.fstride,
                                    ZC_STAGE_BANK_BYTES, sp.pin, &c->cfg.hint, c->shared, &c->cfg.arb, res,
                                    reinterpret_cast<uint32_t*>(dst + y.reg_idx), c->err_word(), c->stream))

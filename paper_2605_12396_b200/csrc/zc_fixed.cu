@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(RT, 2) range_kernel(const __grid_constant__ En
   __shared__ ProfSmem s_prof;
   __shared__ uint32_t s_task;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
-  const bool automode = p.pin == ZC_PIN_AUTO;
+  const bool automode = p.pin == ZC_PIN_AUTO && !g.planned;  // window profiles are this kernel's tasks
   // symbols whose per-unit max zig-zag the producer already knows (the ring's reduce sink): no
   // slice is read; one task per unit profiles the window (Auto) and decides
   const bool pre = SRC != SRC_F32 && p.maxzz_in != nullptr;
@@ -730,7 +730,7 @@ __device__ __forceinline__ int32_t row_symbol(const uint32_t (&a)[W], int i) {
 
 // One tile in shared memory: packed rows in, swizzled fp32 tile out (same buffer).
 template <int W, bool kRaw, int OUT>
-__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, double rcp, const void* accp, int lane,
+__device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, const int32_t (&acc)[32], int lane,
                                                  uint32_t& mz, uint32_t& err) {
   uint32_t a[W];
   const uint32_t row = buf + lane * W * 4;
@@ -748,20 +748,16 @@ __device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, dou
 #pragma unroll
     for (int j = 0; j < W; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[j]) : "r"(row + 4 * j));
   }
+  constexpr bool kAdd = OUT == OUT_ADD_I32 || OUT == OUT_ADD_Q;
   __syncwarp();  // every lane holds its row before the output overwrites the buffer
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     uint32_t o[4];
-    int4 add = make_int4(0, 0, 0, 0);
-    if (OUT == OUT_ADD_I32) add = __ldcg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(accp) + lane * 32) + m);
-    if (OUT == OUT_ADD_Q) {  // the local fp32 chunk, quantized on the fly (quant.cpp:22-27)
-      const float4 xf = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(accp) + lane * 32) + m);
-      add = make_int4(quantize_one(static_cast<double>(xf.x), scale, rcp, err),
-                      quantize_one(static_cast<double>(xf.y), scale, rcp, err),
-                      quantize_one(static_cast<double>(xf.z), scale, rcp, err),
-                      quantize_one(static_cast<double>(xf.w), scale, rcp, err));
+    int32_t ad[4] = {0, 0, 0, 0};
+    if (kAdd) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ad[q] = acc[4 * m + q];
     }
-    const int32_t ad[4] = {add.x, add.y, add.z, add.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int32_t sym = row_symbol<W, kRaw>(a, 4 * m + q);
@@ -783,16 +779,16 @@ __device__ __forceinline__ void decode_tile_smem(uint32_t buf, double scale, dou
 }
 
 template <int OUT>
-__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, double rcp,
-                                                     const void* acc, int lane, uint32_t& mz, uint32_t& err) {
+__device__ __forceinline__ void decode_tile_dispatch(const DecView& v, uint32_t buf, double scale, const int32_t (&acc)[32],
+                                                     int lane, uint32_t& mz, uint32_t& err) {
   if (v.codec == ZC_CODEC_RAW) {
-    decode_tile_smem<32, true, OUT>(buf, scale, rcp, acc, lane, mz, err);
+    decode_tile_smem<32, true, OUT>(buf, scale, acc, lane, mz, err);
     return;
   }
   switch (v.width) {
-#define ZC_DC(W)                                                               \
-  case W:                                                                      \
-    decode_tile_smem<W, false, OUT>(buf, scale, rcp, acc, lane, mz, err); \
+#define ZC_DC(W)                                                          \
+  case W:                                                                 \
+    decode_tile_smem<W, false, OUT>(buf, scale, acc, lane, mz, err); \
     break;
     ZC_DC(1) ZC_DC(2) ZC_DC(3) ZC_DC(4) ZC_DC(5) ZC_DC(6) ZC_DC(7) ZC_DC(8) ZC_DC(9) ZC_DC(10) ZC_DC(11)
     ZC_DC(12) ZC_DC(13) ZC_DC(14) ZC_DC(15) ZC_DC(16) ZC_DC(17) ZC_DC(18) ZC_DC(19) ZC_DC(20) ZC_DC(21)
@@ -812,6 +808,37 @@ __device__ __forceinline__ DecView unpack_view(uint8_t b) {
   v.codec = b == 0 ? kFallback : b == 33 ? ZC_CODEC_RAW : ZC_CODEC_FIXEDLEN;
   v.width = b == 33 ? 32u : b;
   return v;
+}
+
+// The reduce sinks' accumulator row of lane L (its 32 values of the local chunk): eight 16-byte
+// loads in flight at once, then (ADD_Q) the fp32 values quantized with the branch-free fast path
+// and, only when some value sits near a rounding tie or out of the fast range, the exact division
+// out of line.  Emitted once per kernel, outside the per-width decoders.
+template <int OUT>
+__device__ __forceinline__ void load_acc_row(const void* accp, int lane, double scale, double rcp, int32_t (&acc)[32],
+                                             uint32_t& err) {
+  uint32_t b[32];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint4 v = OUT == OUT_ADD_I32 ? __ldcg(reinterpret_cast<const uint4*>(static_cast<const int32_t*>(accp) + lane * 32) + m)
+                                       : __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(accp) + lane * 32) + m);
+    b[4 * m] = v.x;
+    b[4 * m + 1] = v.y;
+    b[4 * m + 2] = v.z;
+    b[4 * m + 3] = v.w;
+  }
+  if (OUT == OUT_ADD_I32) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = static_cast<int32_t>(b[i]);
+    return;
+  }
+  bool slow = false;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = quantize_fast(f2d_bits(b[i], slow), rcp, slow);
+  if (slow) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = static_cast<int32_t>(quantize_exact(__uint_as_float(b[i]), scale, rcp, &err));
+  }
 }
 
 struct DecSeq {  // a warp's tile sequence over owned units, with the view of the current unit
@@ -879,6 +906,10 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     const uint8_t* src = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes + (c & umask) * bytes;
     tma::mbar_arrive_expect_tx(&bars[st], bytes);
     tma::load_1d(my + st * TILE_BYTES, src, bytes, &bars[st]);
+    // the reduce sinks also read the tile's accumulator (the local chunk): into L2 now, so the
+    // lane-row loads of the decode hit L2 instead of waiting on HBM
+    if (OUT == OUT_ADD_I32) tma::prefetch_l2(static_cast<const int32_t*>(p.out) + c * TILE_ELEMS, TILE_BYTES);
+    if (OUT == OUT_ADD_Q) tma::prefetch_l2(p.acc_f32 + c * TILE_ELEMS, TILE_BYTES);
   };
   uint64_t c_issue = iss.next(p, gw * CHUNK);
   for (int i = 0; i < DSTAGES - 1; ++i) {
@@ -909,7 +940,9 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
       mz_flush();
       mz_u = static_cast<uint32_t>(c >> ush);
     }
-    decode_tile_dispatch<OUT>(prc.cv, buf, scale, rcp, acc, lane, mz, err);
+    int32_t ad[32];
+    if (OUT == OUT_ADD_I32 || OUT == OUT_ADD_Q) load_acc_row<OUT>(acc, lane, scale, rcp, ad, err);
+    decode_tile_dispatch<OUT>(prc.cv, buf, scale, ad, lane, mz, err);
     tma::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -1003,13 +1036,16 @@ bool fixed_path_ok(const EncParams& p) {
 
 cudaError_t launch_fixed_range_m(const EncParams& p, void* scratch, uint64_t total_slices, uint32_t s_full, int sms,
                                  int mode, cudaStream_t s) {
-  BGeom g;
+  BGeom g{};
   g.s_full = s_full;
   g.total = total_slices;
   g.fast = 1;
   g.spec = mode == 1 ? 1u : 0u;
   note_launch();
-  const uint64_t tasks = (mode == 1 || (p.src_kind != SRC_F32 && p.maxzz_in != nullptr)) ? p.nunits : total_slices + p.nunits;
+  g.planned = mode == 3 ? 1u : 0u;
+  const uint64_t tasks = (mode == 1 || (p.src_kind != SRC_F32 && p.maxzz_in != nullptr)) ? p.nunits
+                         : mode == 3                                                    ? total_slices
+                                                                                        : total_slices + p.nunits;
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(tasks, 2ull * sms)));
   if (p.src_kind == SRC_F32)
     range_kernel<SRC_F32><<<grid, RT, 0, s>>>(p, static_cast<BUnit*>(scratch), g);
@@ -1043,7 +1079,7 @@ cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t tota
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (rows > 0 && !make_row_tensor_map(&map, p.src, rows)) return cudaErrorInvalidValue;
-  BGeom g;
+  BGeom g{};
   g.s_full = s_full;
   g.total = total_slices;
   g.fast = 1;

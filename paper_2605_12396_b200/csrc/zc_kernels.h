@@ -58,6 +58,7 @@ struct EncParams {
   double scale, rcp;   // float sources
   const double* dscale;  // or, when set, {scale, 1/scale} in device memory (allreduce_eb's agreed scale)
   const uint32_t* maxzz_in;  // SRC_BYTES: each unit's max zig-zag, known from the producer (or null)
+  int no_spec;               // fp32: take the two-read FixedLen path (heavy-tailed data defeats the guess)
   uint64_t total_bytes;
   uint64_t unit_bytes;
   uint32_t nunits;

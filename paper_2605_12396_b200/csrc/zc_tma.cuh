@@ -55,6 +55,10 @@ __device__ __forceinline__ void store_2d(const CUtensorMap* map, const void* src
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) of global memory into L2.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // Waits until at most N committed bulk groups are still READING shared memory.
 template <int N>
