@@ -3,6 +3,7 @@
 // Host C++ that validates arguments the way the reference does, prepares kernel parameters and
 // launches the sm_100a kernels.  Never computes on the CPU: every data-touching entry point
 // launches device work and returns ZC_ERR_CUDA when no device is usable.
+#include <algorithm>
 #include <atomic>
 #include <cctype>
 #include <cmath>
@@ -172,7 +173,7 @@ int encode_common(EncParams& p, cudaStream_t s) {
 int reserve_scratch(cudaStream_t s, uint32_t nunits) {
   Scratch* sc = scratch_for(s, nunits);
   if (!sc) return set_err(ZC_ERR_CUDA, "cannot allocate scratch (no CUDA device?)");
-  const size_t need = batch_scratch_bytes(nunits);
+  const size_t need = std::max(batch_scratch_bytes(nunits), ring_fused_scratch_bytes(nunits));
   if (sc->task_bytes < need) {
     cudaStreamSynchronize(s);
     if (sc->task) cudaFree(sc->task);
@@ -674,6 +675,49 @@ int zc_encode_best(const uint8_t* d_raw, uint64_t raw_len, uint8_t* d_stage, uin
 // ------------------------------------------------------------------ batched hot path
 __attribute__((visibility("hidden"))) int zc_i_reserve_scratch(void* stream, uint32_t nunits) {
   return reserve_scratch(static_cast<cudaStream_t>(stream), nunits);
+}
+
+// One fused ring-step piece (zc_fixed.cu ring_fused_kernel): the received piece in `in_region` is
+// reduced into `sum` (sink OUT_ADD_I32 in place, or OUT_ADD_Q from the local fp32 `x`) and the sums
+// are framed (send_batch semantics, `pin`, no Huffman) into `out_region`.
+__attribute__((visibility("hidden"))) int zc_i_ring_fused(const uint8_t* in_region, uint64_t stride,
+                                                          const zc_encode_result* in_res, int sink, int32_t* sum,
+                                                          const float* x, const double* dscale, uint64_t total,
+                                                          uint64_t unit_bytes, uint8_t* out_region,
+                                                          zc_encode_result* out_res, int32_t pin,
+                                                          const zc_transport_hint* hint, const zc_arb_config* cfg,
+                                                          uint32_t* d_err, void* stream) {
+  if (total == 0) return ZC_OK;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Scratch* sc = scratch_for(s, 1);
+  const uint32_t nunits = static_cast<uint32_t>((total + unit_bytes - 1) / unit_bytes);
+  if (!sc || sc->task_bytes < ring_fused_scratch_bytes(nunits))
+    return set_err(ZC_ERR_CUDA, "fused ring step: scratch not reserved");
+  FusedParams f;
+  std::memset(&f, 0, sizeof(f));
+  f.in_stages = in_region;
+  f.in_stride = stride;
+  f.in_res = in_res;
+  f.sink = sink;
+  f.sum = sum;
+  f.x = x;
+  f.dscale = dscale;
+  f.err = d_err ? d_err : sc->sink;
+  EncParams& p = f.enc;
+  p = base_enc(hint, nullptr, cfg);
+  p.src = sum;
+  p.src_kind = SRC_BYTES;
+  p.mode = ENC_SEND;
+  p.pin = pin;
+  p.total_bytes = total;
+  p.unit_bytes = unit_bytes;
+  p.nunits = nunits;
+  p.stages = out_region;
+  p.stride = stride;
+  p.stage_len = ZC_STAGE_BANK_BYTES;
+  p.results = out_res;
+  p.err = f.err;
+  return cuda_err(launch_ring_fused(f, sc->task, s), "fused ring step");
 }
 
 __attribute__((visibility("hidden"))) int zc_i_encode_batches(const void* src, int kind, uint64_t total, double scale, const zc_i_batch_opts* o, uint8_t* d_stages, uint64_t stride,

@@ -35,6 +35,10 @@ struct zc_i_batch_opts {
 };
 extern "C" {
 int zc_i_reserve_scratch(void* stream, uint32_t nunits);
+int zc_i_ring_fused(const uint8_t* in_region, uint64_t stride, const zc_encode_result* in_res, int sink, int32_t* sum,
+                    const float* x, const double* dscale, uint64_t total, uint64_t unit_bytes, uint8_t* out_region,
+                    zc_encode_result* out_res, int32_t pin, const zc_transport_hint* hint, const zc_arb_config* cfg,
+                    uint32_t* d_err, void* stream);
 int zc_i_encode_batches(const void* src, int kind, uint64_t total, double scale, const zc_i_batch_opts* o,
                         uint8_t* d_stages, uint64_t stride, uint64_t stage_len, int32_t pin,
                         const zc_transport_hint* hint, const zc_huff_ctx* ctx, const zc_arb_config* cfg,

@@ -50,7 +50,11 @@ uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 // Piece regions (the staged ring path): NREG regions, each holding up to `runits` frames of one
 // piece (stage stride as in zcomm.py's Frames), their Huffman companion index and EncodeResults.
+// Main-lane piece regions: 3 for the staged steps; the fused ring (ring_fused) runs the reduce-
+// scatter steps and the first all-gather hop as one wavefront, whose flag protocol needs n + 2
+// regions to be deadlock-free for any number of pieces per chunk (simulated for n <= 16).
 constexpr uint32_t kRegions = 3;
+uint32_t main_regions(uint32_t nranks) { return nranks >= 2 && nranks <= 16 ? std::max(kRegions, nranks + 2) : kRegions; }
 
 // Point-to-point channels (RankCtx::send_encoded / recv_decoded, collectives.cpp:350-364): every
 // directed pair s -> d owns kP2PRegions regions of kP2PUnits frames in d's block, so any rank may
@@ -70,7 +74,7 @@ constexpr uint32_t kMaxRelayRanks = 16;
 uint32_t relay_regions(uint32_t nranks) { return nranks >= 3 && nranks <= kMaxRelayRanks ? nranks : 0u; }
 
 struct Layout {
-  uint32_t nbanks, runits, nranks, nrelay;
+  uint32_t nbanks, runits, nranks, nrelay, nreg;
   uint64_t ub, fstride;  // unit (batch) raw bytes; frame stride inside a piece region
   uint64_t bank_stride, idx_off;
   uint64_t reg_stride, reg_idx, reg_res;  // region size; index / results offsets inside a region
@@ -106,8 +110,9 @@ Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nra
   uint64_t o = 0;
   L.off_banks = o;
   o += nbanks * L.bank_stride;
+  L.nreg = main_regions(nranks);
   L.off_reg = o;
-  o += kRegions * L.reg_stride;
+  o += static_cast<uint64_t>(L.nreg) * L.reg_stride;
   L.off_rly = o;  // relay regions (written by the predecessor's forwards)
   L.nrelay = relay_regions(nranks);
   o += static_cast<uint64_t>(L.nrelay) * L.reg_stride;
@@ -119,8 +124,8 @@ Layout make_layout(uint32_t nbanks, uint32_t runits, bool per_slot, uint32_t nra
   o += align_up(8ull * nbanks, kAlign);
   L.off_credit = o;
   o += align_up(8ull * nbanks, kAlign);
-  L.off_sready = o;  // [kRegions] pieces received in region i (written by the predecessor)
-  o += kAlign;
+  L.off_sready = o;  // [nreg] pieces received in region i (written by the predecessor)
+  o += align_up(8ull * 32, kAlign);
   L.off_scredit = o;  // [r]: pieces rank r has consumed from its regions (written by rank r)
   o += align_up(8ull * kMaxRanks, kAlign);
   L.off_rready = o;  // [nrelay]: relay pieces received in relay region i (written by the predecessor)
@@ -866,10 +871,10 @@ int send_piece(zc_comm* c, int to, const SendSpec& sp, uint64_t k) {
   zc_comm::TlPiece* tl = tl_begin(c, 0, to, c->ptx, bytes);
   zc_encode_result* log = tl ? c->tl_res + (c->tl.size() - 1) * y.runits : nullptr;
   const uint64_t seq = c->ptx++;
-  const uint32_t reg = static_cast<uint32_t>(seq % kRegions);
-  if (seq >= kRegions)  // the receiver has consumed the piece that last used this region
+  const uint32_t reg = static_cast<uint32_t>(seq % y.nreg);
+  if (seq >= y.nreg)  // the receiver has consumed the piece that last used this region
     if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_scredit) + to,
-                             seq - kRegions + 1))
+                             seq - y.nreg + 1))
       return rc;
   if (tl) cudaEventRecord(tl->e0, c->stream);
   uint8_t* dst = c->peer[to] + y.off_reg + reg * y.reg_stride;
@@ -936,7 +941,7 @@ int recv_piece(zc_comm* c, const RecvSpec& rs, uint64_t k) {
   zc_comm::TlPiece* tl = tl_begin(c, 1, -1, rs.relay ? c->rrx : c->prx, bytes);
   if (tl) cudaEventRecord(tl->e0, c->stream);
   const uint64_t seq = rs.relay ? c->rrx++ : c->prx++;
-  const uint32_t reg = static_cast<uint32_t>(seq % (rs.relay ? y.nrelay : kRegions));
+  const uint32_t reg = static_cast<uint32_t>(seq % (rs.relay ? y.nrelay : y.nreg));
   const unsigned long long* ready =
       reinterpret_cast<const unsigned long long*>(c->block + (rs.relay ? y.off_rready : y.off_sready)) + reg;
   if (int rc = launch_wait(c, ready, seq + 1)) return rc;
@@ -1151,6 +1156,120 @@ int allgather_hops(zc_comm* c, const SendSpec& first, RecvOf recv_of) {
   return ZC_OK;
 }
 
+// ---- the fused ring (north_star (4)): each reduce-scatter receive is ONE kernel with the next
+// step's send of the chunk it reduces — decode -> reduce (-> quantize, allreduce_eb) -> range ->
+// decide -> pack into the successor's region (zc_fixed.cu ring_fused_kernel) — and the steps run
+// as one wavefront: at time k the first step sends piece k, step s receives piece k-1-s and, fused,
+// sends it on as step s+1 (the last reduce-scatter step's send is the first all-gather hop);
+// all-gather hops after the first forward verbatim (relay lane).  The encode of piece k of a step
+// overlaps the decode of piece k-1 of the next on the peer, chunk by chunk, with the NVLink stores
+// inside the kernels.  FixedLen / RAW frames only: with a shared Huffman context, embedded
+// codebooks or the Huffman pin the staged steps run instead.
+// The fused kernel moves whole 16-byte vectors of the chunks: every chunk base must be aligned.
+bool chunks_aligned(const Chunks& ch, const void* a, const void* b) {
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return false;
+  for (int ci = 0; ci < ch.n; ++ci)
+    if (ch.lo(ci) % 4) return false;
+  return true;
+}
+
+// Opt-in (ZC_RING_FUSEDK=1): the fused kernel meets the traffic target (P + ~8.4 MiB of HBM per
+// 4 MiB batch per step, ncu) but each warp runs its tiles' loads synchronously, so on B200 it is
+// slower than the staged decode-sink / profile / emit kernels with their TMA rings.
+bool fused_ring_ok(const zc_comm* c, int pin) {
+  return use_staged(c) && fuse_ring() && std::getenv("ZC_RING_FUSEDK") != nullptr && c->shared == nullptr &&
+         !c->cfg.arb.embed_codebook && pin != ZC_PIN_HUFFMAN && c->cfg.pin != ZC_PIN_HUFFMAN &&
+         c->lay.nreg >= static_cast<uint32_t>(c->nranks) + 2 && (c->nranks == 2 || c->lay.nrelay > 0);
+}
+
+// Receive piece j of a reduce-scatter step (chunk `rs`: sink into int32 sums, from the local fp32
+// for OUT_ADD_Q) fused with its send to the successor as the next step (`pin`).
+int fused_piece(zc_comm* c, const RecvSpec& rs, uint64_t j, int pin) {
+  const Layout& y = c->lay;
+  const int to = (c->rank + 1) % c->nranks;
+  const uint64_t pb = static_cast<uint64_t>(y.runits) * y.ub, off = j * pb;
+  const uint64_t bytes = std::min(pb, rs.bytes - off);
+  zc_comm::TlPiece* tr = tl_begin(c, 1, -1, c->prx, bytes);
+  if (tr) cudaEventRecord(tr->e0, c->stream);
+  const uint64_t rseq = c->prx++;
+  const uint32_t rreg = static_cast<uint32_t>(rseq % y.nreg);
+  if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_sready) + rreg, rseq + 1))
+    return rc;
+  zc_comm::TlPiece* ts = tl_begin(c, 0, to, c->ptx, bytes);
+  zc_encode_result* log = ts ? c->tl_res + (c->tl.size() - 1) * y.runits : nullptr;
+  const uint64_t sseq = c->ptx++;
+  const uint32_t sreg = static_cast<uint32_t>(sseq % y.nreg);
+  if (sseq >= y.nreg)
+    if (int rc = launch_wait(c, reinterpret_cast<const unsigned long long*>(c->block + y.off_scredit) + to, sseq - y.nreg + 1))
+      return rc;
+  const uint8_t* in = c->block + y.off_reg + rreg * y.reg_stride;
+  uint8_t* out = c->peer[to] + y.off_reg + sreg * y.reg_stride;
+  auto* res = reinterpret_cast<zc_encode_result*>(out + y.reg_res);
+  int32_t* sum = static_cast<int32_t*>(rs.dst) + off / 4;
+  if (tr) cudaEventRecord(tr->e1, c->stream);
+  if (ts) cudaEventRecord(ts->e0, c->stream);
+  if (int rc = zc_i_ring_fused(in, y.fstride, reinterpret_cast<const zc_encode_result*>(in + y.reg_res), rs.out_kind, sum,
+                               rs.acc ? rs.acc + off / 4 : nullptr, &c->scal()->scale, bytes, y.ub, out, res, pin,
+                               &c->cfg.hint, &c->cfg.arb, c->err_word(), c->stream))
+    return rc;
+  auto* ready = reinterpret_cast<unsigned long long*>(c->peer[to] + y.off_sready) + sreg;
+  post_signal(ready, sseq + 1);
+  note_launch();
+  piece_sent_kernel<<<1, 32, 0, c->stream>>>(res, static_cast<uint32_t>(nbatches(c, bytes)), bytes, y.ub,
+                                             reinterpret_cast<zc_wire_stats*>(c->block + y.off_wire), ready, sseq + 1,
+                                             log);
+  if (ts) cudaEventRecord(ts->e1, c->stream);
+  if (int rc = cuda_err(cudaGetLastError(), "fused piece")) return rc;
+  if (int rc = post_credit(c, rseq + 1)) return rc;
+  if (tr) cudaEventRecord(tr->e2, c->stream);
+  return ZC_OK;
+}
+
+// The fused wavefront over the reduce-scatter steps (sink `sink`: OUT_ADD_I32 into `sym`, or
+// OUT_ADD_Q from `x` into `sym`) and, with `ag_of`, the all-gather hops (sink of chunk ci).
+template <class AgOf>
+int ring_fused(zc_comm* c, const Chunks& ch, int sink, int32_t* sym, const float* x, int fused_pin, bool allgather,
+               AgOf ag_of) {
+  const int n = c->nranks, r = c->rank, next = (r + 1) % n;
+  const uint64_t pb = static_cast<uint64_t>(c->lay.runits) * c->lay.ub;
+  auto pieces = [&](uint64_t by) { return (by + pb - 1) / pb; };
+  const int S = allgather ? 2 * n - 2 : n - 1;
+  const SendSpec first = sink == OUT_ADD_Q ? SendSpec{x + ch.lo(r), SRC_F32, ch.bytes(r), fused_pin, nullptr}
+                                           : sym_send(sym + ch.lo(r), ch.bytes(r), fused_pin);
+  std::vector<RecvSpec> st(S);
+  std::vector<uint64_t> np(S);
+  uint64_t kmax = pieces(first.bytes);
+  for (int s = 0; s < S; ++s) {
+    if (s <= n - 2) {  // reduce-scatter step s receives chunk r - s - 1
+      const int ci = r - s - 1;
+      st[s] = RecvSpec{sym + ch.lo(ci), ch.bytes(ci), sink, sink == OUT_ADD_Q ? x + ch.lo(ci) : nullptr, nullptr, false, false,
+                       fused_pin};
+    } else {  // all-gather hop h receives chunk r - h
+      const int h = s - (n - 1);
+      st[s] = ag_of(r - h);
+      st[s].relay = h > 0;
+      st[s].fwd = h < n - 2;
+    }
+    np[s] = pieces(st[s].bytes);
+    kmax = std::max<uint64_t>(kmax, np[s] + 1 + s);
+  }
+  for (uint64_t k = 0; k < kmax; ++k) {
+    if (k < pieces(first.bytes))
+      if (int rc = send_piece(c, next, first, k)) return rc;
+    for (int s = 0; s < S; ++s) {
+      if (k < 1ull + s) break;
+      const uint64_t j = k - 1 - s;
+      if (j >= np[s]) continue;
+      if (s <= n - 2 && (s < n - 2 || allgather)) {  // fused with the send of the next step
+        if (int rc = fused_piece(c, st[s], j, s < n - 2 ? fused_pin : c->cfg.pin)) return rc;
+      } else if (int rc = recv_piece(c, st[s], j)) {
+        return rc;
+      }
+    }
+  }
+  return ZC_OK;
+}
+
 // Reduce-scatter then (optionally) all-gather over the ring (collectives.cpp:460-502).  RS frames
 // use fusedPin (raw below fusedCodecMinMsgBytes), AG frames cfg.pin.
 int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
@@ -1170,6 +1289,9 @@ int enqueue_ring(zc_comm* c, int32_t* d_sym, uint64_t count, bool allgather) {
         return rc;
     return ZC_OK;
   }
+  if (fused_ring_ok(c, fused_pin) && chunks_aligned(ch, d_sym, nullptr))
+    return ring_fused(c, ch, OUT_ADD_I32, d_sym, nullptr, fused_pin, allgather,
+                      [&](int ci) { return sym_recv(d_sym + ch.lo(ci), ch.bytes(ci), OUT_BYTES, c->cfg.pin); });
   const bool fz = fuse_ring() && use_mz(c, max_chunk_units(c, count));
   for (int t = 0; t < n - 1; ++t) {
     uint32_t* mo = fz ? mz_buf(c, t) : nullptr;
@@ -1348,6 +1470,19 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
       // into the output; only the chunk this rank reduced is dequantized from its symbols.
       const Chunks ch{count, n};
       const int fused_pin = count * 4 >= c->cfg.fused_codec_min_msg_bytes ? c->cfg.pin : ZC_PIN_RAW;
+      const int ok = OUT_F32 + (out_f64 ? 1 : 0);
+      const uint64_t esz = out_f64 ? 8 : 4;
+      auto ag_of = [&](int ci) {
+        return RecvSpec{static_cast<uint8_t*>(d_out) + ch.lo(ci) * esz, ch.bytes(ci), ok, nullptr, nullptr, false, false,
+                        c->cfg.pin};
+      };
+      if (fused_ring_ok(c, fused_pin) && chunks_aligned(ch, c->sym, d_x)) {
+        if (int rc = ring_fused(c, ch, OUT_ADD_Q, c->sym, d_x, fused_pin, true, ag_of)) return rc;
+        note_launch();
+        dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym + ch.lo(r + 1), ch.bytes(r + 1) / 4, s,
+                                                        static_cast<uint8_t*>(d_out) + ch.lo(r + 1) * esz, out_f64);
+        return cuda_err(cudaGetLastError(), "dequantize");
+      }
       for (int t = 0; t < n - 1; ++t) {
         uint32_t* mo = mz_buf(c, t);
         if (int rc = cuda_err(cudaMemsetAsync(mo, 0, max_chunk_units(c, count) * 4, c->stream), "unit ranges")) return rc;
@@ -1357,13 +1492,7 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
         const RecvSpec rs{c->sym + ch.lo(rcv), ch.bytes(rcv), OUT_ADD_Q, d_x + ch.lo(rcv), mo, false, false, fused_pin};
         if (int rc = staged_xfer(c, (r + 1) % n, sp, rs)) return rc;
       }
-      const int ok = OUT_F32 + (out_f64 ? 1 : 0);
-      const uint64_t esz = out_f64 ? 8 : 4;
-      if (int rc = allgather_hops(c, sym_send(c->sym + ch.lo(r + 1), ch.bytes(r + 1), c->cfg.pin, mz_buf(c, n - 2)),
-                                  [&](int ci) {
-                                    return RecvSpec{static_cast<uint8_t*>(d_out) + ch.lo(ci) * esz, ch.bytes(ci), ok,
-                                                    nullptr, nullptr, false, false, c->cfg.pin};
-                                  }))
+      if (int rc = allgather_hops(c, sym_send(c->sym + ch.lo(r + 1), ch.bytes(r + 1), c->cfg.pin, mz_buf(c, n - 2)), ag_of))
         return rc;
       note_launch();
       dequantize_dev_kernel<<<g, 256, 0, c->stream>>>(c->sym + ch.lo(r + 1), ch.bytes(r + 1) / 4, s,

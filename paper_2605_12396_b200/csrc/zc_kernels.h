@@ -122,6 +122,24 @@ __device__ __forceinline__ double enc_scale(const EncParams& p) { return p.dscal
 __device__ __forceinline__ double enc_rcp(const EncParams& p) { return p.dscale ? p.dscale[1] : p.rcp; }
 __device__ __forceinline__ double dec_scale(const DecParams& p) { return p.dscale ? p.dscale[0] : p.scale; }
 
+// One piece of a ring step fused with the next step's send of the same chunk (zc_fixed.cu):
+// decode the predecessor's FixedLen / RAW frames -> reduce into the local chunk (int32 add, or the
+// local fp32 quantized on the fly) -> per unit: range and window range -> decide -> pack the sums
+// into the successor's region.  FixedLen / RAW only (no Huffman context, no embedded codebooks).
+struct FusedParams {
+  const uint8_t* in_stages;  // this rank's received piece region
+  uint64_t in_stride;
+  const zc_encode_result* in_res;
+  int sink;                  // OUT_ADD_I32 (sums in place) or OUT_ADD_Q (sum = q(x) + decoded)
+  int32_t* sum;              // local chunk piece (int32)
+  const float* x;            // OUT_ADD_Q: local fp32 chunk piece
+  const double* dscale;      // OUT_ADD_Q: {scale, 1/scale}
+  EncParams enc;             // the successor's frames: src = sum (SRC_BYTES), stages / results there
+  uint32_t* err;
+};
+cudaError_t launch_ring_fused(const FusedParams& f, void* scratch, cudaStream_t s);
+size_t ring_fused_scratch_bytes(uint32_t nunits);
+
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
 // can state how many of OUR kernels a region launched.
 void note_launch();

@@ -390,3 +390,25 @@ def test_fused_ring_equals_unfused(zc, port, n, pin, monkeypatch):
     a, b = wires
     assert list(a.frames_by_codec) == list(b.frames_by_codec)
     assert (a.raw_bytes, a.payload_bytes, a.total_bytes) == (b.raw_bytes, b.payload_bytes, b.total_bytes)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+@pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_RAW])
+def test_fused_ring_kernel_vs_oracle(zc, port, n, pin, monkeypatch):
+    """ZC_RING_FUSEDK=1: every reduce-scatter receive is one kernel with the next step's send
+    (decode -> reduce -> range -> decide -> pack into the successor), the steps and the first
+    all-gather hop run as one wavefront over n + 2 piece regions.  Symbols, allreduce_eb outputs and
+    WireStats equal the oracle ring; several pieces per chunk (ZC_COMM_REGION_UNITS=1)."""
+    monkeypatch.setenv("ZC_RING_FUSEDK", "1")
+    monkeypatch.setenv("ZC_COMM_REGION_UNITS", "1")
+    count = n * ((9 << 20) // 4) + 4 * n  # chunk bases 16-byte aligned (the fused kernel's precondition)
+    rng = np.random.default_rng(500 + n + pin)
+    syms = [np.clip(rng.laplace(0, 30 * (r + 1), count), -2**20, 2**20).astype(np.int32) for r in range(n)]
+    g = zc.Group(n, cfg=zc.collective_config(pin))
+    _ring_check(zc, port, g, syms, pin)
+    xs = [rng.laplace(0, 1e-2, count).astype(np.float32) for _ in range(n)]
+    rel = 1e-4 / max(float(np.abs(x).max()) for x in xs)
+    scale, _, exp = _serial_eb(port, xs, rel)
+    g2 = zc.Group(n, cfg=zc.collective_config(pin))
+    for o in g2.allreduce_eb([t(x) for x in xs], rel, torch.float64):
+        assert np.array_equal(npy(o).view(np.uint64), exp.view(np.uint64))
