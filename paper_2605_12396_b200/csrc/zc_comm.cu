@@ -1173,11 +1173,10 @@ bool chunks_aligned(const Chunks& ch, const void* a, const void* b) {
   return true;
 }
 
-// Opt-in (ZC_RING_FUSEDK=1): the fused kernel meets the traffic target (P + ~8.4 MiB of HBM per
-// 4 MiB batch per step, ncu) but each warp runs its tiles' loads synchronously, so on B200 it is
-// slower than the staged decode-sink / profile / emit kernels with their TMA rings.
+// Default wherever it applies (ZC_RING_NOFUSEDK=1 falls back to the staged decode-sink / profile /
+// emit kernels for A/B runs).
 bool fused_ring_ok(const zc_comm* c, int pin) {
-  return use_staged(c) && fuse_ring() && std::getenv("ZC_RING_FUSEDK") != nullptr && c->shared == nullptr &&
+  return use_staged(c) && fuse_ring() && std::getenv("ZC_RING_NOFUSEDK") == nullptr && c->shared == nullptr &&
          !c->cfg.arb.embed_codebook && pin != ZC_PIN_HUFFMAN && c->cfg.pin != ZC_PIN_HUFFMAN &&
          c->lay.nreg >= static_cast<uint32_t>(c->nranks) + 2 && (c->nranks == 2 || c->lay.nrelay > 0);
 }

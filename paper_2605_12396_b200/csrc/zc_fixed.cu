@@ -1006,15 +1006,15 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
 // unit's max zig-zag and its 64 KiB window's max zig-zag are merged), then, once the unit's phase A
 // has completed, decided (arbitrate_plan on the window, encode_best's post-check / the pin on the
 // unit range) and packed from the just-written sums — still in L2 — into the successor's region
-// (phase B).  Work is an ordered task queue of 16-tile groups, A(0) A(1) B(0) A(2) B(1) ... : a B
-// task only waits for A tasks claimed before it by running CTAs, so it cannot deadlock, and a
+// (phase B).  Work is an ordered task queue of 8-tile groups, A(0) A(1) B(0) A(2) B(1) ... : a B
+// task only waits for A tasks claimed before it by running warps, so it cannot deadlock, and a
 // unit's sums are re-read right after they were written.
-// Small CTAs, many per SM: a task's barrier only waits for its own 4 warps, and the SM interleaves
-// the latency chains of many independent tasks.
+// Tasks are claimed per WARP (no CTA barriers); within a task the warp double-buffers its tiles
+// with cp.async (the next tile's packed rows and accumulator tile load while this one is reduced).
 constexpr int FT_WARPS = 4;
 constexpr int FT = FT_WARPS * 32;
-constexpr int FT_CTAS = 4;   // per SM (128 registers x 128 threads x 4 = the register file)
-constexpr uint32_t FG = 8;   // tiles per task (two per warp)
+constexpr int FT_CTAS = 3;   // per SM: 12 warps x 16 KiB of stages
+constexpr uint32_t FG = 8;   // tiles per warp task
 
 struct FusedUnit {
   uint32_t maxzz, wmz, adone, bdone;
@@ -1053,43 +1053,48 @@ __device__ __forceinline__ void decode_row_dispatch(uint32_t codec, uint32_t wid
   }
 }
 
-// Task t of the queue -> (phase B?, unit, group).  Units 0..U-2 have G groups, the last GL.
-__device__ __forceinline__ bool fused_task(uint32_t t, uint32_t U, uint32_t G, uint32_t GL, uint32_t& u, uint32_t& g) {
+// Task t of the queue -> (phase B?, unit, group).  Units 0..U-2 have G groups, the last GL.  The
+// queue runs phase B `lag` units behind phase A — A(0..lag-1), then A(i) B(i-lag), then the last B
+// — with lag ~ the warps in flight / G, so a unit's phase A has (almost always) completed when its
+// first B task is claimed, and its sums are still in L2.
+__device__ __forceinline__ bool fused_task(uint32_t t, uint32_t U, uint32_t G, uint32_t GL, uint32_t lag, uint32_t& u,
+                                           uint32_t& g) {
   auto groups = [&](uint32_t v) { return v + 1 == U ? GL : G; };
-  // block 0: A(0); block i (1..U-1): A(i) B(i-1); block U: B(U-1)
-  if (t < groups(0)) {
-    u = 0;
-    g = t;
-    return false;  // A
-  }
-  t -= groups(0);
-  for (uint32_t i = 1; i < U; ++i) {
-    if (t < groups(i)) {
-      u = i;
+  uint32_t na = 0, nb = 0;  // next A / B unit
+  for (;;) {
+    const bool take_a = na < U && (na < lag || nb + lag <= na);
+    const uint32_t v = take_a ? na : nb;
+    const uint32_t k = groups(v);
+    if (t < k) {
+      u = v;
       g = t;
-      return false;
+      return !take_a;
     }
-    t -= groups(i);
-    if (t < groups(i - 1)) {
-      u = i - 1;
-      g = t;
-      return true;
-    }
-    t -= groups(i - 1);
+    t -= k;
+    if (take_a) ++na;
+    else ++nb;
   }
-  u = U - 1;
-  g = t;
-  return true;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int SINK>
 __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_constant__ FusedParams f, BUnit* us,
-                                                           FusedUnit* fu, uint32_t* task_ctr) {
-  extern __shared__ __align__(128) uint8_t s_buf[];  // FT_WARPS tiles
-  __shared__ uint32_t s_task, s_u, s_g, s_b, s_codec, s_width, s_in_codec, s_in_width, s_mz[FT_WARPS], s_wmz[FT_WARPS];
-  __shared__ unsigned long long s_P;
+                                                                 FusedUnit* fu, uint32_t* task_ctr, uint32_t lag) {
+  extern __shared__ __align__(128) uint8_t s_buf[];
   const EncParams& p = f.enc;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // per warp, two stages of {the tile's packed rows, the accumulator / sums tile (swizzled rows)}
+  const uint32_t wbase = tma::smem_u32(s_buf) + static_cast<uint32_t>(warp) * 4 * TILE_BYTES;
+  auto pk = [&](int st) { return wbase + static_cast<uint32_t>(st) * 2 * TILE_BYTES; };
+  auto ac = [&](int st) { return wbase + static_cast<uint32_t>(st) * 2 * TILE_BYTES + TILE_BYTES; };
   const uint32_t U = p.nunits;
   const uint32_t ush = unit_tile_shift(p.unit_bytes);
   const uint32_t unit_tiles = 1u << ush;
@@ -1098,153 +1103,151 @@ __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_co
   const uint32_t G = (unit_tiles + FG - 1) / FG, GL = (last_tiles + FG - 1) / FG;
   const uint32_t ntasks = 2 * ((U - 1) * G + GL);
   const double scale = SINK == OUT_ADD_Q ? f.dscale[0] : 1.0, rcp = SINK == OUT_ADD_Q ? f.dscale[1] : 1.0;
-  const uint32_t buf = tma::smem_u32(s_buf + warp * TILE_BYTES);
   uint32_t err = 0;
+  // a 4 KiB tile of int32 / fp32 values into swizzled rows (chunk ch of row r at r*128 + (ch ^ r&7)*16)
+  auto issue_tile = [&](uint32_t dst, const void* src) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = lane + 32 * k, row = c >> 3, ch = c & 7;
+      cp_async16(dst + row * 128 + ((ch ^ (row & 7)) << 4), static_cast<const uint8_t*>(src) + 16 * c);
+    }
+  };
+  auto row_of = [&](uint32_t buf, uint32_t (&v)[32]) {  // lane's row of a swizzled tile
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[4 * m]), "=r"(v[4 * m + 1]), "=r"(v[4 * m + 2]), "=r"(v[4 * m + 3])
+                   : "r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)));
+  };
   for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t t = atomicAdd(task_ctr, 1u);
-      s_task = t;
-      if (t < ntasks) {
-        uint32_t u, g;
-        s_b = fused_task(t, U, G, GL, u, g) ? 1u : 0u;
-        s_u = u;
-        s_g = g;
-      }
-    }
-    __syncthreads();
-    if (s_task >= ntasks) break;
-    if (tid == 32 && s_task + gridDim.x < ntasks) {
-      // the task this CTA's successor in the queue order will take next round: its phase-A inputs
-      // (the packed rows and the accumulator tiles) into L2 while this task runs
-      uint32_t pu, pg;
-      if (!fused_task(s_task + gridDim.x, U, G, GL, pu, pg)) {
-        const uint64_t pR = unit_R(p, pu), pn = pR / 4;
-        const uint64_t pe0 = static_cast<uint64_t>(pg) * FG * TILE_ELEMS;
-        if (pe0 < pn) {
-          const uint64_t pe1 = min(pn, pe0 + FG * TILE_ELEMS) / TILE_ELEMS * TILE_ELEMS;  // whole tiles
-          const uint64_t pbase = static_cast<uint64_t>(pu) * (p.unit_bytes / 4);
-          if (pe1 > pe0) {
-            const void* a = SINK == OUT_ADD_I32 ? static_cast<const void*>(f.sum + pbase + pe0)
-                                                : static_cast<const void*>(f.x + pbase + pe0);
-            tma::prefetch_l2(a, static_cast<uint32_t>((pe1 - pe0) * 4));
-            const zc_frame_header h = header_from_words(reinterpret_cast<const uint64_t*>(f.in_stages + pu * f.in_stride));
-            const uint32_t w = h.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(h.params & 63) : 32u;
-            if (w >= 1 && w <= 32)
-              tma::prefetch_l2(f.in_stages + pu * f.in_stride + kHeaderBytes + pe0 / 8 * w,
-                               static_cast<uint32_t>((pe1 - pe0) / 8 * w));
-          }
-        }
-      }
-    }
-    const uint32_t u = s_u, g = s_g;
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(task_ctr, 1u);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= ntasks) break;
+    uint32_t u, g;
+    const bool isB = fused_task(t, U, G, GL, lag, u, g);
     const uint64_t R = unit_R(p, u);
     const uint64_t n_elem = R / 4;
     const uint32_t tiles_u = static_cast<uint32_t>((n_elem + TILE_ELEMS - 1) / TILE_ELEMS);
     const uint32_t t0 = g * FG, t1 = min(tiles_u, t0 + FG);
+    const uint32_t tf1 = min(t1, static_cast<uint32_t>(n_elem / TILE_ELEMS));  // full tiles: [t0, tf1)
     const uint64_t ebase = static_cast<uint64_t>(u) * (p.unit_bytes / 4);  // unit's first element in the piece
-    if (!s_b) {  // ---- phase A: decode + reduce
-      if (tid == 0) {
+    FusedUnit& F = fu[u];
+    if (!isB) {  // ---- phase A: decode + reduce
+      uint32_t icodec = 0, iw = 0;
+      if (lane == 0) {
         FrameCheck fc;
         check_frame<true>(f.in_stages + static_cast<uint64_t>(u) * f.in_stride, f.in_res[u].total_bytes, R, nullptr, false,
                           nullptr, false, fc);
-        s_in_codec = fc.codec;
-        s_in_width = fc.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(fc.h.params) : 32u;
+        icodec = fc.codec;
+        iw = fc.codec == ZC_CODEC_FIXEDLEN ? static_cast<uint32_t>(fc.h.params) : 32u;
       }
-      __syncthreads();
-      const uint32_t icodec = s_in_codec, iw = s_in_width;
+      icodec = __shfl_sync(FULL, icodec, 0);
+      iw = __shfl_sync(FULL, iw, 0);
       const uint8_t* payload = f.in_stages + static_cast<uint64_t>(u) * f.in_stride + kHeaderBytes;
       uint32_t mz = 0, wmz = 0;
       if (icodec != ZC_CODEC_RAW && icodec != ZC_CODEC_FIXEDLEN) {
         err |= ZC_DERR_CORRUPT;  // never from this library's encoder; the reduce cannot be replayed
       } else {
-        for (uint32_t tl = t0 + warp; tl < t1; tl += FT_WARPS) {
+        auto issue = [&](uint32_t tl, int st) {
           const uint64_t e0 = static_cast<uint64_t>(tl) * TILE_ELEMS;
-          int32_t* sumt = f.sum + ebase + e0;
-          if (e0 + TILE_ELEMS <= n_elem) {
-            // the tile's packed rows (128 * width bytes) into shared memory, coalesced
-            const uint4* src = reinterpret_cast<const uint4*>(payload + e0 / 8 * iw);
-            for (uint32_t i = lane; i < 8 * iw; i += 32) {
-              const uint4 v = __ldcg(src + i);
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf + 16 * i), "r"(v.x), "r"(v.y), "r"(v.z),
-                           "r"(v.w)
-                           : "memory");
-            }
-            __syncwarp();
-            int32_t sym[32], acc[32];
-            decode_row_dispatch(icodec, iw, buf, lane, sym);
-            load_acc_row<SINK>(SINK == OUT_ADD_I32 ? static_cast<const void*>(sumt) : static_cast<const void*>(f.x + ebase + e0),
-                               lane, scale, rcp, acc, err);
-            __syncwarp();  // every lane has its packed row before the sums overwrite the buffer
+          const uint8_t* src = payload + e0 / 8 * iw;  // the tile's 128 * width packed bytes
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-              uint32_t o[4];
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t i = lane + 32u * k;
+            if (i < 8 * iw) cp_async16(pk(st) + 16 * i, src + 16 * i);
+          }
+          issue_tile(ac(st), SINK == OUT_ADD_I32 ? static_cast<const void*>(f.sum + ebase + e0)
+                                                 : static_cast<const void*>(f.x + ebase + e0));
+          cp_async_commit();
+        };
+        if (t0 < tf1) issue(t0, 0);
+        for (uint32_t tl = t0; tl < tf1; ++tl) {
+          const int st = (tl - t0) & 1;
+          if (tl + 1 < tf1) {
+            issue(tl + 1, st ^ 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncwarp();
+          int32_t sym[32];
+          decode_row_dispatch(icodec, iw, pk(st), lane, sym);
+          uint32_t b[32];
+          row_of(ac(st), b);
+          if (SINK == OUT_ADD_Q) {  // the local fp32, quantized (fast path; exact division near a tie)
+            bool slow = false;
+            uint32_t q[32];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const long long sm = static_cast<long long>(acc[4 * m + q]) + sym[4 * m + q];
-                if (sm != static_cast<int32_t>(sm)) err |= ZC_DERR_OVERFLOW;
-                o[q] = static_cast<uint32_t>(static_cast<int32_t>(sm));
-                const uint32_t z = zigzag32(static_cast<int32_t>(o[q]));
-                mz = max(mz, z);
-                if (tl * TILE_BYTES < kSampleWindow) wmz = max(wmz, z);
-              }
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)),
-                           "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
-                           : "memory");
-            }
-            __syncwarp();
+            for (int i = 0; i < 32; ++i) q[i] = static_cast<uint32_t>(quantize_fast(f2d_bits(b[i], slow), rcp, slow));
+            if (slow) {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {  // the sums out, 512 contiguous bytes per instruction
-              const int row = 4 * m + (lane >> 3), ch = lane & 7;
-              uint32_t o0, o1, o2, o3;
-              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(o0), "=r"(o1), "=r"(o2), "=r"(o3)
-                           : "r"(buf + row * 128 + ((ch ^ (row & 7)) << 4))
-                           : "memory");
-              reinterpret_cast<uint4*>(sumt + row * 32)[ch] = make_uint4(o0, o1, o2, o3);
+              for (int i = 0; i < 32; ++i) q[i] = quantize_exact(__uint_as_float(b[i]), scale, rcp, &err);
             }
-            __syncwarp();
-          } else {  // the piece's last, partial tile: element by element
-            const uint64_t P = icodec == ZC_CODEC_RAW ? 4 * n_elem : packed_bytes(n_elem, iw);
-            for (uint64_t e = e0 + lane; e < n_elem; e += 32) {
-              int32_t sy;
-              if (icodec == ZC_CODEC_RAW) {
-                sy = static_cast<int32_t>(stream_word<true>(payload, P, e));
-              } else {
-                const uint64_t bit = e * iw;
-                const unsigned long long xw = (static_cast<unsigned long long>(stream_word<true>(payload, P, bit / 32 + 1)) << 32) |
-                                              stream_word<true>(payload, P, bit / 32);
-                sy = unzigzag32(static_cast<uint32_t>((xw >> (bit & 31)) & (iw == 32 ? 0xffffffffull : ((1ull << iw) - 1))));
-              }
-              const int32_t a = SINK == OUT_ADD_I32 ? f.sum[ebase + e]
-                                                    : quantize_one(static_cast<double>(f.x[ebase + e]), scale, rcp, err);
-              const long long sm = static_cast<long long>(a) + sy;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) b[i] = q[i];
+          }
+          const bool win = static_cast<uint64_t>(tl) * TILE_BYTES < kSampleWindow;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const long long sm = static_cast<long long>(static_cast<int32_t>(b[4 * m + q])) + sym[4 * m + q];
               if (sm != static_cast<int32_t>(sm)) err |= ZC_DERR_OVERFLOW;
-              f.sum[ebase + e] = static_cast<int32_t>(sm);
-              const uint32_t z = zigzag32(static_cast<int32_t>(sm));
+              o[q] = static_cast<uint32_t>(static_cast<int32_t>(sm));
+              const uint32_t z = zigzag32(static_cast<int32_t>(o[q]));
               mz = max(mz, z);
-              if (e * 4 < kSampleWindow) wmz = max(wmz, z);
+              if (win) wmz = max(wmz, z);
             }
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ac(st) + lane * 128 + ((m ^ (lane & 7)) << 4)),
+                         "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                         : "memory");
+          }
+          __syncwarp();
+          int32_t* sumt = f.sum + ebase + static_cast<uint64_t>(tl) * TILE_ELEMS;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {  // the sums out, 512 contiguous bytes per instruction
+            const int row = 4 * m + (lane >> 3), ch = lane & 7;
+            uint32_t o0, o1, o2, o3;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(o0), "=r"(o1), "=r"(o2), "=r"(o3)
+                         : "r"(ac(st) + row * 128 + ((ch ^ (row & 7)) << 4))
+                         : "memory");
+            reinterpret_cast<uint4*>(sumt + row * 32)[ch] = make_uint4(o0, o1, o2, o3);
+          }
+          __syncwarp();  // the stage's buffers are refilled two tiles later
+        }
+        if (t1 > tf1) {  // the piece's last, partial tile: element by element
+          const uint64_t e0 = static_cast<uint64_t>(tf1) * TILE_ELEMS;
+          const uint64_t P = icodec == ZC_CODEC_RAW ? 4 * n_elem : packed_bytes(n_elem, iw);
+          for (uint64_t e = e0 + lane; e < n_elem; e += 32) {
+            int32_t sy;
+            if (icodec == ZC_CODEC_RAW) {
+              sy = static_cast<int32_t>(stream_word<true>(payload, P, e));
+            } else {
+              const uint64_t bit = e * iw;
+              const unsigned long long xw = (static_cast<unsigned long long>(stream_word<true>(payload, P, bit / 32 + 1)) << 32) |
+                                            stream_word<true>(payload, P, bit / 32);
+              sy = unzigzag32(static_cast<uint32_t>((xw >> (bit & 31)) & (iw == 32 ? 0xffffffffull : ((1ull << iw) - 1))));
+            }
+            const int32_t a = SINK == OUT_ADD_I32 ? f.sum[ebase + e]
+                                                  : quantize_one(static_cast<double>(f.x[ebase + e]), scale, rcp, err);
+            const long long sm = static_cast<long long>(a) + sy;
+            if (sm != static_cast<int32_t>(sm)) err |= ZC_DERR_OVERFLOW;
+            f.sum[ebase + e] = static_cast<int32_t>(sm);
+            const uint32_t z = zigzag32(static_cast<int32_t>(sm));
+            mz = max(mz, z);
+            if (e * 4 < kSampleWindow) wmz = max(wmz, z);
           }
         }
       }
       mz = __reduce_max_sync(FULL, mz);
       wmz = __reduce_max_sync(FULL, wmz);
       if (lane == 0) {
-        s_mz[warp] = mz;
-        s_wmz[warp] = wmz;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        uint32_t a = 0, b = 0;
-        for (int i = 0; i < FT_WARPS; ++i) {
-          a = max(a, s_mz[i]);
-          b = max(b, s_wmz[i]);
-        }
-        FusedUnit& F = fu[u];
-        atomicMax(&F.maxzz, a);
-        if (b) atomicMax(&F.wmz, b);
-        uint32_t old;  // release: the sums and the ranges above before the tiles count
+        atomicMax(&F.maxzz, mz);
+        if (wmz) atomicMax(&F.wmz, wmz);
+        uint32_t old;  // acq_rel: this task's sums and ranges before its tiles count; the last sees all
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&F.adone), "r"(t1 - t0) : "memory");
         if (old + (t1 - t0) == tiles_u) {
           // the unit's last phase-A task decides it (a pure function of the unit's ranges):
@@ -1252,14 +1255,14 @@ __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_co
           const uint64_t pcap = p.stage_len > kHeaderBytes ? p.stage_len - kHeaderBytes : 0;
           uint32_t plan = ZC_CODEC_RAW;
           if (!(R <= p.cfg.small_batch_threshold_bytes || p.stage_len <= kHeaderBytes)) {
-            zc_sample_stats st;
-            st.sampled_bytes = R < kSampleWindow ? R : kSampleWindow;
-            st.max_zigzag = __ldcg(&F.wmz);
-            st.ctx_code_len_bits = 0.0;
-            st.ctx_code_len_valid = 0u;
-            st.self_code_len_bits = 0.0;
-            st.self_code_len_valid = 0u;
-            plan = arbitrate_plan(R, pcap, st, p.hint, false, p.cfg).choice;
+            zc_sample_stats sst;
+            sst.sampled_bytes = R < kSampleWindow ? R : kSampleWindow;
+            sst.max_zigzag = __ldcg(&F.wmz);
+            sst.ctx_code_len_bits = 0.0;
+            sst.ctx_code_len_valid = 0u;
+            sst.self_code_len_bits = 0.0;
+            sst.self_code_len_valid = 0u;
+            plan = arbitrate_plan(R, pcap, sst, p.hint, false, p.cfg).choice;
           }
           BUnit& L = us[u];  // decide_unit / final_codec read only the fields set here
           L.plan = plan;
@@ -1279,72 +1282,73 @@ __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_co
           asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&F.decided), "r"(1u) : "memory");
         }
       }
+      __syncwarp();
       continue;
     }
-    // ---- phase B: pack (the unit's phase-A tasks were claimed before this one by running CTAs;
-    // the last of them has decided the unit)
-    if (tid == 0) {
-      FusedUnit& F = fu[u];
-      for (;;) {
+    // ---- phase B: pack the sums (every phase-A task of the unit was claimed before this one by a
+    // running warp, and the last of them decided the unit)
+    if (lane == 0) {
+      for (;;) {  // relaxed polls (no L1 invalidation per poll), then the acquire below
         uint32_t d;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(&F.decided) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(&F.decided) : "memory");
         if (d) break;
-        __nanosleep(32);
+        __nanosleep(64);
       }
-      s_codec = __ldcg(&F.codec);
-      s_width = __ldcg(&F.width);
-      s_P = __ldcg(&F.payload);
     }
-    __syncthreads();
-    const uint32_t codec = s_codec, width = s_width;
-    const uint64_t P = s_P;
+    __syncwarp();
+    {
+      uint32_t d;  // every lane acquires the decision (and with it the sums)
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(&F.decided) : "memory");
+      (void)d;
+    }
+    const uint32_t codec = __ldcg(&F.codec), width = __ldcg(&F.width);
+    const uint64_t P = __ldcg(&F.payload);
     uint8_t* opay = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
     if (codec == ZC_CODEC_RAW || codec == ZC_CODEC_FIXEDLEN) {
-      for (uint32_t tl = t0 + warp; tl < t1; tl += FT_WARPS) {
-        const uint64_t e0 = static_cast<uint64_t>(tl) * TILE_ELEMS;
+      if (t0 < tf1) {
+        issue_tile(ac(0), f.sum + ebase + static_cast<uint64_t>(t0) * TILE_ELEMS);
+        cp_async_commit();
+      }
+      for (uint32_t tl = t0; tl < tf1; ++tl) {
+        const int st = (tl - t0) & 1;
+        if (tl + 1 < tf1) {
+          issue_tile(ac(st ^ 1), f.sum + ebase + static_cast<uint64_t>(tl + 1) * TILE_ELEMS);
+          cp_async_commit();
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
+        uint32_t sv[32];
+        row_of(ac(st), sv);
+        __syncwarp();
+        store_row(codec, width, sv, opay, static_cast<uint64_t>(tl) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
+      }
+      if (t1 > tf1) {  // partial tile: the lane's row, guarded
+        const uint64_t e0 = static_cast<uint64_t>(tf1) * TILE_ELEMS;
+        const uint64_t r0 = e0 + static_cast<uint64_t>(lane) * 32;
         const int32_t* sumt = f.sum + ebase + e0;
-        if (e0 + TILE_ELEMS <= n_elem) {
+        uint32_t sv[32];
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {  // the sums in (L2), coalesced, into the swizzled tile
-            const int row = 4 * m + (lane >> 3), ch = lane & 7;
-            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(sumt + row * 32) + ch);
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf + row * 128 + ((ch ^ (row & 7)) << 4)),
-                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                         : "memory");
-          }
-          __syncwarp();
-          uint32_t sv[32];
+        for (int i = 0; i < 32; ++i) sv[i] = r0 + i < n_elem ? static_cast<uint32_t>(__ldcg(sumt + lane * 32 + i)) : 0u;
+        if (codec == ZC_CODEC_RAW) {
 #pragma unroll
-          for (int m = 0; m < 8; ++m)
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(sv[4 * m]), "=r"(sv[4 * m + 1]), "=r"(sv[4 * m + 2]), "=r"(sv[4 * m + 3])
-                         : "r"(buf + lane * 128 + ((m ^ (lane & 7)) << 4)));
-          __syncwarp();
-          store_row(codec, width, sv, opay, e0 + static_cast<uint64_t>(lane) * 32);
-        } else {  // partial tile: the lane's row, guarded
-          const uint64_t r0 = e0 + static_cast<uint64_t>(lane) * 32;
-          uint32_t sv[32];
+          for (int i = 0; i < 32; ++i)
+            if (r0 + i < n_elem) reinterpret_cast<uint32_t*>(opay)[r0 + i] = sv[i];
+        } else {
+          uint32_t z[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[i] = r0 + i < n_elem ? static_cast<uint32_t>(sumt[lane * 32 + i]) : 0u;
-          if (codec == ZC_CODEC_RAW) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (r0 + i < n_elem) reinterpret_cast<uint32_t*>(opay)[r0 + i] = sv[i];
-          } else {
-            uint32_t z[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) z[i] = zigzag32(static_cast<int32_t>(sv[i]));
-            if (r0 < n_elem) pack_store_w(width, z, opay, (r0 / 32) * width, P);
-          }
+          for (int i = 0; i < 32; ++i) z[i] = zigzag32(static_cast<int32_t>(sv[i]));
+          if (r0 < n_elem) pack_store_w(width, z, opay, (r0 / 32) * width, P);
         }
       }
-    } else if (tid == 0) {
+    } else if (lane == 0) {
       err |= ZC_DERR_CAPACITY;  // cannot ship even raw (collectives.cpp:278-281)
     }
-    __syncthreads();
-    if (tid == 0) {  // the unit's last B task writes the header and the EncodeResult
+    __syncwarp();
+    if (lane == 0) {  // the unit's last phase-B task writes the header and the EncodeResult
       __threadfence();
-      if (atomicAdd(&fu[u].bdone, t1 - t0) + (t1 - t0) == tiles_u) write_frame_header(p, u, codec, width, P);
+      if (atomicAdd(&F.bdone, t1 - t0) + (t1 - t0) == tiles_u) write_frame_header(p, u, codec, width, P);
     }
   }
   err = __reduce_or_sync(FULL, err);
@@ -1501,7 +1505,7 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
 }
 
 
-constexpr size_t FT_SMEM = static_cast<size_t>(FT_WARPS) * TILE_BYTES;
+constexpr size_t FT_SMEM = static_cast<size_t>(FT_WARPS) * 4 * TILE_BYTES;
 size_t ring_fused_scratch_bytes(uint32_t nunits) {
   return sizeof(FusedUnit) * (nunits ? nunits : 1) + 256 + sizeof(BUnit) * (nunits ? nunits : 1);
 }
@@ -1522,12 +1526,14 @@ cudaError_t launch_ring_fused(const FusedParams& f, void* scratch, cudaStream_t 
     cudaFuncSetAttribute(ring_fused_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(FT_SMEM));
   }
   const uint64_t tiles = (f.enc.total_bytes / 4 + TILE_ELEMS - 1) / TILE_ELEMS;
-  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + FG - 1) / FG, static_cast<uint64_t>(FT_CTAS) * sms)));
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + FG * FT_WARPS - 1) / (FG * FT_WARPS), static_cast<uint64_t>(FT_CTAS) * sms)));
   note_launch();
+  const uint32_t G = static_cast<uint32_t>(((f.enc.unit_bytes / TILE_BYTES) + FG - 1) / FG);
+  const uint32_t lag = static_cast<uint32_t>(std::max<uint64_t>(1, (static_cast<uint64_t>(grid) * FT_WARPS + G - 1) / G + 1));
   if (f.sink == OUT_ADD_Q)
-    ring_fused_kernel<OUT_ADD_Q><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr);
+    ring_fused_kernel<OUT_ADD_Q><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag);
   else
-    ring_fused_kernel<OUT_ADD_I32><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr);
+    ring_fused_kernel<OUT_ADD_I32><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag);
   return cudaGetLastError();
 }
 

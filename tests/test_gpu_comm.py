@@ -394,13 +394,16 @@ def test_fused_ring_equals_unfused(zc, port, n, pin, monkeypatch):
 
 @pytest.mark.parametrize("n", [2, 3, 5])
 @pytest.mark.parametrize("pin", [abi.PIN_AUTO, abi.PIN_FIXEDLEN, abi.PIN_RAW])
-def test_fused_ring_kernel_vs_oracle(zc, port, n, pin, monkeypatch):
-    """ZC_RING_FUSEDK=1: every reduce-scatter receive is one kernel with the next step's send
-    (decode -> reduce -> range -> decide -> pack into the successor), the steps and the first
+@pytest.mark.parametrize("fusedk", [True, False])
+def test_fused_ring_kernel_vs_oracle(zc, port, n, pin, fusedk, monkeypatch):
+    """The fused ring (default; ZC_RING_NOFUSEDK=1 opts out): every reduce-scatter receive is one
+    kernel with the next step's send (decode -> reduce -> range -> decide -> pack into the
+    successor), the steps and the first
     all-gather hop run as one wavefront over n + 2 piece regions.  Symbols, allreduce_eb outputs and
     WireStats equal the oracle ring; several pieces per chunk (ZC_COMM_REGION_UNITS=1)."""
-    monkeypatch.setenv("ZC_RING_FUSEDK", "1")
     monkeypatch.setenv("ZC_COMM_REGION_UNITS", "1")
+    if not fusedk:
+        monkeypatch.setenv("ZC_RING_NOFUSEDK", "1")
     count = n * ((9 << 20) // 4) + 4 * n  # chunk bases 16-byte aligned (the fused kernel's precondition)
     rng = np.random.default_rng(500 + n + pin)
     syms = [np.clip(rng.laplace(0, 30 * (r + 1), count), -2**20, 2**20).astype(np.int32) for r in range(n)]

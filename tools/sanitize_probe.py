@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2605_12396_b200 import zcomm  # noqa: E402
 
 n = int(os.environ.get("NR", 3))
-count = (9 << 20) // 4 + 7
+count = 3 * ((3 << 20) // 4)  # chunk bases 16-byte aligned: the fused ring kernel runs
 g = torch.Generator(device="cuda").manual_seed(5)
 xs = [torch.randn(count, generator=g, device="cuda") for _ in range(n)]
 grp = zcomm.Group(n)
