@@ -872,7 +872,24 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
   const uint64_t per = ZC_BATCH_RAW_BYTES / 4;  // elements per batch
   const uint64_t nb = (count + per - 1) / per;
   const uint64_t gb = group_batches ? group_batches : 4;
-  const uint64_t ngroups = (nb + gb - 1) / gb;
+  // Group sizes ramp 1, 2, 4, ... up to gb at the start and back down at the end: the first H2D
+  // and the last D2H run alone (nothing to overlap them with), so short edge groups keep both copy
+  // directions busy for almost the whole call while the middle groups amortise their launches.
+  std::vector<uint64_t> sizes;
+  {
+    std::vector<uint64_t> head, tail;
+    uint64_t left = nb;
+    for (uint64_t k = 1; k < gb && left > 2 * k; k *= 2) {
+      head.push_back(k);
+      tail.push_back(k);
+      left -= 2 * k;
+    }
+    sizes = head;
+    for (; left >= gb; left -= gb) sizes.push_back(gb);
+    if (left) sizes.push_back(left);
+    sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+  }
+  const uint64_t ngroups = sizes.size();
   // frames of this call's own encoder: without a usable Huffman path every valid frame is
   // FixedLen / RAW and the general decode kernels have nothing to do
   // (embedded codebooks: Auto may pick Huffman without a shared context, rea.cpp:160)
@@ -881,10 +898,10 @@ extern "C" int zc_codec_roundtrip_host_f32(const float* h_x, uint64_t count, dou
   if (int rc = cuda_err(cudaEventRecord(pp->start, caller), "pipeline start")) return rc;
   for (cudaStream_t s : {pp->h2d, pp->work, pp->d2h})
     if (int rc = cuda_err(cudaStreamWaitEvent(s, pp->start, 0), "pipeline wait")) return rc;
-  for (uint64_t g = 0; g < ngroups; ++g) {
-    const uint64_t b0 = g * gb;
+  uint64_t b0 = 0;
+  for (uint64_t g = 0; g < ngroups; b0 += sizes[g], ++g) {
     const uint64_t e0 = b0 * per;
-    const uint64_t n = (count - e0) < gb * per ? (count - e0) : gb * per;
+    const uint64_t n = (count - e0) < sizes[g] * per ? (count - e0) : sizes[g] * per;
     cudaEvent_t in = pp->in[g % kEv], done = pp->done[g % kEv];
     if (int rc = cuda_err(cudaMemcpyAsync(d_work + e0, h_x + e0, n * 4, cudaMemcpyHostToDevice, pp->h2d), "H2D")) return rc;
     if (int rc = cuda_err(cudaEventRecord(in, pp->h2d), "H2D event")) return rc;
