@@ -35,6 +35,8 @@ constexpr uint32_t PV = ZC_SAMPLE_WINDOW_BYTES / 16 / PC;
 
 template <int SRC>
 __global__ void __launch_bounds__(PT) profile_kernel(const EncParams p, BUnit* us) {
+  // the speculative emit may launch now (it waits for this grid's completion before reading units)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t u = blockIdx.x / PC, part = blockIdx.x % PC;
   __shared__ uint32_t s_hist[256];

@@ -30,6 +30,7 @@ namespace {
 constexpr int RT = 512;                  // range kernel threads
 constexpr int ET_WARPS = 16;             // emit kernel warps per CTA
 constexpr int ET = ET_WARPS * 32;
+constexpr int ET_CTAS = 1;               // emit CTAs per SM
 constexpr int STAGES = 3;                // tiles in flight per warp
 constexpr uint32_t TILE_ELEMS = 1024;    // 32 x 32 fp32
 constexpr uint32_t TILE_BYTES = TILE_ELEMS * 4;
@@ -429,6 +430,83 @@ __device__ __forceinline__ void store_row(uint32_t codec, uint32_t width, const 
   }
 }
 
+// Half a row (16 values): quantize_row's fast path and exactness test on 16 values, so a row is
+// quantized and packed in two passes and only half of it is live in registers at a time.
+__device__ __forceinline__ void quantize_half(const float (&x)[16], double scale, double rcp, float xlim, bool big,
+                                              uint32_t (&s)[16], uint32_t& err) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  uint32_t rm = 0;
+  float am = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double xd = static_cast<double>(x[i]);
+    const double t = __fma_rn(xd, rcp, kMagic);
+    const double r = __fma_rn(xd, rcp, -__dsub_rn(t, kMagic));
+    rm = max(rm, static_cast<uint32_t>(__double2hiint(r)) & 0x7fffffffu);
+    s[i] = static_cast<uint32_t>(__double2loint(t));
+    if (i & 1) am = absmax3(am, x[i - 1], x[i]);
+  }
+  if (big || rm >= 0x3FDFFFF0u || !(am < xlim)) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s[i] = quantize_exact(x[i], scale, rcp, &err);
+  }
+}
+
+// One row (lane's 32 values of a swizzled fp32 / symbol tile in shared memory) -> its W packed
+// words (FixedLen) or 32 symbol words (kRaw), in two 16-value halves; `spec`: the exact symbols'
+// max zig-zag into sp_mz.
+template <int W, bool kRaw, int SRC>
+__device__ __forceinline__ void emit_row(uint32_t row, int lane, double scale, double rcp, float xlim, bool big, bool spec,
+                                         uint32_t& sp_mz, uint32_t* dst, uint32_t& err) {
+  uint32_t o[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) o[k] = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float x[16];
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const int m = 4 * h + mm;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x[4 * mm]), "=f"(x[4 * mm + 1]), "=f"(x[4 * mm + 2]), "=f"(x[4 * mm + 3])
+                   : "r"(row + ((m ^ (lane & 7)) << 4)));
+    }
+    uint32_t sv[16];
+    if (SRC == SRC_F32) {
+      quantize_half(x, scale, rcp, xlim, big, sv, err);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sv[i] = __float_as_uint(x[i]);
+    }
+    if (spec) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sp_mz = max(sp_mz, zigzag32(static_cast<int32_t>(sv[i])));
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int idx = 16 * h + i;
+      if (kRaw) {
+        o[idx] = sv[i];
+      } else {  // fields are disjoint: + is | (one IMAD per symbol)
+        const uint32_t z = zigzag32(static_cast<int32_t>(sv[i]));
+        const int bit = idx * W, k = bit >> 5, sh = bit & 31;
+        o[k] += z << sh;
+        if (sh + W > 32) o[k + 1] += z >> (32 - sh);
+      }
+    }
+  }
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j) reinterpret_cast<uint4*>(dst)[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) reinterpret_cast<uint2*>(dst)[j] = make_uint2(o[2 * j], o[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < W; ++j) dst[j] = o[j];
+  }
+}
+
 // Grid sizing: a warp's contiguous share of the tiles is at least about CHUNK tiles.
 constexpr uint64_t CHUNK = 4;
 // The decoder's warp tile order: warp gw owns chunks gw, gw + tw, ... of CHUNK consecutive tiles
@@ -513,7 +591,7 @@ __device__ __noinline__ void spec_flush(const EncParams& p, BUnit* us, uint32_t 
 }
 
 template <int SRC, int kMode>
-__global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ EncParams p, const BUnit* us, BGeom g,
+__global__ void __launch_bounds__(ET, ET_CTAS) emit_kernel(const __grid_constant__ EncParams p, const BUnit* us, BGeom g,
                                                      const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
                                                      uint64_t nfull) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
@@ -523,6 +601,9 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES) + warp * STAGES;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   uint32_t err = 0;
+  // Launched as a programmatic dependent of the window profile (mode 1): everything above ran
+  // while the profile drained; the unit states are read only after it has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // the redo emit has nothing to do unless a speculation missed
   if (kMode == 2 && *reinterpret_cast<const volatile uint32_t*>(&bglobal(const_cast<BUnit*>(us), p.nunits)->n_redo) == 0)
     return;
@@ -596,14 +677,7 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
     const uint32_t st = k % STAGES;
     tma::mbar_wait(&bars[st], (k / STAGES) & 1u);
     const uint8_t* tile = my + st * TILE_BYTES;
-    float x[32];
     const uint32_t row = tma::smem_u32(tile) + lane * 128;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                   : "=f"(x[4 * m]), "=f"(x[4 * m + 1]), "=f"(x[4 * m + 2]), "=f"(x[4 * m + 3])
-                   : "r"(row + ((m ^ (lane & 7)) << 4)));
-    }
     const uint32_t u = static_cast<uint32_t>(c >> ush);
     if (u != cur_u) {
       cur_u = u;
@@ -611,20 +685,33 @@ __global__ void __launch_bounds__(ET, 1) emit_kernel(const __grid_constant__ Enc
       payload = p.stages + static_cast<uint64_t>(u) * p.stride + kHeaderBytes;
     }
     if (kMode == 1 && sp_n && sp_u != u) spec_run_flush();
-    uint32_t s[32];
-    if (SRC == SRC_F32) {
-      quantize_row(x, scale, rcp, xlim, v.big, s, err);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) s[i] = __float_as_uint(x[i]);
-    }
-    if (kMode == 1 && v.spec) {  // the exact symbols' max zig-zag (non-finite inputs raised by quantize_row)
-#pragma unroll
-      for (int i = 0; i < 32; ++i) sp_mz = max(sp_mz, zigzag32(static_cast<int32_t>(s[i])));
+    const bool spec = kMode == 1 && v.spec;  // the exact symbols' max zig-zag (non-finite inputs raised by the quantizer)
+    if (spec) {
       sp_u = u;
       ++sp_n;
     }
-    store_row(v.codec, v.width, s, payload, (c & umask) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32);
+    {
+      const uint64_t row_sym = (c & umask) * TILE_ELEMS + static_cast<uint64_t>(lane) * 32;
+      uint32_t* base = reinterpret_cast<uint32_t*>(payload);
+      if (v.codec == ZC_CODEC_RAW) {
+        emit_row<32, true, SRC>(row, lane, scale, rcp, xlim, v.big, spec, sp_mz, base + row_sym, err);
+      } else {
+        uint32_t* d = base + (row_sym / 32) * v.width;
+        switch (v.width) {
+#define ZC_ER(W)                                                                          \
+  case W:                                                                                 \
+    emit_row<W, false, SRC>(row, lane, scale, rcp, xlim, v.big, spec, sp_mz, d, err); \
+    break;
+          ZC_ER(1) ZC_ER(2) ZC_ER(3) ZC_ER(4) ZC_ER(5) ZC_ER(6) ZC_ER(7) ZC_ER(8) ZC_ER(9) ZC_ER(10) ZC_ER(11)
+          ZC_ER(12) ZC_ER(13) ZC_ER(14) ZC_ER(15) ZC_ER(16) ZC_ER(17) ZC_ER(18) ZC_ER(19) ZC_ER(20) ZC_ER(21)
+          ZC_ER(22) ZC_ER(23) ZC_ER(24) ZC_ER(25) ZC_ER(26) ZC_ER(27) ZC_ER(28) ZC_ER(29) ZC_ER(30) ZC_ER(31)
+          ZC_ER(32)
+#undef ZC_ER
+          default:
+            break;
+        }
+      }
+    }
     // Refill this stage only now: the row's values have been consumed (stored), so every lane's
     // shared-memory reads of the tile have completed before the async proxy overwrites it (a
     // refill right after the loads raced them when the row work is short, e.g. RAW symbols).
@@ -1442,12 +1529,23 @@ cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t tota
   g.fast = 1;
   g.spec = mode == 1 ? 1u : 0u;
   const uint64_t want = (ntiles + ET_WARPS * CHUNK - 1) / (ET_WARPS * CHUNK);
-  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(ET_CTAS) * sms)));
   note_launch();
   const BUnit* us = static_cast<const BUnit*>(scratch);
   if (p.src_kind == SRC_F32) {
-    if (mode == 1)
-      emit_kernel<SRC_F32, 1><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+    if (mode == 1) {  // programmatic dependent launch after profile_kernel (griddepcontrol.wait inside)
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(ET);
+      lc.dynamicSmemBytes = EMIT_SMEM;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      if (cudaError_t e = cudaLaunchKernelEx(&lc, emit_kernel<SRC_F32, 1>, p, us, g, map, ntiles, nfull)) return e;
+    }
     else if (mode == 2)
       emit_kernel<SRC_F32, 2><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
     else
