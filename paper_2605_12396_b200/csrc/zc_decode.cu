@@ -33,6 +33,86 @@ __device__ __forceinline__ uint64_t unit_region(const DecParams& p, uint32_t u) 
   return p.frame_len ? p.frame_len[u].total_bytes : p.region;
 }
 
+
+// Index-less Huffman frames (e.g. from the CPU reference: huffman.cpp:281-314 has no sync points),
+// decoded by the whole CTA with self-synchronisation.  The stream's bits are split into one
+// segment per thread; every thread decodes from a start position to the first code boundary at or
+// past its segment's end, counting the codes that start inside.  Round 0 starts every thread at
+// its raw segment start (mid-code: garbage at first, but a Huffman decoder falls into step with
+// the true code boundaries after a few codes); each later round restarts thread t at the end
+// thread t-1 reached.  When no start changes, every thread decoded from a true boundary: the
+// counts are exact, an exclusive scan places each thread's symbols, and a last pass writes them.
+// Codes crossing the stream end are not decoded (as huff_run); the first n symbols must decode.
+// Returns false when they do not (the caller then replays the sequential decoder, which also
+// reproduces the reference's partial output).  out: the n raw bytes.  All threads call.
+struct SyncScan {
+  uint64_t end;       // first code boundary >= the segment end (or where decoding stopped)
+  uint32_t count;     // codes starting in [start, segment end)
+  uint32_t bad_at;    // codes before an undecodable code / a code crossing the stream end, or ~0
+};
+__device__ __forceinline__ SyncScan sync_scan(const DevHuff* t, const uint8_t* s, uint64_t slen, uint64_t start,
+                                              uint64_t seg_end, uint8_t* out, uint64_t obase, uint64_t n) {
+  const uint64_t total = slen * 8;
+  SyncScan r{start, 0u, 0xffffffffu};
+  uint64_t bitpos = start;
+  while (bitpos < seg_end) {
+    // a 64-bit window at bitpos (bits past the stream end read as zero)
+    const uint64_t w = bitpos >> 5;
+    const unsigned long long acc =
+        ((static_cast<unsigned long long>(stream_word<false>(s, slen, w + 1)) << 32) | stream_word<false>(s, slen, w)) >>
+        (bitpos & 31);
+    const uint16_t e = t->lut[acc & ((1u << ZC_HUFF_ROOT_BITS) - 1)];
+    uint32_t l = e >> 8, sym = e & 0xFFu;
+    if (l == 0) l = huff_long(t, acc, sym);  // acc holds >= 33 valid bits
+    if (l == 0 || bitpos + l > total) {
+      r.bad_at = r.count;
+      break;
+    }
+    if (out != nullptr && obase + r.count < n) out[obase + r.count] = static_cast<uint8_t>(sym);
+    ++r.count;
+    bitpos += l;
+  }
+  r.end = bitpos;
+  return r;
+}
+
+__device__ bool huff_parallel_sync(const DevHuff* t, const uint8_t* s, uint64_t slen, uint64_t n, uint8_t* out) {
+  __shared__ unsigned long long s_end[DT];
+  __shared__ uint32_t s_cnt[DT];
+  __shared__ uint32_t s_fail;
+  const int tid = threadIdx.x;
+  const uint64_t total = slen * 8;
+  const uint64_t seg0 = total * tid / DT, seg1 = total * (tid + 1) / DT;
+  uint64_t start = tid == 0 ? 0 : seg0;
+  SyncScan r{};
+  for (int round = 0;; ++round) {
+    r = sync_scan(t, s, slen, start, seg1, nullptr, 0, 0);
+    s_end[tid] = r.end;
+    __syncthreads();
+    const uint64_t ns = tid == 0 ? 0 : max(static_cast<uint64_t>(s_end[tid - 1]), seg0);
+    const bool changed = ns != start;
+    start = ns;
+    __syncthreads();
+    if (!__syncthreads_or(changed)) break;
+    if (round >= DT) return false;  // no convergence: let the sequential decoder decide
+  }
+  // exclusive scan of the counts; the first n symbols must all decode
+  s_cnt[tid] = r.count;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  uint64_t off = 0, sum = 0;
+  for (int i = 0; i < DT; ++i) {  // 256 shared reads per thread: cheap next to the decode
+    if (i < tid) off += s_cnt[i];
+    sum += s_cnt[i];
+  }
+  if (r.bad_at != 0xffffffffu && off + r.bad_at < n) atomicOr(&s_fail, 1u);
+  __syncthreads();
+  if (s_fail || sum < n) return false;
+  if (off < n) sync_scan(t, s, slen, start, seg1, out, off, n);
+  __syncthreads();
+  return true;
+}
+
 // The unit's last decode CTA (one per unit, when a flag is set): sequential Huffman decode for units whose index is missing or
 // disagrees with the payload (flag bit 0), and the raw-copy fallback for undecodable units.
 __device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameCheck& fc, DevHuff& s_t, uint8_t* s_lens,
@@ -52,9 +132,35 @@ __device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameChec
   __syncthreads();
   const double sc = dec_scale(p);
   Sink sink{p.out_kind, p.out, sc, p.out_kind == OUT_ADD_Q ? 1.0 / sc : 0.0, p.acc_f32, 0u};
+  __shared__ uint32_t s_par;
   if (!s_fail && fc.codec == ZC_CODEC_HUFFMAN) {
     const bool ok = load_huff_tables<false>(fc, payload, p.ctx, &s_t, &s_flag, s_lens);
-    if (!ok) {
+    // byte / fp32 outputs: the CTA-parallel self-synchronising decode into the output's raw bytes,
+    // then (fp32) the sink applied in place, 16 bytes at a time (same size)
+    if (threadIdx.x == 0) s_par = 0;
+    __syncthreads();
+    if (ok && (p.out_kind == OUT_BYTES || p.out_kind == OUT_F32)) {
+      const bool emb = (fc.h.flags & ZC_FLAG_EMBEDDED_CODEBOOK) != 0;
+      const uint8_t* s = payload + (emb ? ZC_HUFF_CODEBOOK_BYTES : 0);
+      const uint64_t slen = fc.h.payload_bytes - (emb ? ZC_HUFF_CODEBOOK_BYTES : 0);
+      const uint64_t n = fc.h.raw_bytes;
+      uint8_t* raw = static_cast<uint8_t*>(p.out) + obase;
+      if (huff_parallel_sync(&s_t, s, slen, n, raw)) {
+        if (p.out_kind == OUT_F32) {
+          for (uint64_t v = threadIdx.x; v * 16 < n; v += DT) {
+            const uint32_t nb = static_cast<uint32_t>(n - v * 16 < 16 ? n - v * 16 : 16);
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (uint32_t j = 0; j < nb; ++j) w[j >> 2] |= static_cast<uint32_t>(raw[v * 16 + j]) << (8 * (j & 3));
+            emit16(sink, obase + v * 16, w, nb, err);
+          }
+        }
+        if (threadIdx.x == 0) s_par = 1;
+      }
+      __syncthreads();
+    }
+    if (s_par) {
+      // decoded
+    } else if (!ok) {
       if (threadIdx.x == 0) s_fail = 1;
     } else if (threadIdx.x == 0) {
       const bool emb = (fc.h.flags & ZC_FLAG_EMBEDDED_CODEBOOK) != 0;

@@ -613,3 +613,39 @@ def test_small_stage_capacity_vs_oracle(zc, port, pin, stage_len):
         if er.total_bytes:
             assert np.array_equal(st[b * stride: b * stride + er.total_bytes], ef), f"frame {b}"
         assert np.all(st[b * stride + stage_len:(b + 1) * stride] == 0xA5), f"stage {b} overrun"
+
+
+@pytest.mark.parametrize("embed", [False, True])
+def test_indexless_4mib_reference_frame_parallel_decode(zc, port, embed):
+    """A 4 MiB Huffman frame produced by the CPU reference path (no companion index, huffman.cpp:
+    216-246) decodes on the device through recv_batch's dispatch: the CTA-parallel
+    self-synchronising decoder, bit-exact, in milliseconds (the sequential decoder is the fallback)."""
+    import time
+    rng = np.random.default_rng(44 + embed)
+    sym = np.clip(rng.laplace(0, 40, (4 << 20) // 4), -3000, 3000).astype(np.int32)
+    raw = sym.view(np.uint8)
+    o = port.huff_from_bytes(raw[: 1 << 20])
+    c = zc.HuffmanContext.from_bytes(raw[: 1 << 20])
+    cfg = abi.default_arb_config()
+    cfg.embed_codebook = 1 if embed else 0
+    r, frame = port.send_batch(raw, abi.PIN_HUFFMAN, abi.make_hint(), None if embed else o, cfg)
+    assert r.codec == abi.CODEC_HUFFMAN
+    h = zc.parse_header(bytes(frame[:32]))
+    payload = t(frame[32:32 + h.payload_bytes].copy())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ok, back = zc.huffman_decode(h, payload, None if embed else c, len(raw))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    assert ok and np.array_equal(npy(back), raw)
+    assert dt < 1.0, f"index-less 4 MiB decode took {dt:.2f} s"
+    # the same frame through the batched receive path with an fp32 sink (dequantize_into)
+    fr = zc.alloc_frames(len(raw), DEV)
+    fr.stages[: len(frame)] = t(frame)
+    er = abi.EncodeResult()
+    er.codec, er.payload_bytes, er.total_bytes = abi.CODEC_HUFFMAN, h.payload_bytes, len(frame)
+    fr.results[: C.sizeof(er)] = t(np.frombuffer(bytes(er), np.uint8).copy())
+    y = zc.decode_batches(fr, None if embed else c, scale=2e-4, use_index=False)
+    exp = np.zeros(len(sym), np.float32)
+    port.lib.zo_dequantize_f32(sym, len(sym), 0, 2e-4, 0, exp)
+    assert np.array_equal(npy(y), exp)
