@@ -756,6 +756,8 @@ __device__ __forceinline__ void grain_pack(const EncParams& p, const RawVec rv[2
 // at once: one launch instead of three.
 template <int SRC, bool kFused>
 __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUnit* us, BGeom g) {
+  pdl_trigger();
+  pdl_wait();  // a programmatic dependent of the FixedLen emit (the units' decisions)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ unsigned long long s_enc[256];
   __shared__ uint32_t s_start[BS / kIndexGrain + 1];
@@ -1002,7 +1004,7 @@ void launch_huff_emit(const EncParams& p, BUnit* us, const BGeom& g, int sms, cu
   }
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(g.total, static_cast<uint64_t>(2 * sms)));
   note_launch();
-  huff_emit_kernel<SRC, kFused><<<grid, NT, kHuffEmitSmem, s>>>(p, us, g);
+  launch_pdl(huff_emit_kernel<SRC, kFused>, dim3(grid), dim3(NT), kHuffEmitSmem, s, p, us, g);
 }
 
 template <int SRC>

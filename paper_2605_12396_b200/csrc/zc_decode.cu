@@ -211,6 +211,7 @@ __device__ void fixup_unit(const DecParams& p, uint32_t u, uint32_t f, FrameChec
 }
 
 __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
+  pdl_wait();  // a programmatic dependent of the FixedLen decoder (it writes the codecs / outputs first)
   const uint32_t u = blockIdx.y;
   const uint64_t R = unit_raw(p, u);
   const uint64_t nvec = (R + 15) / 16;
@@ -303,6 +304,7 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   static std::atomic<uint64_t> carve{0};
   if (first_on_device(carve)) cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
   note_launch();
+  if (p.fast) return launch_pdl(decode_kernel, grid, dim3(DT), 0, s, p);
   decode_kernel<<<grid, DT, 0, s>>>(p);
   return cudaGetLastError();
 }

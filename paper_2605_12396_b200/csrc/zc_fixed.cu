@@ -601,9 +601,10 @@ __global__ void __launch_bounds__(ET, ET_CTAS) emit_kernel(const __grid_constant
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_tiles + static_cast<size_t>(ET_WARPS) * STAGES * TILE_BYTES) + warp * STAGES;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   uint32_t err = 0;
-  // Launched as a programmatic dependent of the window profile (mode 1): everything above ran
-  // while the profile drained; the unit states are read only after it has completed.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Launched as a programmatic dependent (mode 1 of the window profile, mode 2 of mode 1):
+  // everything above ran while the previous kernel drained; units are read only after it completed.
+  pdl_trigger();
+  pdl_wait();
   // the redo emit has nothing to do unless a speculation missed
   if (kMode == 2 && *reinterpret_cast<const volatile uint32_t*>(&bglobal(const_cast<BUnit*>(us), p.nunits)->n_redo) == 0)
     return;
@@ -952,6 +953,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
                                                           const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
                                                           uint64_t nfull) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
+  pdl_trigger();  // the general decoder (its programmatic dependent) may be placed now
   uint8_t* s_tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* my = s_tiles + static_cast<size_t>(warp) * DSTAGES * TILE_BYTES;
@@ -1547,7 +1549,10 @@ cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t tota
       if (cudaError_t e = cudaLaunchKernelEx(&lc, emit_kernel<SRC_F32, 1>, p, us, g, map, ntiles, nfull)) return e;
     }
     else if (mode == 2)
-      emit_kernel<SRC_F32, 2><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
+      {
+        if (cudaError_t e = launch_pdl(emit_kernel<SRC_F32, 2>, dim3(grid), dim3(ET), EMIT_SMEM, s, p, us, g, map, ntiles, nfull))
+          return e;
+      }
     else
       emit_kernel<SRC_F32, 0><<<grid, ET, EMIT_SMEM, s>>>(p, us, g, map, ntiles, nfull);
   } else {

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
 
 #include "zc_common.cuh"
 
@@ -139,6 +140,28 @@ struct FusedParams {
 };
 cudaError_t launch_ring_fused(const FusedParams& f, void* scratch, cudaStream_t s);
 size_t ring_fused_scratch_bytes(uint32_t nunits);
+
+// Programmatic dependent launch: the kernel may begin while the previous kernel on the stream drains
+// (its CTAs are placed as the previous ones retire); it executes griddepcontrol.wait before it reads
+// anything the previous kernels wrote, so stream semantics are unchanged.  Used along the codec
+// step's chain of mostly-empty kernels (redo emit, Huffman side, general decoder), whose launch and
+// placement latency would otherwise add to the step.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
 // can state how many of OUR kernels a region launched.
