@@ -1579,14 +1579,19 @@ int drain(zc_comm* c) {
     clock_gettime(CLOCK_MONOTONIC, &ts);
     return static_cast<unsigned long long>(ts.tv_sec) * 1000000000ull + static_cast<unsigned long long>(ts.tv_nsec);
   };
-  unsigned long long last = now(), spins = 0;
+  const unsigned long long t_enter = now();
+  unsigned long long last = t_enter;
   bool have = false;
   for (;;) {
     const cudaError_t q = cudaStreamQuery(c->stream);
     if (q == cudaSuccess) return ZC_OK;
     if (q != cudaErrorNotReady) return cuda_err(q, "collective");
-    if (++spins < 2000) {  // the common case: done within a few ms, no sampling
-      usleep(spins < 200 ? 5 : 50);
+    // the common case: done within a few ms.  Busy-poll the first 2 ms (a sleep of even 5 us costs
+    // the timer slack, ~60 us, per rank drained), then poll every 50 us and sample the flags.
+    const unsigned long long el = now() - t_enter;
+    if (el < 2000000ull) continue;
+    if (el < 20000000ull) {
+      usleep(50);
       continue;
     }
     usleep(2000);

@@ -30,12 +30,12 @@ def laplacian(count, rank):
     return (-1e-2 * torch.sign(u) * torch.log1p(-2 * u.abs())).float()
 
 
-def run(n, count, pin, reps, warmup):
+def run(n, count, pin, reps, warmup, shared=True):
     xs = [laplacian(count, r) for r in range(n)]
     gmax = max(float(x.abs().max().item()) for x in xs)
     rel = 1e-4 / gmax
     grp = zcomm.Group(n, cfg=zcomm.collective_config(pin))
-    if pin in (abi.PIN_AUTO, abi.PIN_HUFFMAN):
+    if pin == abi.PIN_HUFFMAN or (pin == abi.PIN_AUTO and shared):
         scale = 2 * rel * gmax
         grp.set_shared_huffman_from_bytes(zcomm.eb_quantize_with_scale(xs[0][: 1 << 20], scale).cpu().numpy().view("uint8"))
     outs = [torch.empty_like(x) for x in xs]
@@ -64,6 +64,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--out", default="profiles/sweep")
+    ap.add_argument("--no-shared", action="store_true",
+                    help="Auto without a shared Huffman context (FixedLen / RAW only: the fused ring kernel runs)")
     args = ap.parse_args()
     rows = []
     for n in args.ranks:
@@ -71,7 +73,7 @@ def main():
             count = mb * (1 << 20) // 4
             t_raw = None
             for name, pin in PINS:
-                dt, wall, w = run(n, count, pin, args.reps, args.warmup)
+                dt, wall, w = run(n, count, pin, args.reps, args.warmup, shared=not args.no_shared)
                 if name == "raw":
                     t_raw = dt
                 r = report.ReportRow(collective=0, ranks=n, msg_bytes=4 * count, codec=CODEC_INDEX[name], quant=1,
