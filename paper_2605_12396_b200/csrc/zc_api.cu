@@ -35,6 +35,7 @@ std::atomic<uint64_t>& launch_counter() {
   return n;
 }
 void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+void note_launches(uint64_t k) { launch_counter().fetch_add(k, std::memory_order_relaxed); }
 
 namespace {
 std::atomic<int> g_inflight{0};

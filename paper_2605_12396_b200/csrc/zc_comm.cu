@@ -23,6 +23,7 @@
 // releases the local waits so the stream drains.
 #include <cuda.h>
 #include <time.h>
+#include <ucontext.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -30,6 +31,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <condition_variable>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -489,6 +492,10 @@ struct zc_comm {
   zc_collective_config cfg{};
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr;  // orders the collective after the caller's stream
+  uint32_t* h_err = nullptr;     // pinned host copy of the error word, queued behind a group's work
+  bool h_err_queued = false;
+  cudaEvent_t ev_join = nullptr;  // fork / join of a captured group collective
+  uint64_t gen = 0;               // bumped by every change that invalidates captured collectives
   Layout lay{};
   uint8_t* block = nullptr;
   std::vector<uint8_t*> peer;      // every rank's block base, valid on this device
@@ -623,15 +630,20 @@ bool signal_posted(const void* addr, unsigned long long v) {
   return it != m.end() && it->second >= v;
 }
 
+// The ranks' enqueue bodies run as fibers (ucontext) on the calling thread: a hand-off is a
+// user-level context switch (~1 us) instead of a thread wake-up, and no thread is created per call.
 struct Baton {
-  std::mutex mu;
-  std::condition_variable cv;
-  int n = 0, turn = 0;
+  int n = 0, cur = 0;
   std::vector<int> state;  // 0 runnable, 1 waiting for a signal, 2 finished
   std::vector<const void*> w_addr;
   std::vector<unsigned long long> w_val;
-  // next rank to run after `r` (call with mu held); -1 when every rank has finished
-  int next_locked(int r) {
+  std::vector<ucontext_t> ctx;
+  ucontext_t sched;
+  std::function<int(int)> body;
+  std::vector<int>* rcs = nullptr;
+  std::vector<std::string>* msgs = nullptr;
+  // next rank to run after `r`; -1 when every rank has finished
+  int next(int r) {
     for (int k = 1; k <= n; ++k) {
       const int q = (r + k) % n;
       if (state[q] == 0 || (state[q] == 1 && signal_posted(w_addr[q], w_val[q]))) return q;
@@ -644,56 +656,71 @@ struct Baton {
 thread_local Baton* tl_baton = nullptr;
 thread_local int tl_rank = -1;
 
-// Called by a rank thread before it enqueues a wait for *addr >= v.
+// Called by a rank body before it enqueues a wait for *addr >= v: yields to the scheduler.
 void baton_wait(const void* addr, unsigned long long v) {
   Baton* b = tl_baton;
   if (b == nullptr || signal_posted(addr, v)) return;
-  std::unique_lock<std::mutex> lk(b->mu);
   const int r = tl_rank;
   b->state[r] = 1;
   b->w_addr[r] = addr;
   b->w_val[r] = v;
-  const int q = b->next_locked(r);
-  b->turn = q < 0 ? r : q;
-  b->state[b->turn] = 0;
-  b->cv.notify_all();
-  b->cv.wait(lk, [&] { return b->turn == r; });
-  b->state[r] = 0;
+  swapcontext(&b->ctx[static_cast<size_t>(r)], &b->sched);
 }
 
-// Runs enqueue(r) for every rank on its own thread under the baton; returns each rank's status
-// and error text.
-template <typename F>
-void baton_run(int n, F enqueue, std::vector<int>& rcs, std::vector<std::string>& msgs) {
+void baton_fiber() {
+  Baton* b = tl_baton;
+  const int r = tl_rank;
+  int rc;
+  try {
+    rc = b->body(r);
+  } catch (const std::exception& e) {
+    rc = set_err(ZC_ERR_RUNTIME, e.what());
+  }
+  (*b->rcs)[static_cast<size_t>(r)] = rc;
+  if (rc) (*b->msgs)[static_cast<size_t>(r)] = zc_last_error();
+  b->state[r] = 2;
+}  // returns into b->sched (uc_link)
+
+// Runs enqueue(r) for every rank under the baton; resume(r) restores per-rank host state (the
+// current device) whenever rank r is switched in.  Returns each rank's status and error text.
+template <typename F, typename R>
+void baton_run(int n, F enqueue, R resume, std::vector<int>& rcs, std::vector<std::string>& msgs) {
+  constexpr size_t kStack = 1u << 20;
+  static thread_local std::vector<std::unique_ptr<char[]>> stacks;
+  while (static_cast<int>(stacks.size()) < n) stacks.emplace_back(new char[kStack]);
   Baton b;
   b.n = n;
   b.state.assign(n, 0);
   b.w_addr.assign(n, nullptr);
   b.w_val.assign(n, 0);
+  b.ctx.resize(n);
+  b.body = enqueue;
   rcs.assign(n, ZC_OK);
   msgs.assign(n, std::string());
-  std::vector<std::thread> th;
-  for (int r = 0; r < n; ++r)
-    th.emplace_back([&, r] {
-      tl_baton = &b;
-      tl_rank = r;
-      {
-        std::unique_lock<std::mutex> lk(b.mu);
-        b.cv.wait(lk, [&] { return b.turn == r; });
-      }
-      rcs[r] = enqueue(r);
-      if (rcs[r]) msgs[r] = zc_last_error();
-      std::unique_lock<std::mutex> lk(b.mu);
-      b.state[r] = 2;
-      const int q = b.next_locked(r);
-      if (q >= 0) {
-        b.turn = q;
-        b.state[q] = 0;
-      }
-      b.cv.notify_all();
-      tl_baton = nullptr;
-    });
-  for (auto& t : th) t.join();
+  b.rcs = &rcs;
+  b.msgs = &msgs;
+  Baton* const outer = tl_baton;
+  const int outer_rank = tl_rank;
+  tl_baton = &b;
+  std::vector<bool> started(n, false);
+  for (int r = 0; r >= 0;) {
+    tl_rank = r;
+    b.state[r] = 0;
+    if (!started[r]) {
+      started[r] = true;
+      getcontext(&b.ctx[r]);
+      b.ctx[r].uc_stack.ss_sp = stacks[r].get();
+      b.ctx[r].uc_stack.ss_size = kStack;
+      b.ctx[r].uc_link = &b.sched;
+      makecontext(&b.ctx[r], baton_fiber, 0);
+    } else {
+      resume(r);
+    }
+    swapcontext(&b.sched, &b.ctx[r]);
+    r = b.next(r);
+  }
+  tl_baton = outer;
+  tl_rank = outer_rank;
 }
 
 // Stream memory operations on this rank's stream.  Waits are always on the rank's own block.
@@ -722,7 +749,7 @@ int stream_wait_geq(zc_comm* c, const void* flag, unsigned long long v) {
   baton_wait(flag, v);
   const CUresult r = memops().wait(reinterpret_cast<CUstream>(c->stream), reinterpret_cast<CUdeviceptr>(flag), v,
                                    c->wait_flags);
-  return r == CUDA_SUCCESS ? ZC_OK : set_err(ZC_ERR_CUDA, "cuStreamWaitValue64 failed");
+  return r == CUDA_SUCCESS ? ZC_OK : set_err(ZC_ERR_CUDA, "cuStreamWaitValue64 failed (CUresult " + std::to_string(r) + ")");
 }
 int stream_write(zc_comm* c, void* addr, unsigned long long v) {
   post_signal(addr, v);
@@ -1565,14 +1592,16 @@ void release_rank(zc_comm* c, uint32_t bit);
 // timeout of their own, so while it runs the rank's flag words are sampled; when none has moved
 // for the communicator's timeout, every rank is poisoned (ZC_DERR_TIMEOUT, the reference's link
 // poisoning) and this rank's flags are released so its stream drains.
-int drain(zc_comm* c) {
-  if (!c->memops) return cuda_err(cudaStreamSynchronize(c->stream), "collective");
-  const Layout& y = c->lay;
+int drain_watch(zc_comm* const* cs, int n, cudaStream_t stream) {
+  const Layout& y = cs[0]->lay;
   const uint64_t lo = y.off_sready, hi = y.off_err;  // sready, scredit
-  std::vector<uint8_t> snap(hi - lo + 8ull * kMaxRanks), cur(snap.size());
+  const size_t per = hi - lo + 8ull * kMaxRanks;
+  std::vector<uint8_t> snap(per * n), cur(snap.size());
   auto sample = [&](std::vector<uint8_t>& v) {
-    cudaMemcpy(v.data(), c->block + lo, hi - lo, cudaMemcpyDeviceToHost);
-    cudaMemcpy(v.data() + (hi - lo), c->block + y.off_mflag, 8ull * kMaxRanks, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < n; ++i) {
+      cudaMemcpy(v.data() + per * i, cs[i]->block + lo, hi - lo, cudaMemcpyDeviceToHost);
+      cudaMemcpy(v.data() + per * i + (hi - lo), cs[i]->block + y.off_mflag, 8ull * kMaxRanks, cudaMemcpyDeviceToHost);
+    }
   };
   auto now = [] {
     timespec ts;
@@ -1583,7 +1612,7 @@ int drain(zc_comm* c) {
   unsigned long long last = t_enter;
   bool have = false;
   for (;;) {
-    const cudaError_t q = cudaStreamQuery(c->stream);
+    const cudaError_t q = cudaStreamQuery(stream);
     if (q == cudaSuccess) return ZC_OK;
     if (q != cudaErrorNotReady) return cuda_err(q, "collective");
     // the common case: done within a few ms.  Busy-poll the first 2 ms (a sleep of even 5 us costs
@@ -1604,28 +1633,70 @@ int drain(zc_comm* c) {
     }
     // a peer poisoned the link (its abort or its own timeout): no need to wait out our timeout
     uint32_t pe = 0;
-    cudaMemcpy(&pe, c->err_word(), 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&pe, cs[0]->err_word(), 4, cudaMemcpyDeviceToHost);
     if ((pe & (ZC_DERR_ABORT | ZC_DERR_TIMEOUT)) && now() - last > 50ull * 1000 * 1000) {
-      release_rank(c, 0);
-      return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+      for (int i = 0; i < n; ++i) release_rank(cs[i], 0);
+      return cuda_err(cudaStreamSynchronize(stream), "collective");
     }
-    if (now() - last < c->timeout_ns) continue;
-    for (int r = 0; r < c->nranks; ++r) {  // poison every rank (link poisoning), release our waits
+    if (now() - last < cs[0]->timeout_ns) continue;
+    for (int r = 0; r < cs[0]->nranks; ++r) {  // poison every rank (link poisoning), release our waits
       uint32_t e = 0;
-      cudaMemcpy(&e, c->peer[r] + y.off_err, 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&e, cs[0]->peer[r] + y.off_err, 4, cudaMemcpyDeviceToHost);
       e |= ZC_DERR_TIMEOUT;
-      cudaMemcpy(c->peer[r] + y.off_err, &e, 4, cudaMemcpyHostToDevice);
+      cudaMemcpy(cs[0]->peer[r] + y.off_err, &e, 4, cudaMemcpyHostToDevice);
     }
-    release_rank(c, ZC_DERR_TIMEOUT);
-    return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+    for (int i = 0; i < n; ++i) release_rank(cs[i], ZC_DERR_TIMEOUT);
+    return cuda_err(cudaStreamSynchronize(stream), "collective");
   }
 }
 
-int finish(zc_comm* c) {
-  if (int rc = drain(c)) return rc;
+int drain(zc_comm* c) {
+  if (!c->memops) return cuda_err(cudaStreamSynchronize(c->stream), "collective");
+  return drain_watch(&c, 1, c->stream);
+}
+
+// Pinned host words for the error-word read-back (process lifetime: freeing pinned memory would
+// synchronise the device while other communicators may have waits in flight).
+uint32_t* pinned_err_slot() {
+  static std::mutex mu;
+  static std::vector<uint32_t*> free_slots;
+  std::lock_guard<std::mutex> g(mu);
+  if (free_slots.empty()) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 4096, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    for (int i = 0; i < 4096 / 64; ++i) free_slots.push_back(reinterpret_cast<uint32_t*>(static_cast<char*>(p) + 64 * i));
+  }
+  uint32_t* s = free_slots.back();
+  free_slots.pop_back();
+  return s;
+}
+
+// Queues the error word's copy to host behind the collective, so finish needs no extra round trip.
+int queue_err_readback(zc_comm* c) {
+  if (c->h_err == nullptr && (c->h_err = pinned_err_slot()) == nullptr) return ZC_OK;
+  if (cudaMemcpyAsync(c->h_err, c->err_word(), 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) return ZC_OK;
+  c->h_err_queued = true;
+  return ZC_OK;
+}
+
+// The collective's status once its work has drained.
+int status_after_drain(zc_comm* c) {
+  const bool queued = c->h_err_queued;
+  c->h_err_queued = false;
   uint32_t e = 0;
-  if (int rc = cuda_err(cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost), "error word")) return rc;
+  if (queued)
+    e = *reinterpret_cast<volatile uint32_t*>(c->h_err);
+  else if (int rc = cuda_err(cudaMemcpy(&e, c->err_word(), 4, cudaMemcpyDeviceToHost), "error word"))
+    return rc;
   return status_from_err(e);
+}
+
+int finish(zc_comm* c) {
+  if (int rc = drain(c)) {
+    c->h_err_queued = false;
+    return rc;
+  }
+  return status_after_drain(c);
 }
 
 int alloc_comm(int rank, int nranks, int device, const zc_collective_config* cfg, zc_comm** out) {
@@ -1731,16 +1802,25 @@ void release_rank(zc_comm* c, uint32_t bit) {
 
 // Single-process group: every rank's collective is enqueued by its own host thread under the
 // baton (see baton_run), then each rank's stream is drained; on failure every rank is reset.
+double mono_us() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<double>(ts.tv_sec) * 1e6 + static_cast<double>(ts.tv_nsec) * 1e-3;
+}
+
 template <typename F>
 int run_group_inner(zc_comm* const* cs, int n, F enqueue) {
   InFlight inflight;
   std::vector<int> rcs;
   std::vector<std::string> msgs;
+  static const bool host_timing = std::getenv("ZC_HOST_TIMING") != nullptr;
+  const double t0 = host_timing ? mono_us() : 0.0;
   baton_run(n, [&](int r) -> int {
     if (int rc = dev_guard(cs[r])) return rc;
     if (int rc = order_after(cs[r], nullptr)) return rc;
-    return enqueue(r);
-  }, rcs, msgs);
+    if (int rc = enqueue(r)) return rc;
+    return queue_err_readback(cs[r]);
+  }, [&](int r) { dev_guard(cs[r]); }, rcs, msgs);
   int first = ZC_OK;
   std::string msg;
   for (int r = 0; r < n; ++r)
@@ -1753,9 +1833,142 @@ int run_group_inner(zc_comm* const* cs, int n, F enqueue) {
       dev_guard(cs[r]);
       release_rank(cs[r], ZC_DERR_ABORT);
     }
+  const double t1 = host_timing ? mono_us() : 0.0;
   for (int r = 0; r < n; ++r) {
     dev_guard(cs[r]);
     int e = finish(cs[r]);
+    if (!first && e) {
+      first = e;
+      msg = zc_last_error();
+    }
+  }
+  if (host_timing) std::fprintf(stderr, "zc host: enqueue %.1f us, drain %.1f us\n", t1 - t0, mono_us() - t1);
+  if (first) {
+    for (int r = 0; r < n; ++r) reset_state(cs[r]);
+    set_err(first, msg);
+  }
+  return first;
+}
+
+// ---- captured group collectives.  A single-process group call is synchronous, so between two
+// calls every flag is quiescent.  A collective enqueued from zeroed flags and zeroed host counters
+// therefore issues the same operations with the same flag values every time it is called with the
+// same arguments: it is captured once as a CUDA graph (every rank's stream forked from rank 0's,
+// the flag words zeroed by the graph's first nodes) and replayed.  A replay leaves the host
+// counters where the capture left them, and adds the capture's host-side accounting (control
+// frames, launch count).  Anything that cannot be captured falls back to the eager path.
+struct HostCounters {
+  uint64_t tx_seq = 0, rx_seq = 0, ptx = 0, prx = 0, rtx = 0, rrx = 0;
+  std::vector<uint64_t> p2p_tx, p2p_rx;
+  unsigned long long epoch = 0;
+};
+HostCounters save_counters(const zc_comm* c) {
+  HostCounters h;
+  h.tx_seq = c->tx_seq;
+  h.rx_seq = c->rx_seq;
+  h.ptx = c->ptx;
+  h.prx = c->prx;
+  h.rtx = c->rtx;
+  h.rrx = c->rrx;
+  h.p2p_tx = c->p2p_tx;
+  h.p2p_rx = c->p2p_rx;
+  h.epoch = c->epoch;
+  return h;
+}
+void load_counters(zc_comm* c, const HostCounters& h) {
+  c->tx_seq = h.tx_seq;
+  c->rx_seq = h.rx_seq;
+  c->ptx = h.ptx;
+  c->prx = h.prx;
+  c->rtx = h.rtx;
+  c->rrx = h.rrx;
+  c->p2p_tx = h.p2p_tx;
+  c->p2p_rx = h.p2p_rx;
+  c->epoch = h.epoch;
+}
+void zero_counters(zc_comm* c) {
+  HostCounters z;
+  z.p2p_tx.assign(c->p2p_tx.size(), 0);
+  z.p2p_rx.assign(c->p2p_rx.size(), 0);
+  load_counters(c, z);
+}
+
+struct GroupGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<zc_comm*> cs;
+  std::vector<HostCounters> end;
+  std::vector<zc_wire_stats> wire;  // host-side accounting of one call, per rank
+  uint64_t launches = 0;
+  uint64_t last_use = 0;
+  int fails = 0;  // failed captures (a first call may allocate lazily: it is retried once)
+  bool eager_only = false;
+};
+std::mutex g_graph_mu;
+std::unordered_map<std::string, GroupGraph>& graph_cache() {
+  static std::unordered_map<std::string, GroupGraph> m;
+  return m;
+}
+uint64_t g_graph_clock = 0;
+constexpr size_t kMaxGraphs = 64;
+
+void drop_graph(GroupGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+}
+void forget_graphs_of(const zc_comm* c) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  auto& m = graph_cache();
+  for (auto it = m.begin(); it != m.end();) {
+    if (std::find(it->second.cs.begin(), it->second.cs.end(), c) != it->second.cs.end()) {
+      drop_graph(it->second);
+      it = m.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// Not under a profiler or sanitizer (CUDA_INJECTION64_PATH): those serialise kernels in launch
+// order, which the eager path's baton ordering is built for; a graph's branch order is not.
+bool tool_attached() {
+  for (char** e = environ; e && *e; ++e)
+    if (std::strstr(*e, "INJECTION") != nullptr && std::strchr(*e, '=') > std::strstr(*e, "INJECTION")) return true;
+  return std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr;
+}
+bool graphs_enabled() {
+  static const bool on = std::getenv("ZC_GROUP_NOGRAPH") == nullptr && !tool_attached();
+  return on;
+}
+
+// Key of a captured collective: the operation and its arguments, the communicators and their
+// generations.
+struct GraphKey {
+  std::string k;
+  template <typename T>
+  GraphKey& add(const T& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+    return *this;
+  }
+  template <typename T>
+  GraphKey& add_n(const T* v, int n) {
+    for (int i = 0; i < n; ++i) add(v[i]);
+    return *this;
+  }
+};
+
+void add_wire(zc_wire_stats& a, const zc_wire_stats& d, int sign) {
+  for (int i = 0; i < 3; ++i) a.frames_by_codec[i] += sign * d.frames_by_codec[i];
+  a.raw_bytes += sign * d.raw_bytes;
+  a.payload_bytes += sign * d.payload_bytes;
+  a.total_bytes += sign * d.total_bytes;
+}
+
+int graph_status(zc_comm* const* cs, int n, int drc) {
+  int first = drc;
+  std::string msg = drc ? zc_last_error() : std::string();
+  for (int r = 0; r < n; ++r) {
+    dev_guard(cs[r]);
+    const int e = status_after_drain(cs[r]);
     if (!first && e) {
       first = e;
       msg = zc_last_error();
@@ -1768,9 +1981,167 @@ int run_group_inner(zc_comm* const* cs, int n, F enqueue) {
   return first;
 }
 
+// Captures enqueue (every rank, from zeroed counters) into a graph; nullptr exec on failure (the
+// streams are then out of capture and nothing was run).
 template <typename F>
-int run_group(zc_comm* const* cs, int n, F enqueue) {
-  const int rc = run_group_inner(cs, n, enqueue);
+cudaGraphExec_t capture_group(zc_comm* const* cs, int n, F enqueue) {
+  for (int r = 0; r < n; ++r) {
+    zc_comm* c = cs[r];
+    dev_guard(c);
+    zero_counters(c);
+    forget_signals(c->block + c->lay.off_ready, c->block + c->lay.off_wire);
+    if (c->ev_join == nullptr && cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+  }
+  zc_comm* o = cs[0];
+  dev_guard(o);
+  if (cudaStreamBeginCapture(o->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  bool ok = true;
+  for (int r = 0; r < n && ok; ++r)
+    ok = cudaMemsetAsync(cs[r]->block + cs[r]->lay.off_ready, 0, cs[r]->lay.off_wire - cs[r]->lay.off_ready,
+                         o->stream) == cudaSuccess;
+  ok = ok && cudaEventRecord(o->ev_join, o->stream) == cudaSuccess;
+  std::vector<int> rcs;
+  std::vector<std::string> msgs;
+  // Inside a graph the flag waits and writes are tiny kernels (wait_geq_kernel, flag stores, the
+  // one-kernel mailbox): a kernel node launches in ~2 us where a memory-operation node costs ~5 us
+  // of device latency and ~1 us of host time at every launch, and a spinning one-thread kernel
+  // never blocks an independent branch the way a queued wait operation can.
+  static const bool keep_memops = std::getenv("ZC_GRAPH_MEMOPS") != nullptr;
+  std::vector<bool> had(n);
+  for (int r = 0; r < n; ++r) {
+    had[r] = cs[r]->memops;
+    if (!keep_memops) cs[r]->memops = false;
+  }
+  if (ok) {
+    baton_run(n, [&](int r) -> int {
+      zc_comm* c = cs[r];
+      if (int rc = dev_guard(c)) return rc;
+      if (r && cudaStreamWaitEvent(c->stream, o->ev_join, 0) != cudaSuccess) return set_err(ZC_ERR_CUDA, "fork");
+      if (int rc = enqueue(r)) return rc;
+      queue_err_readback(c);
+      if (r && cudaEventRecord(c->ev_join, c->stream) != cudaSuccess) return set_err(ZC_ERR_CUDA, "join");
+      return ZC_OK;
+    }, [&](int r) { dev_guard(cs[r]); }, rcs, msgs);
+    for (int r = 0; r < n; ++r) ok = ok && rcs[r] == ZC_OK;
+  }
+  for (int r = 0; r < n; ++r) cs[r]->memops = had[r];
+  dev_guard(o);
+  for (int r = 1; r < n && ok; ++r) ok = cudaStreamWaitEvent(o->stream, cs[r]->ev_join, 0) == cudaSuccess;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(o->stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (ok && ec == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (std::getenv("ZC_HOST_TIMING") && (!ok || ec != cudaSuccess || !exec)) {
+    std::fprintf(stderr, "zc graph: capture failed (%s)", cudaGetErrorString(ec));
+    for (size_t r = 0; r < rcs.size(); ++r) std::fprintf(stderr, " [rank %zu rc %d %s]", r, rcs[r], msgs[r].c_str());
+    std::fprintf(stderr, "\n");
+  }
+  if (!ok || ec != cudaSuccess) {
+    if (exec) cudaGraphExecDestroy(exec);
+    return nullptr;
+  }
+  return exec;
+}
+
+template <typename F>
+int run_group(zc_comm* const* cs, int n, F enqueue, const GraphKey* key = nullptr) {
+  bool graph_ok = key != nullptr && n > 1 && graphs_enabled();
+  for (int r = 0; r < n && graph_ok; ++r)
+    graph_ok = cs[r]->memops && cs[r]->tl_cap == 0 && cs[r]->device == cs[0]->device;
+  if (!graph_ok) {
+    const int rc = run_group_inner(cs, n, enqueue);
+    flush_deferred_if_idle();
+    return rc;
+  }
+  const double t0 = mono_us();
+  GraphKey k = *key;
+  for (int r = 0; r < n; ++r) k.add(cs[r]).add(cs[r]->gen);
+  InFlight inflight;
+  std::unique_lock<std::mutex> lk(g_graph_mu);
+  auto& m = graph_cache();
+  auto it = m.find(k.k);
+  if (it != m.end() && it->second.eager_only) {
+    lk.unlock();
+    const int rc = run_group_inner(cs, n, enqueue);
+    flush_deferred_if_idle();
+    return rc;
+  }
+  zc_comm* o = cs[0];
+  if (it == m.end() || it->second.exec == nullptr) {
+    const int fails = it == m.end() ? 0 : it->second.fails;
+    lk.unlock();
+    std::vector<zc_wire_stats> w0(n);
+    for (int r = 0; r < n; ++r) w0[r] = cs[r]->host_wire;
+    const uint64_t l0 = zc_launch_count();
+    dev_guard(o);
+    if (int rc = order_after(o, nullptr)) return rc;
+    cudaGraphExec_t exec = capture_group(cs, n, enqueue);
+    GroupGraph g;
+    g.cs.assign(cs, cs + n);
+    if (exec == nullptr) {  // not capturable: from a clean state, eagerly (and from now on)
+      for (int r = 0; r < n; ++r) {
+        cs[r]->host_wire = w0[r];
+        reset_state(cs[r]);
+      }
+      g.fails = fails + 1;
+      g.eager_only = g.fails >= 2;
+      lk.lock();
+      m[k.k] = std::move(g);
+      lk.unlock();
+      const int rc = run_group_inner(cs, n, enqueue);
+      flush_deferred_if_idle();
+      return rc;
+    }
+    g.exec = exec;
+    g.launches = zc_launch_count() - l0;
+    for (int r = 0; r < n; ++r) {
+      g.end.push_back(save_counters(cs[r]));
+      zc_wire_stats d = cs[r]->host_wire;
+      add_wire(d, w0[r], -1);
+      g.wire.push_back(d);
+    }
+    lk.lock();
+    if (m.size() >= kMaxGraphs) {  // evict the least recently used
+      auto lru = m.begin();
+      for (auto j = m.begin(); j != m.end(); ++j)
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      drop_graph(lru->second);
+      m.erase(lru);
+    }
+    m.erase(k.k);
+    it = m.emplace(k.k, std::move(g)).first;
+    it->second.last_use = ++g_graph_clock;
+    lk.unlock();
+    dev_guard(o);
+    if (int rc = cuda_err(cudaGraphLaunch(exec, o->stream), "graph launch")) return rc;
+  } else {
+    GroupGraph& g = it->second;
+    g.last_use = ++g_graph_clock;
+    cudaGraphExec_t exec = g.exec;
+    for (int r = 0; r < n; ++r) {
+      load_counters(cs[r], g.end[r]);
+      add_wire(cs[r]->host_wire, g.wire[r], 1);
+      cs[r]->h_err_queued = true;
+    }
+    note_launches(g.launches);
+    lk.unlock();
+    dev_guard(o);
+    if (int rc = order_after(o, nullptr)) return rc;
+    if (int rc = cuda_err(cudaGraphLaunch(exec, o->stream), "graph launch")) return rc;
+  }
+  static const bool host_timing = std::getenv("ZC_HOST_TIMING") != nullptr;
+  const double t1 = host_timing ? mono_us() : 0.0;
+  const int drc = drain_watch(cs, n, o->stream);
+  const double t2 = host_timing ? mono_us() : 0.0;
+  const int rc = graph_status(cs, n, drc);
+  if (host_timing)
+    std::fprintf(stderr, "zc graph: launch %.1f us, drain %.1f us, status %.1f us\n", t1 - t0, t2 - t1, mono_us() - t2);
   flush_deferred_if_idle();
   return rc;
 }
@@ -1879,6 +2250,7 @@ int zc_comm_create_group(int nranks, const int* devices, const zc_collective_con
 
 void zc_comm_destroy(zc_comm* c) {
   if (!c) return;
+  forget_graphs_of(c);
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int r = 0; r < c->nranks; ++r)
@@ -1889,6 +2261,7 @@ void zc_comm_destroy(zc_comm* c) {
   release_device_memory(c->device, c->block, false);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->shared) zc_huff_ctx_destroy(c->shared);
   for (auto& t : c->tl) {
     cudaEventDestroy(t.e0);
@@ -1909,6 +2282,8 @@ int zc_comm_set_shared_huffman(zc_comm* c, const zc_huff_ctx* ctx) {
   zc_huff_ctx_code_lengths(ctx, lens);
   zc_huff_ctx* copy = nullptr;
   if (int rc = zc_huff_ctx_from_lengths(lens, &copy)) return rc;
+  forget_graphs_of(c);  // captured collectives hold the old tables
+  ++c->gen;
   if (c->shared) zc_huff_ctx_destroy(c->shared);
   c->shared = copy;
   if (int rc = dev_guard(c)) return rc;
@@ -2035,6 +2410,7 @@ int zc_comm_timeline_enable(zc_comm* c, int32_t max_pieces) {
   if (max_pieces < 0) return set_err(ZC_ERR_INVALID_ARGUMENT, "max_pieces must be >= 0");
   if (int rc = dev_guard(c)) return rc;
   cudaStreamSynchronize(c->stream);
+  ++c->gen;
   for (auto& t : c->tl) {
     cudaEventDestroy(t.e0);
     cudaEventDestroy(t.e1);
@@ -2204,7 +2580,10 @@ int zc_comm_reset_stats(zc_comm* c) {
 // Communicator::run analogue; ranks' kernels must run concurrently).
 int zc_group_allreduce_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count, int32_t mode,
                            double* h_scales, uint32_t levels) {
-  int rc = run_group(cs, n, [&](int r) { return enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels); });
+  GraphKey key;
+  key.add(1).add_n(d_syms, n).add(count).add(mode).add_n(h_scales, n).add(levels);
+  int rc = run_group(cs, n, [&](int r) { return enqueue_allreduce_sym(cs[r], d_syms[r], count, mode, h_scales[r], levels); },
+                     &key);
   if (rc) return rc;
   for (int r = 0; r < n; ++r)
     if (n > 1 && count > 0) cudaMemcpy(&h_scales[r], &cs[r]->scal()->scale, 8, cudaMemcpyDeviceToHost);
@@ -2219,16 +2598,27 @@ int zc_group_allreduce_eb_f32(zc_comm* const* cs, int n, const float* const* d_x
     if (int rc = dev_guard(cs[r])) return rc;
     if (int rc = ensure_sym(cs[r], count)) return rc;
   }
-  return run_group(cs, n, [&](int r) { return enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel); });
+  GraphKey key;
+  key.add(2).add_n(d_xs, n).add_n(d_outs, n).add(out_f64).add(count).add(rel);
+  static const bool host_timing = std::getenv("ZC_HOST_TIMING") != nullptr;
+  const double t0 = host_timing ? mono_us() : 0.0;
+  const int rc = run_group(cs, n, [&](int r) { return enqueue_allreduce_eb(cs[r], d_xs[r], d_outs[r], out_f64, count, rel); },
+                           &key);
+  if (host_timing) std::fprintf(stderr, "zc eb: %.1f us\n", mono_us() - t0);
+  return rc;
 }
 
 int zc_group_allgather_sym(zc_comm* const* cs, int n, int32_t* const* d_alls, uint64_t block) {
-  return run_group(cs, n, [&](int r) { return enqueue_allgather(cs[r], d_alls[r], block); });
+  GraphKey key;
+  key.add(3).add_n(d_alls, n).add(block);
+  return run_group(cs, n, [&](int r) { return enqueue_allgather(cs[r], d_alls[r], block); }, &key);
 }
 
 int zc_group_reduce_scatter_sym(zc_comm* const* cs, int n, int32_t* const* d_syms, uint64_t count) {
   if (n == 1 || count == 0) return ZC_OK;
-  return run_group(cs, n, [&](int r) { return enqueue_ring(cs[r], d_syms[r], count, false); });
+  GraphKey key;
+  key.add(4).add_n(d_syms, n).add(count);
+  return run_group(cs, n, [&](int r) { return enqueue_ring(cs[r], d_syms[r], count, false); }, &key);
 }
 
 int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* outs) {
@@ -2257,13 +2647,17 @@ int zc_group_allreduce_max(zc_comm* const* cs, int n, const double* vs, double* 
 
 int zc_group_alltoall_sym(zc_comm* const* cs, int n, const int32_t* const* d_sends, int32_t* const* d_recvs,
                           uint64_t block) {
-  return run_group(cs, n, [&](int r) { return enqueue_alltoall(cs[r], d_sends[r], d_recvs[r], block); });
+  GraphKey key;
+  key.add(5).add_n(d_sends, n).add_n(d_recvs, n).add(block);
+  return run_group(cs, n, [&](int r) { return enqueue_alltoall(cs[r], d_sends[r], d_recvs[r], block); }, &key);
 }
 
 int zc_group_broadcast_sym(zc_comm* const* cs, int n, int32_t* const* d_datas, uint64_t count, int32_t root) {
   if (n == 1 || count == 0) return ZC_OK;
   if (root < 0 || root >= n) return set_err(ZC_ERR_INVALID_ARGUMENT, "broadcast root out of range");
-  return run_group(cs, n, [&](int r) { return enqueue_broadcast(cs[r], d_datas[r], count, root); });
+  GraphKey key;
+  key.add(6).add_n(d_datas, n).add(count).add(root);
+  return run_group(cs, n, [&](int r) { return enqueue_broadcast(cs[r], d_datas[r], count, root); }, &key);
 }
 
 int zc_group_execute(zc_comm* const* cs, int n, zc_coll_request* const* reqs, int32_t nreqs) {

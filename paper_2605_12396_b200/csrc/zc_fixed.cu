@@ -507,17 +507,25 @@ __device__ __forceinline__ void emit_row(uint32_t row, int lane, double scale, d
   }
 }
 
-// Grid sizing: a warp's contiguous share of the tiles is at least about CHUNK tiles.
+// Grid sizing: a warp's share of the tiles is about CHUNK tiles when the message fills the GPU;
+// a small message (the latency regime of small collectives) is spread one tile per warp instead.
 constexpr uint64_t CHUNK = 4;
-// The decoder's warp tile order: warp gw owns chunks gw, gw + tw, ... of CHUNK consecutive tiles
-// (chunks never straddle a unit), so the warps in flight write one advancing window of the output.
-__device__ __forceinline__ uint64_t tile_adv(uint64_t c, uint64_t tw) {
-  return ((c + 1) % CHUNK) != 0 ? c + 1 : c + 1 + (tw - 1) * CHUNK;
+// The decoder's warp tile order: warp gw owns chunks gw, gw + tw, ... of `ch` consecutive tiles
+// (ch divides the unit's tiles: chunks never straddle a unit), so the warps in flight write one
+// advancing window of the output.
+__device__ __forceinline__ uint64_t tile_adv(uint64_t c, uint64_t tw, uint32_t ch) {
+  return ((c + 1) % ch) != 0 ? c + 1 : c + 1 + (tw - 1) * ch;
 }
 // The warp's first tile at or past tile `ue` (a unit boundary), given its current tile c.
-__device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64_t tw) {
-  const uint64_t j = c / CHUNK, je = ue / CHUNK;
-  return (j + ((je - j + tw - 1) / tw) * tw) * CHUNK;
+__device__ __forceinline__ uint64_t tile_skip_to(uint64_t c, uint64_t ue, uint64_t tw, uint32_t ch) {
+  const uint64_t j = c / ch, je = ue / ch;
+  return (j + ((je - j + tw - 1) / tw) * tw) * ch;
+}
+// Tiles per warp chunk for a message of `ntiles` over `slots` warps the GPU can run.
+inline uint32_t chunk_for(uint64_t ntiles, uint64_t slots) {
+  uint64_t ch = CHUNK;
+  while (ch > 1 && ntiles < ch * slots) ch >>= 1;
+  return static_cast<uint32_t>(ch);
 }
 
 constexpr uint32_t kForeign = 0xFEu;  // unit owned by the general kernels
@@ -931,7 +939,7 @@ __device__ __forceinline__ void load_acc_row(const void* accp, int lane, double 
 
 struct DecSeq {  // a warp's tile sequence over owned units, with the view of the current unit
   uint64_t nfull, tw;
-  uint32_t ush, cu;
+  uint32_t ush, cu, ch;
   DecView cv;
   const uint8_t* views;  // shared-memory view table (units < DEC_VIEWS)
   __device__ __forceinline__ uint64_t next(const DecParams& p, uint64_t c) {
@@ -942,7 +950,7 @@ struct DecSeq {  // a warp's tile sequence over owned units, with the view of th
         cv = u < DEC_VIEWS ? unpack_view(views[u]) : dec_view(p, u);
       }
       if (cv.codec != kFallback) return c;
-      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) << ush, tw);
+      c = tile_skip_to(c, static_cast<uint64_t>(u + 1) << ush, tw, ch);
     }
     return nfull;
   }
@@ -951,7 +959,7 @@ struct DecSeq {  // a warp's tile sequence over owned units, with the view of th
 template <int OUT>
 __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant__ DecParams p,
                                                           const __grid_constant__ CUtensorMap tmap, uint64_t ntiles,
-                                                          uint64_t nfull) {
+                                                          uint64_t nfull, uint32_t ch) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
   pdl_trigger();  // the general decoder (its programmatic dependent) may be placed now
   uint8_t* s_tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
@@ -988,7 +996,8 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * DT_WARPS + warp;
   const uint32_t ush = unit_tile_shift(p.unit_bytes);
   const uint64_t umask = (1ull << ush) - 1;
-  DecSeq iss{nfull, tw, ush, 0xffffffffu, {kFallback, 0}, views}, prc{nfull, tw, ush, 0xffffffffu, {kFallback, 0}, views};
+  DecSeq iss{nfull, tw, ush, 0xffffffffu, ch, {kFallback, 0}, views},
+      prc{nfull, tw, ush, 0xffffffffu, ch, {kFallback, 0}, views};
   auto issue = [&](uint32_t st, uint64_t c) {  // lane 0: the packed rows of tile c into stage st
     const uint32_t u = static_cast<uint32_t>(c >> ush);
     const uint32_t bytes = 128u * iss.cv.width;
@@ -1000,15 +1009,15 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     if (OUT == OUT_ADD_I32) tma::prefetch_l2(static_cast<const int32_t*>(p.out) + c * TILE_ELEMS, TILE_BYTES);
     if (OUT == OUT_ADD_Q) tma::prefetch_l2(p.acc_f32 + c * TILE_ELEMS, TILE_BYTES);
   };
-  uint64_t c_issue = iss.next(p, gw * CHUNK);
+  uint64_t c_issue = iss.next(p, gw * ch);
   for (int i = 0; i < DSTAGES - 1; ++i) {
     if (c_issue < nfull) {
       if (lane == 0) issue(i, c_issue);
-      c_issue = iss.next(p, tile_adv(c_issue, tw));
+      c_issue = iss.next(p, tile_adv(c_issue, tw, ch));
     }
   }
   uint32_t k = 0;
-  for (uint64_t c = prc.next(p, gw * CHUNK); c < nfull; c = prc.next(p, tile_adv(c, tw)), ++k) {
+  for (uint64_t c = prc.next(p, gw * ch); c < nfull; c = prc.next(p, tile_adv(c, tw, ch)), ++k) {
     const uint32_t st = k % DSTAGES;
     // refill the stage that tile k-1 used once its store has read the buffer (the ring keeps
     // DSTAGES-1 loads in flight while this tile is decoded)
@@ -1018,7 +1027,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
         tma::bulk_wait_read<0>();
         issue(rs, c_issue);
       }
-      c_issue = iss.next(p, tile_adv(c_issue, tw));
+      c_issue = iss.next(p, tile_adv(c_issue, tw, ch));
     }
     tma::mbar_wait(&bars[st], (k / DSTAGES) & 1u);
     const uint32_t buf = tma::smem_u32(my + st * TILE_BYTES);
@@ -1040,7 +1049,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
     }
   }
   // the message's last, partial tile: symbol by symbol with byte-exact bounds
-  if (nfull < ntiles && gw == (nfull / CHUNK) % tw) {
+  if (nfull < ntiles && gw == (nfull / ch) % tw) {
     const uint32_t u = static_cast<uint32_t>(nfull >> ush);
     const DecView v = dec_view(p, u);
     if (u != mz_u) {
@@ -1103,7 +1112,7 @@ __global__ void __launch_bounds__(DT, 1) fl_decode_kernel(const __grid_constant_
 constexpr int FT_WARPS = 4;
 constexpr int FT = FT_WARPS * 32;
 constexpr int FT_CTAS = 3;   // per SM: 12 warps x 16 KiB of stages
-constexpr uint32_t FG = 8;   // tiles per warp task
+constexpr uint32_t FG = 8;   // tiles per warp task (fewer when the message does not fill the GPU)
 
 struct FusedUnit {
   uint32_t maxzz, wmz, adone, bdone;
@@ -1176,7 +1185,8 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int SINK>
 __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_constant__ FusedParams f, BUnit* us,
-                                                                 FusedUnit* fu, uint32_t* task_ctr, uint32_t lag) {
+                                                                 FusedUnit* fu, uint32_t* task_ctr, uint32_t lag,
+                                                                 uint32_t fg) {
   extern __shared__ __align__(128) uint8_t s_buf[];
   const EncParams& p = f.enc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1189,7 +1199,7 @@ __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_co
   const uint32_t unit_tiles = 1u << ush;
   const uint64_t lastR = p.total_bytes - static_cast<uint64_t>(U - 1) * p.unit_bytes;
   const uint32_t last_tiles = static_cast<uint32_t>((lastR / 4 + TILE_ELEMS - 1) / TILE_ELEMS);  // incl. partial
-  const uint32_t G = (unit_tiles + FG - 1) / FG, GL = (last_tiles + FG - 1) / FG;
+  const uint32_t G = (unit_tiles + fg - 1) / fg, GL = (last_tiles + fg - 1) / fg;
   const uint32_t ntasks = 2 * ((U - 1) * G + GL);
   const double scale = SINK == OUT_ADD_Q ? f.dscale[0] : 1.0, rcp = SINK == OUT_ADD_Q ? f.dscale[1] : 1.0;
   uint32_t err = 0;
@@ -1218,7 +1228,7 @@ __global__ void __launch_bounds__(FT, FT_CTAS) ring_fused_kernel(const __grid_co
     const uint64_t R = unit_R(p, u);
     const uint64_t n_elem = R / 4;
     const uint32_t tiles_u = static_cast<uint32_t>((n_elem + TILE_ELEMS - 1) / TILE_ELEMS);
-    const uint32_t t0 = g * FG, t1 = min(tiles_u, t0 + FG);
+    const uint32_t t0 = g * fg, t1 = min(tiles_u, t0 + fg);
     const uint32_t tf1 = min(t1, static_cast<uint32_t>(n_elem / TILE_ELEMS));  // full tiles: [t0, tf1)
     const uint64_t ebase = static_cast<uint64_t>(u) * (p.unit_bytes / 4);  // unit's first element in the piece
     FusedUnit& F = fu[u];
@@ -1530,7 +1540,8 @@ cudaError_t launch_fixed_emit_m(const EncParams& p, void* scratch, uint64_t tota
   g.total = total_slices;
   g.fast = 1;
   g.spec = mode == 1 ? 1u : 0u;
-  const uint64_t want = (ntiles + ET_WARPS * CHUNK - 1) / (ET_WARPS * CHUNK);
+  const uint64_t ech = chunk_for(ntiles, static_cast<uint64_t>(ET_CTAS) * sms * ET_WARPS);  // warps' shares are contiguous
+  const uint64_t want = (ntiles + ET_WARPS * ech - 1) / (ET_WARPS * ech);
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(ET_CTAS) * sms)));
   note_launch();
   const BUnit* us = static_cast<const BUnit*>(scratch);
@@ -1593,17 +1604,18 @@ cudaError_t launch_fixed_decode(const DecParams& p, cudaStream_t s) {
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   if (rows > 0 && !make_row_tensor_map(&map, p.out, rows)) return cudaErrorInvalidValue;
-  const uint64_t want = (ntiles + DT_WARPS * CHUNK - 1) / (DT_WARPS * CHUNK);
+  const uint32_t ch = chunk_for(ntiles, static_cast<uint64_t>(sms) * DT_WARPS);
+  const uint64_t want = (ntiles + DT_WARPS * ch - 1) / (DT_WARPS * ch);
   const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms))));
   note_launch();
   if (p.out_kind == OUT_F32)
-    fl_decode_kernel<OUT_F32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+    fl_decode_kernel<OUT_F32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull, ch);
   else if (p.out_kind == OUT_ADD_I32)
-    fl_decode_kernel<OUT_ADD_I32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+    fl_decode_kernel<OUT_ADD_I32><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull, ch);
   else if (p.out_kind == OUT_ADD_Q)
-    fl_decode_kernel<OUT_ADD_Q><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+    fl_decode_kernel<OUT_ADD_Q><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull, ch);
   else
-    fl_decode_kernel<OUT_BYTES><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull);
+    fl_decode_kernel<OUT_BYTES><<<grid, DT, DEC_SMEM, s>>>(p, map, ntiles, nfull, ch);
   return cudaGetLastError();
 }
 
@@ -1629,14 +1641,16 @@ cudaError_t launch_ring_fused(const FusedParams& f, void* scratch, cudaStream_t 
     cudaFuncSetAttribute(ring_fused_kernel<OUT_ADD_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(FT_SMEM));
   }
   const uint64_t tiles = (f.enc.total_bytes / 4 + TILE_ELEMS - 1) / TILE_ELEMS;
-  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + FG * FT_WARPS - 1) / (FG * FT_WARPS), static_cast<uint64_t>(FT_CTAS) * sms)));
+  uint32_t fg = FG;
+  while (fg > 1 && tiles < static_cast<uint64_t>(fg) * FT_CTAS * sms * FT_WARPS) fg >>= 1;
+  const uint32_t grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + fg * FT_WARPS - 1) / (fg * FT_WARPS), static_cast<uint64_t>(FT_CTAS) * sms)));
   note_launch();
-  const uint32_t G = static_cast<uint32_t>(((f.enc.unit_bytes / TILE_BYTES) + FG - 1) / FG);
+  const uint32_t G = static_cast<uint32_t>(((f.enc.unit_bytes / TILE_BYTES) + fg - 1) / fg);
   const uint32_t lag = static_cast<uint32_t>(std::max<uint64_t>(1, (static_cast<uint64_t>(grid) * FT_WARPS + G - 1) / G + 1));
   if (f.sink == OUT_ADD_Q)
-    ring_fused_kernel<OUT_ADD_Q><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag);
+    ring_fused_kernel<OUT_ADD_Q><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag, fg);
   else
-    ring_fused_kernel<OUT_ADD_I32><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag);
+    ring_fused_kernel<OUT_ADD_I32><<<grid, FT, FT_SMEM, s>>>(f, us, fu, ctr, lag, fg);
   return cudaGetLastError();
 }
 

@@ -166,6 +166,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // Every kernel launch of the library bumps one process-wide counter (zc_launch_count), so callers
 // can state how many of OUR kernels a region launched.
 void note_launch();
+void note_launches(uint64_t k);  // a replayed graph's launches
 // Function attributes (cudaFuncSetAttribute) are per device: true the first time the current
 // device is seen by the caller's `mask`.
 inline bool first_on_device(std::atomic<uint64_t>& mask) {
