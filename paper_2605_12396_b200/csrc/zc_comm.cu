@@ -198,7 +198,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-enum MailOp : int { MAIL_MAX = 0, MAIL_META = 1, MAIL_EB_SCALE = 2, MAIL_BARRIER = 3 };
+// MAIL_EB_META: allreduce_eb's two control exchanges (the absmax for the shared scale, then the
+// StreamMeta check with that scale) in one round: the record is the StreamMeta with the rank's
+// absmax in its unused tail; the shared scale is a function of the maximum, so every rank's
+// StreamMeta scale would be the same and no requantization can follow.
+enum MailOp : int { MAIL_MAX = 0, MAIL_META = 1, MAIL_EB_SCALE = 2, MAIL_BARRIER = 3, MAIL_EB_META = 4 };
 
 struct MailArgs {
   uint8_t* const* peers;  // device array: every rank's block base
@@ -224,8 +228,9 @@ __device__ __forceinline__ void mail_record(const MailArgs& a, uint32_t (&rec)[8
   for (int i = 0; i < 8; ++i) rec[i] = a.rec[i];
   if (a.rec_from_absmax) {
     unsigned long long b = __double_as_longlong(a.scal->absmax);
-    rec[0] = static_cast<uint32_t>(b);
-    rec[1] = static_cast<uint32_t>(b >> 32);
+    const int at = a.op == MAIL_EB_META ? 6 : 0;
+    rec[at] = static_cast<uint32_t>(b);
+    rec[at + 1] = static_cast<uint32_t>(b >> 32);
   }
   if (a.rec_scale_from_scal) {
     unsigned long long b = __double_as_longlong(a.scal->scale);
@@ -249,7 +254,28 @@ __device__ void mail_reduce(const MailArgs& a) {
   const int par = static_cast<int>(a.epoch & 1);
   const uint8_t* mb = a.peers[a.rank] + a.off_mbox + par * kMaxRanks * 32;
   Scal* s = a.scal;
-  if (a.op == MAIL_MAX || a.op == MAIL_EB_SCALE) {
+  if (a.op == MAIL_EB_META) {
+    double m = 0.0;
+    bool mismatch = false;
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(mb + a.rank * 32);
+    for (int r = 0; r < a.nranks; ++r) {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(mb + r * 32);
+      const double v = __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(q[6]) |
+                                                                   (static_cast<unsigned long long>(q[7]) << 32)));
+      m = r == 0 ? v : fmax(m, v);
+      if ((q[0] & 0xFF) != (mine[0] & 0xFF) || q[1] != mine[1] || q[2] != mine[2] || q[3] != mine[3]) mismatch = true;
+    }
+    if (mismatch) {
+      for (int q = 0; q < a.nranks; ++q) atomicOr(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_err), ZC_DERR_MISMATCH);
+    }
+    s->gmax = m;
+    s->out = m;
+    s->scale = m == 0.0 ? 1.0 : __dmul_rn(__dmul_rn(2.0, a.rel), m);
+    s->rcp = 1.0 / s->scale;
+    s->my_scale = s->scale;
+    s->requant = 0u;
+    s->requant_f = 1.0;
+  } else if (a.op == MAIL_MAX || a.op == MAIL_EB_SCALE) {
     double m = 0.0;
     bool first = true;
     for (int r = 0; r < a.nranks; ++r) {
@@ -1468,28 +1494,28 @@ int enqueue_allreduce_eb(zc_comm* c, const float* d_x, void* d_out, int out_f64,
   const bool fz = n > 1 && count > 0 && use_staged(c) && fuse_ring() && use_mz(c, max_chunk_units(c, count));
   Scal* s = c->scal();
   if (int rc = cuda_err(launch_absmax(d_x, SRC_F32, count, &s->absmax, c->err_word(), c->stream), "absmax")) return rc;
+  uint32_t rec[8] = {0};  // StreamMeta (collectives.cpp:437-445)
+  rec[0] = ZC_QUANT_ERROR_BOUNDED;
+  rec[2] = static_cast<uint32_t>(count);
+  rec[3] = static_cast<uint32_t>(count >> 32);
   if (n > 1) {
+    // the scale allreduce_max (collectives.cpp:398-421) and, for a non-empty message, the
+    // StreamMeta exchange (:437-458) in one mailbox round; WireStats count both
     count_ctrl_frames(c, 8);
-    if (int rc = launch_mail(c, MAIL_EB_SCALE, nullptr, 1, rel)) return rc;
+    if (count > 0) count_ctrl_frames(c, 24);
+    if (int rc = launch_mail(c, count > 0 ? MAIL_EB_META : MAIL_EB_SCALE, rec, 1, rel)) return rc;
   } else {
     note_launch();
     set_scale_kernel<<<1, 1, 0, c->stream>>>(s, rel, 1);
   }
   const int g = sm_count(c->device) * 4;
   if (n > 1 && count > 0) {
-    // allreduce(q) with the shared scale: the meta ring still runs (and checks the counts)
-    uint32_t rec[8] = {0};
-    rec[0] = ZC_QUANT_ERROR_BOUNDED;
-    rec[2] = static_cast<uint32_t>(count);
-    rec[3] = static_cast<uint32_t>(count >> 32);
-    count_ctrl_frames(c, 24);
+    // allreduce(q) with the shared scale
     if (!fz) {
       note_launch();
       quantize_dev_kernel<<<g, 256, 0, c->stream>>>(d_x, count, s, c->sym, c->err_word());
-      if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
       if (int rc = enqueue_ring(c, c->sym, count, true)) return rc;
     } else {
-      if (int rc = launch_mail(c, MAIL_META, rec, 0, 0.0, 1)) return rc;
       // Fused: nothing is quantized or dequantized in a pass of its own.  RS step 0 encodes the
       // rank's own chunk straight from fp32; every RS receive quantizes the local fp32 chunk into
       // the sum (OUT_ADD_Q) and records the sums' range for the next send; AG receives dequantize
