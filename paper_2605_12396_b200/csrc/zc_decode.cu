@@ -21,6 +21,7 @@ namespace {
 constexpr int DT = 256;                // threads per CTA
 constexpr uint64_t SLICE_VEC = 16384;  // 16-byte vectors per CTA slice (256 KiB)
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kCarveout = 75;           // percent of L1 as shared memory: 4 CTAs x ~37 KB
 
 __device__ __forceinline__ uint64_t unit_raw(const DecParams& p, uint32_t u) {
   if (p.bare) return p.hdr.raw_bytes;
@@ -226,10 +227,15 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
   __shared__ FrameCheck fc;
   // a frame is one codec: the Huffman tables and the FixedLen staging words share the space, which
   // leaves the L1 room for every thread's current 128-byte line of its Huffman grain
+  // (Huffman: the tables, then the swizzled root LUT and the warps' stream windows)
   constexpr size_t kWordsBytes = sizeof(uint32_t) * (DT / 32) * 136 * 4;
-  __shared__ __align__(16) uint8_t s_pool[sizeof(DevHuff) > kWordsBytes ? sizeof(DevHuff) : kWordsBytes];
+  constexpr size_t kTabBytes = (sizeof(DevHuff) + 15) / 16 * 16;
+  constexpr size_t kHuffBytes =
+      kTabBytes + 2u * (1u << ZC_HUFF_ROOT_BITS) + sizeof(uint32_t) * (DT / 32) * kHuffWarpScratchWords;
+  __shared__ __align__(16) uint8_t s_pool[kHuffBytes > kWordsBytes ? kHuffBytes : kWordsBytes];
   DevHuff& s_t = *reinterpret_cast<DevHuff*>(s_pool);
   uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pool);
+  uint32_t* s_hscratch = p.huff_lane ? nullptr : reinterpret_cast<uint32_t*>(s_pool + kTabBytes);
   __shared__ uint8_t s_lens[256];
   __shared__ uint32_t s_flag;
   uint32_t err = 0;
@@ -248,7 +254,8 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
   const double sc = dec_scale(p);
   Sink sink{p.out_kind, p.out, sc, p.out_kind == OUT_ADD_Q ? 1.0 / sc : 0.0, p.acc_f32, 0u};
   const uint32_t* idx = p.index ? p.index + static_cast<uint64_t>(u) * p.index_stride : nullptr;
-  uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err);
+  uint32_t f = decode_slice<false, 4>(fc, payload, R, v0, v1, sink, obase, idx, p.ctx, &s_t, &s_flag, s_lens, s_words, err,
+                                       s_hscratch);
   if (p.maxzz_out != nullptr && is_add_sink(p.out_kind)) {  // the sums' range, for the next send
     const uint32_t m = __reduce_max_sync(FULL, sink.mz);
     if (lane == 0 && m) atomicMax(p.maxzz_out + u, m);
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(DT) decode_kernel(const DecParams p) {
 }  // namespace
 
 void preload_decode_kernels() {
-  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
+  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, kCarveout);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, decode_kernel);
   cudaGetLastError();
@@ -302,7 +309,9 @@ cudaError_t launch_decode(const DecParams& p0, cudaStream_t s) {
   const uint32_t slices = static_cast<uint32_t>((nvec + SLICE_VEC - 1) / SLICE_VEC);
   dim3 grid(slices > 0 ? slices : 1, p.nunits);
   static std::atomic<uint64_t> carve{0};
-  if (first_on_device(carve)) cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 40);
+  if (first_on_device(carve)) cudaFuncSetAttribute(decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, kCarveout);
+  static const bool lane_dec = std::getenv("ZC_HUFF_LANE") != nullptr;  // A/B: the per-lane grain decoder
+  p.huff_lane = lane_dec ? 1 : 0;
   note_launch();
   if (p.fast) return launch_pdl(decode_kernel, grid, dim3(DT), 0, s, p);
   decode_kernel<<<grid, DT, 0, s>>>(p);

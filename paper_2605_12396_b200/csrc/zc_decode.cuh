@@ -356,6 +356,101 @@ __device__ __forceinline__ bool huff_grain(const DevHuff* t, const uint8_t* s, u
   return ok && pos <= slen * 8;
 }
 
+// ---- warp-staged short-code grain decoder (max code length <= ROOT_BITS; the throughput path)
+//
+// huff_grain above reads each lane's stream with its own loads: a warp load touches 32 lines, and
+// a predicated refill waits (per-warp scoreboard) on the load another lane issued one symbol ago,
+// so L2 latency sits on the chain.  Here the warp decodes its 32 grains in rounds of 32 symbols
+// per lane.  Each round first stages every lane's next 16 stream words (>= the 31 + 32 x 12 + 64
+// bits a round can touch) into a per-warp shared window with cooperative loads (one warp load =
+// two lanes' 64-byte windows), then each lane decodes groups of 4 codes from a 64-bit funnel of
+// its window (4 x 12 <= 48 bits: no refill inside a group).  The root LUT is read through a copy
+// whose u16 slots are XOR-swizzled by the index's high bits: the low index bits are the next
+// code's bits, highly skewed for short codes, and would otherwise pile the warp's lookups onto a
+// few banks.
+constexpr int kHWinWords = 16;   // staged words per lane and round
+constexpr int kHWinPitch = 33;   // words between a window's word k and k+1 (bank = k + lane)
+constexpr uint32_t kHuffWarpScratchWords = kHWinWords * kHWinPitch;  // per warp
+
+__device__ __forceinline__ uint32_t lut_swz(uint32_t i) { return i ^ ((i >> 6) & 0x3eu); }
+
+// Swizzled copy of t->lut into slut (all threads call; synchronises).
+__device__ __forceinline__ void swizzle_lut(const DevHuff* t, uint16_t* slut) {
+  for (uint32_t i = threadIdx.x; i < (1u << ZC_HUFF_ROOT_BITS); i += blockDim.x) slut[lut_swz(i)] = t->lut[i];
+  __syncthreads();
+}
+
+// All 32 lanes call.  Lanes with n == 0 only help stage windows.  Lanes with n > 0 decode n
+// symbols (n a multiple of 32) from bit `start`, handing 16 bytes at a time to emit16 at ob.
+// Returns per lane: false on an undecodable code; *end = the final bit position.
+template <bool kCoherent>
+__device__ __forceinline__ bool huff_grain_warp(const uint16_t* slut, const uint8_t* s, uint64_t slen, uint32_t start,
+                                                uint32_t n, const Sink& sink, uint64_t ob, uint32_t* win, uint32_t* end,
+                                                uint32_t& err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* ws = reinterpret_cast<const uint32_t*>(s);
+  const uint64_t full_words = slen / 4;
+  const uint32_t rounds = __reduce_max_sync(0xffffffffu, n) / 32;
+  const uint32_t my_rounds = n / 32;
+  const uint32_t lut = static_cast<uint32_t>(__cvta_generic_to_shared(slut));
+  const uint32_t wsh = static_cast<uint32_t>(__cvta_generic_to_shared(win)) + 4u * lane;
+  uint32_t pos = start;
+  uint32_t emin = 0xffffu;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    // stage: load j serves owners 2j and 2j+1, word (lane & 15) of each window
+    const uint32_t wbase = pos >> 5;
+    uint32_t v[kHWinWords];
+#pragma unroll
+    for (int j = 0; j < kHWinWords; ++j) {
+      const uint32_t owner = 2 * j + (lane >> 4);
+      const uint64_t w = static_cast<uint64_t>(__shfl_sync(0xffffffffu, wbase, owner)) + (lane & 15);
+      v[j] = w < full_words ? ld32<kCoherent>(ws + w) : stream_word<kCoherent>(s, slen, w);
+    }
+    __syncwarp();  // the previous round's reads of the window are done
+#pragma unroll
+    for (int j = 0; j < kHWinWords; ++j) win[(lane & 15) * kHWinPitch + 2 * j + (lane >> 4)] = v[j];
+    __syncwarp();
+    if (r < my_rounds) {
+      uint32_t o = pos & 31;  // bit offset from window word 0
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t a = wsh + 4u * kHWinPitch * (o >> 5);
+          uint32_t x0, x1, x2;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(a));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x1) : "r"(a + 4u * kHWinPitch));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x2) : "r"(a + 8u * kHWinPitch));
+          const uint32_t sh = o & 31;
+          unsigned long long acc = (static_cast<unsigned long long>(__funnelshift_r(x1, x2, sh)) << 32) |
+                                   __funnelshift_r(x0, x1, sh);
+          uint32_t word = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t e;
+            asm volatile("ld.shared.u16 %0, [%1];"
+                         : "=r"(e)
+                         : "r"(lut + 2u * lut_swz(static_cast<uint32_t>(acc) & ((1u << ZC_HUFF_ROOT_BITS) - 1))));
+            const uint32_t l = e >> 8;
+            emin = min(emin, e);
+            acc >>= l;
+            o += l;
+            word = __byte_perm(word, e, k == 0 ? 0x3214u : k == 1 ? 0x3240u : k == 2 ? 0x3410u : 0x4210u);
+          }
+          w4[q] = word;
+        }
+        emit16(sink, ob + 32ull * r + 16u * h, w4, 16, err);
+      }
+      pos = (pos & ~31u) + o;
+    }
+  }
+  *end = pos;
+  // a LUT entry of length 0 (no code starts with the pattern): undecodable; codes past the
+  // stream end (read as zero bits) leave pos beyond it
+  return emin >= 256u && pos <= slen * 8;
+}
+
 // Decode tables for a Huffman frame into shared memory: the embedded codebook rebuilt (with the
 // reference's validation) or a copy of the shared context.  All threads call.
 template <bool kCoherent>
@@ -391,7 +486,7 @@ template <bool kCoherent, int kDecU>
 __device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* payload, uint64_t R, uint64_t v0, uint64_t v1,
                                  const Sink& sink, uint64_t obase, const uint32_t* idx, const DevHuff* ctx,
                                  DevHuff* s_t, uint32_t* s_flag, uint8_t* s_lens_tmp, uint32_t* s_words,
-                                 uint32_t& err) {
+                                 uint32_t& err, uint32_t* s_hscratch = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
   uint32_t flags = 0;
   const uint32_t codec = fc.codec;
@@ -485,7 +580,30 @@ __device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* pay
       const uint64_t Rh = fc.h.raw_bytes;
       const uint64_t ngr = (Rh + kIndexGrain - 1) / kIndexGrain;
       const uint64_t g0 = v0 / 64, g1 = min(ngr, (v1 + 63) / 64);
-      for (uint64_t g = g0 + tid; g < g1; g += nthr) {
+      const bool shortc = s_t->max_len <= ZC_HUFF_ROOT_BITS;
+      const bool aligned = (reinterpret_cast<uintptr_t>(s) & 3) == 0;
+      uint64_t gseq = g0;  // grains from here on run the per-lane decoder
+      if (s_hscratch != nullptr && shortc && aligned) {
+        // warp-staged decoder for every full grain; the unit's partial last grain (if any) after
+        uint16_t* slut = reinterpret_cast<uint16_t*>(s_hscratch);
+        uint32_t* win = s_hscratch + (1u << ZC_HUFF_ROOT_BITS) / 2 + warp * kHuffWarpScratchWords;
+        swizzle_lut(s_t, slut);
+        const uint64_t gfull = min(g1, Rh / kIndexGrain);
+        for (uint64_t gb = g0 + warp * 32; gb < gfull; gb += nthr) {
+          const uint64_t g = gb + lane;
+          const bool mine = g < gfull;
+          const uint32_t start = mine ? ld32<kCoherent>(idx + g) : 0u;
+          uint32_t endb = 0;
+          const bool good = huff_grain_warp<kCoherent>(slut, s, slen, start, mine ? kIndexGrain : 0u, sink,
+                                                       obase + g * kIndexGrain, win, &endb, err);
+          if (mine) {
+            if (!good) flags |= 2u;
+            else if (g + 1 < ngr && endb != ld32<kCoherent>(idx + g + 1)) flags |= 1u;
+          }
+        }
+        gseq = max(g0, gfull);
+      }
+      for (uint64_t g = gseq + tid; g < g1; g += nthr) {
         const uint64_t b0 = g * kIndexGrain;
         const uint64_t n = Rh - b0 < kIndexGrain ? Rh - b0 : kIndexGrain;
         unsigned long long lo = 0, hi = 0;
@@ -494,11 +612,10 @@ __device__ inline uint32_t decode_slice(const FrameCheck& fc, const uint8_t* pay
         bool good;
         // unchecked 16-byte reads only where even a corrupt grain cannot leave the payload: a
         // grain consumes <= 1024 codes x 32 bits, the reader runs <= 384 bits ahead
-        const bool shortc = s_t->max_len <= ZC_HUFF_ROOT_BITS;
-        if ((reinterpret_cast<uintptr_t>(s) & 3) == 0 && start + 32768 + 1024 <= slen * 8)
+        if (aligned && start + 32768 + 1024 <= slen * 8)
           good = shortc ? huff_grain<kCoherent, false, true>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err)
                         : huff_grain<kCoherent, false, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
-        else if ((reinterpret_cast<uintptr_t>(s) & 3) == 0)
+        else if (aligned)
           good = huff_grain<kCoherent, true, false>(s_t, s, slen, start, static_cast<uint32_t>(n), sink, obase + b0, &endb, err);
         else good = huff_run<kCoherent>(s_t, s, slen, start, n, &endb, [&](uint64_t j, uint32_t sym) {
           const uint32_t k = static_cast<uint32_t>(j & 15);

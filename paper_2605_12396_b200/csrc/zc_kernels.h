@@ -115,6 +115,7 @@ struct DecParams {
   int fast;                // zc_fixed.cu's decoder has handled the valid FixedLen / RAW units
   int own_frames;          // the frames come from this library's batched encoder without a Huffman
                            // context: all valid FixedLen / RAW, so the general kernels are skipped
+  int huff_lane;           // (set by launch_decode) Huffman grains on the per-lane decoder only
 };
 
 // Quantizer bin width of a float source / dequantization factor: the host value, or the device
