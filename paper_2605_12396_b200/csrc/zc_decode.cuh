@@ -155,6 +155,34 @@ __device__ __forceinline__ void emit16(const Sink& k, uint64_t ob, const uint32_
   }
 }
 
+// 32 decoded raw bytes (8 symbol words) at raw offset ob: one 256-bit store per lane for the
+// fp32 and byte sinks (a warp store of 32 lanes' rows at different grains touches 32 lines; 32-byte
+// rows halve the store wavefronts of two 16-byte ones), emit16 twice otherwise.
+__device__ __forceinline__ void emit32(const Sink& k, uint64_t ob, const uint32_t w[8], uint32_t& err) {
+  if (k.kind == OUT_F32) {
+    float* o = static_cast<float*>(k.out) + ob / 4;
+    if ((reinterpret_cast<uintptr_t>(o) & 31) == 0) {
+      float f[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = d2f_rn(__dmul_rn(k.scale, i2d(w[i])));
+      asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "f"(f[0]), "f"(f[1]), "f"(f[2]),
+                   "f"(f[3]), "f"(f[4]), "f"(f[5]), "f"(f[6]), "f"(f[7])
+                   : "memory");
+      return;
+    }
+  } else if (k.kind == OUT_BYTES) {
+    uint8_t* o = static_cast<uint8_t*>(k.out) + ob;
+    if ((reinterpret_cast<uintptr_t>(o) & 31) == 0) {
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                   "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                   : "memory");
+      return;
+    }
+  }
+  emit16(k, ob, w, 16, err);
+  emit16(k, ob + 16, w + 4, 16, err);
+}
+
 // Header checks of recv_batch (collectives.cpp:313-321) and of the codec decoders' preambles
 // (fixedlen.cpp:41-47, huffman.cpp:249-265).  hdr == nullptr: parse the header from the stage.
 // bare: `hdr` describes a payload that starts at the stage (no header bytes, no raw fallback).
@@ -400,11 +428,16 @@ __device__ __forceinline__ bool huff_grain_warp(const uint16_t* slut, const uint
     // stage: load j serves owners 2j and 2j+1, word (lane & 15) of each window
     const uint32_t wbase = pos >> 5;
     uint32_t v[kHWinWords];
+    if (__reduce_max_sync(0xffffffffu, wbase) + kHWinWords <= full_words) {  // the whole warp in bounds
+      const uint32_t* wl = ws + (lane & 15);
 #pragma unroll
-    for (int j = 0; j < kHWinWords; ++j) {
-      const uint32_t owner = 2 * j + (lane >> 4);
-      const uint64_t w = static_cast<uint64_t>(__shfl_sync(0xffffffffu, wbase, owner)) + (lane & 15);
-      v[j] = w < full_words ? ld32<kCoherent>(ws + w) : stream_word<kCoherent>(s, slen, w);
+      for (int j = 0; j < kHWinWords; ++j) v[j] = ld32<kCoherent>(wl + __shfl_sync(0xffffffffu, wbase, 2 * j + (lane >> 4)));
+    } else {
+#pragma unroll
+      for (int j = 0; j < kHWinWords; ++j) {
+        const uint64_t w = static_cast<uint64_t>(__shfl_sync(0xffffffffu, wbase, 2 * j + (lane >> 4))) + (lane & 15);
+        v[j] = w < full_words ? ld32<kCoherent>(ws + w) : stream_word<kCoherent>(s, slen, w);
+      }
     }
     __syncwarp();  // the previous round's reads of the window are done
 #pragma unroll
@@ -412,9 +445,10 @@ __device__ __forceinline__ bool huff_grain_warp(const uint16_t* slut, const uint
     __syncwarp();
     if (r < my_rounds) {
       uint32_t o = pos & 31;  // bit offset from window word 0
+      uint32_t w8[8];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        uint32_t w4[4];
+        uint32_t* w4 = w8 + 4 * h;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t a = wsh + 4u * kHWinPitch * (o >> 5);
@@ -440,8 +474,8 @@ __device__ __forceinline__ bool huff_grain_warp(const uint16_t* slut, const uint
           }
           w4[q] = word;
         }
-        emit16(sink, ob + 32ull * r + 16u * h, w4, 16, err);
       }
+      emit32(sink, ob + 32ull * r, w8, err);
       pos = (pos & ~31u) + o;
     }
   }
