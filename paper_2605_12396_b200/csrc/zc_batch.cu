@@ -694,17 +694,20 @@ __device__ __forceinline__ void grain_codes(const EncParams& p, const RawVec& rv
 }
 
 // Packs one lane's codes LSB-first at tile bit `pos`.  Codes are <= 32 bits, so each code flushes
-// at most one word; every flush is an ATOMS.OR (branch-free: the first and last words may be
-// shared with neighbouring lanes, the tile is zeroed).
+// at most one word.  Only the lane's first and last words may be shared with neighbouring lanes
+// (ATOMS.OR into the zeroed tile); the words between are the lane's own (plain stores).
 __device__ __forceinline__ void pack_codes(uint32_t* tile, uint32_t pos, const unsigned long long ev[16]) {
   uint32_t wi = pos >> 5, nbit = pos & 31;
   unsigned long long acc = 0;
+  bool first = true;
 #pragma unroll
   for (uint32_t j = 0; j < 16; ++j) {
     acc |= (ev[j] & 0xffffffffull) << nbit;
     nbit += static_cast<uint32_t>(ev[j] >> 32);
     const bool f = nbit >= 32;
-    if (f) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+    if (f && first) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+    if (f && !first) tile[wi] = static_cast<uint32_t>(acc);
+    first = first && !f;
     acc = f ? (acc >> 32) : acc;
     wi += f ? 1u : 0u;
     nbit -= f ? 32u : 0u;
@@ -719,7 +722,7 @@ __device__ __forceinline__ void grain_fetch(const EncParams& p, uint64_t uoff, u
   for (int k = 0; k < 2; ++k) {
     const uint64_t v = gv + 32 * k + lane;
     if (kFull) {
-      fetch_full<SRC, false>(p, uoff, v, rv[k]);
+      fetch_full<SRC, false, (SRC == SRC_F32 || SRC == SRC_BYTES) ? kPolDrop : kPolNone>(p, uoff, v, rv[k]);
     } else {
       rv[k].nb = 0;
       if (v < nvec) fetch<SRC, false>(p, uoff, R, v, rv[k]);
@@ -803,6 +806,32 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
       uint32_t* uindex = p.index + static_cast<uint64_t>(u) * p.index_stride;
       uint32_t zero = 0;
       unsigned long long hb = 0;
+      // every vector of the slice full, 16-byte aligned and inside whole grains: no tail checks, and
+      // the slice is read with an evict-last hint (the emit task re-reads it)
+      if ((SRC == SRC_F32 || SRC == SRC_BYTES) && fast_ok && ((v1 - v0) & 63) == 0 && v1 * 16 <= R) {
+        uint32_t lmin = 0xffu;
+        for (uint64_t gv = v0 + static_cast<uint64_t>(warp) * 64; gv < v1; gv += NT * 2) {
+          RawVec rv[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) fetch_full<SRC, false, kPolKeep>(p, uoff, gv + 2 * lane + k, rv[k]);
+          uint32_t gb = 0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            uint32_t w[4];
+            words_full<SRC>(p, rv[k], w, err);
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              const uint32_t l = s_clens[__byte_perm(w[j >> 2], 0u, 0x4440u + (j & 3))];
+              gb += l;
+              lmin = min(lmin, l);
+            }
+          }
+          hb += gb;
+          gb = __reduce_add_sync(FULL, gb);
+          if (lane == 0) uindex[gv / 64] = gb;
+        }
+        zero = lmin == 0 ? 1u : 0u;
+      } else
       for (uint64_t gv = v0 + static_cast<uint64_t>(warp) * 64; gv < v1; gv += NT * 2) {
         RawVec rv[2];
 #pragma unroll
