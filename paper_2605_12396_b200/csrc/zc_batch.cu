@@ -715,6 +715,61 @@ __device__ __forceinline__ void pack_codes(uint32_t* tile, uint32_t pos, const u
   if (nbit > 0) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
 }
 
+// Codes of <= 24 bits (every context whose longest code fits): one u32 per symbol, code in the low
+// 24 bits and length in the top 8, so a lane's 16 codes take 16 registers instead of 32.
+template <int SRC>
+__device__ __forceinline__ void grain_codes32(const EncParams& p, const RawVec& rv, const uint32_t* s_enc32, uint32_t ev[16],
+                                              uint32_t& L, uint32_t& err) {
+  uint32_t w[4];
+  words_full<SRC>(p, rv, w, err);
+  L = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) {
+    ev[j] = s_enc32[__byte_perm(w[j >> 2], 0u, 0x4440u + (j & 3))];
+    L += ev[j] >> 24;
+  }
+}
+
+__device__ __forceinline__ void pack_codes32(uint32_t* tile, uint32_t pos, const uint32_t ev[16]) {
+  uint32_t wi = pos >> 5, nbit = pos & 31;
+  unsigned long long acc = 0;
+  bool first = true;
+#pragma unroll
+  for (uint32_t j = 0; j < 16; ++j) {
+    acc |= static_cast<unsigned long long>(ev[j] & 0xffffffu) << nbit;
+    nbit += ev[j] >> 24;
+    const bool f = nbit >= 32;
+    if (f && first) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+    if (f && !first) tile[wi] = static_cast<uint32_t>(acc);
+    first = first && !f;
+    acc = f ? (acc >> 32) : acc;
+    wi += f ? 1u : 0u;
+    nbit -= f ? 32u : 0u;
+  }
+  if (nbit > 0) atomicOr(&tile[wi], static_cast<uint32_t>(acc));
+}
+
+// grain_pack for full grains with <= 24-bit codes.
+template <int SRC>
+__device__ __forceinline__ void grain_pack32(const EncParams& p, const RawVec rv[2], const uint32_t* s_enc32, uint32_t* tile,
+                                             uint32_t sh0, int lane, uint32_t& err) {
+  uint32_t run = sh0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    uint32_t ev[16];
+    uint32_t L;
+    grain_codes32<SRC>(p, rv[k], s_enc32, ev, L, err);
+    uint32_t x = L;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    pack_codes32(tile, run + x - L, ev);
+    run += __shfl_sync(FULL, x, 31);
+  }
+}
+
 template <int SRC, bool kFull>
 __device__ __forceinline__ void grain_fetch(const EncParams& p, uint64_t uoff, uint64_t R, uint64_t nvec, uint64_t gv,
                                             int lane, RawVec rv[2]) {
@@ -763,6 +818,7 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
   pdl_wait();  // a programmatic dependent of the FixedLen emit (the units' decisions)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ unsigned long long s_enc[256];
+  __shared__ uint32_t s_enc32[256];
   __shared__ uint32_t s_start[BS / kIndexGrain + 1];
   __shared__ uint8_t s_clens[256];
   __shared__ unsigned long long s_r64[NW];
@@ -772,11 +828,13 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
   uint32_t* tile = s_tiles + warp * HT;
   const bool ctx_ok = p.ctx != nullptr && p.ctx->valid != 0;
   const bool fast_ok = aligned16(p.src) && (p.unit_bytes % 16) == 0;
+  const bool codes24 = ctx_ok && p.ctx->max_len <= 24;
   BGlobal* gl = bglobal(us, p.nunits);
   if (g.fast && p.pin == ZC_PIN_AUTO && *reinterpret_cast<const volatile uint32_t*>(&gl->n_huff) == 0) return;
   if (!ctx_ok) return;
   for (int i = tid; i < 256; i += NT) {
     s_enc[i] = p.ctx->enc[i];
+    s_enc32[i] = static_cast<uint32_t>(p.ctx->enc[i] & 0xffffffu) | (static_cast<uint32_t>(p.ctx->len[i]) << 24);
     s_clens[i] = p.ctx->len[i];
   }
   __syncthreads();
@@ -1005,7 +1063,8 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
       }
       for (uint32_t i = lane; i < nw; i += 32) tile[i] = 0;
       __syncwarp();
-      if (full) grain_pack<SRC, true>(p, rv, s_enc, tile, sh0, lane, err);
+      if (full && codes24) grain_pack32<SRC>(p, rv, s_enc32, tile, sh0, lane, err);
+      else if (full) grain_pack<SRC, true>(p, rv, s_enc, tile, sh0, lane, err);
       else grain_pack<SRC, false>(p, rv, s_enc, tile, sh0, lane, err);
       __syncwarp();
       if (lane == 0 && prevtail) tile[0] |= prevtail;
