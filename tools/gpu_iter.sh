@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-PINS=huffman REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k huff_emit_kernel --launch-skip 2 --launch-count 1 \
-  -o /tmp/he -f python tools/codec_probe.py > gpurun_out/ncu_he.log 2>&1
-ncu -i /tmp/he.ncu-rep --page source --csv --print-source=sass > gpurun_out/he_sass.csv 2>&1
-ncu -i /tmp/he.ncu-rep --page raw --csv > gpurun_out/he_raw.csv 2>&1
-tail -1 gpurun_out/ncu_he.log
+PINS=huffman,auto REPS=10 timeout 300 python tools/codec_probe.py > gpurun_out/probe_new.txt 2>&1; cat gpurun_out/probe_new.txt
+timeout 900 python -m pytest tests -m gpu -x -q -k "huff or Huff or golden or codec or ring or embedded" 2>&1 | tail -2
