@@ -425,23 +425,24 @@ __device__ __forceinline__ bool huff_grain_warp(const uint16_t* slut, const uint
   uint32_t pos = start;
   uint32_t emin = 0xffffu;
   for (uint32_t r = 0; r < rounds; ++r) {
-    // stage: load j serves owners 2j and 2j+1, word (lane & 15) of each window
+    // stage: load j serves owners j and j+16, word (lane & 15) of each window (shared-memory banks
+    // k + owner: the two half-warps' banks are disjoint)
     const uint32_t wbase = pos >> 5;
     uint32_t v[kHWinWords];
     if (__reduce_max_sync(0xffffffffu, wbase) + kHWinWords <= full_words) {  // the whole warp in bounds
       const uint32_t* wl = ws + (lane & 15);
 #pragma unroll
-      for (int j = 0; j < kHWinWords; ++j) v[j] = ld32<kCoherent>(wl + __shfl_sync(0xffffffffu, wbase, 2 * j + (lane >> 4)));
+      for (int j = 0; j < kHWinWords; ++j) v[j] = ld32<kCoherent>(wl + __shfl_sync(0xffffffffu, wbase, j + 16 * (lane >> 4)));
     } else {
 #pragma unroll
       for (int j = 0; j < kHWinWords; ++j) {
-        const uint64_t w = static_cast<uint64_t>(__shfl_sync(0xffffffffu, wbase, 2 * j + (lane >> 4))) + (lane & 15);
+        const uint64_t w = static_cast<uint64_t>(__shfl_sync(0xffffffffu, wbase, j + 16 * (lane >> 4))) + (lane & 15);
         v[j] = w < full_words ? ld32<kCoherent>(ws + w) : stream_word<kCoherent>(s, slen, w);
       }
     }
     __syncwarp();  // the previous round's reads of the window are done
 #pragma unroll
-    for (int j = 0; j < kHWinWords; ++j) win[(lane & 15) * kHWinPitch + 2 * j + (lane >> 4)] = v[j];
+    for (int j = 0; j < kHWinWords; ++j) win[(lane & 15) * kHWinPitch + j + 16 * (lane >> 4)] = v[j];
     __syncwarp();
     if (r < my_rounds) {
       uint32_t o = pos & 31;  // bit offset from window word 0
