@@ -649,3 +649,46 @@ def test_indexless_4mib_reference_frame_parallel_decode(zc, port, embed):
     exp = np.zeros(len(sym), np.float32)
     port.lib.zo_dequantize_f32(sym, len(sym), 0, 2e-4, 0, exp)
     assert np.array_equal(npy(y), exp)
+
+
+# ------------------------------------------------------------------ warp-staged short-code decoder
+def _kraft_lengths(maxlen):
+    """A complete prefix code with lengths 1..maxlen plus a second maxlen code (Kraft sum = 1)."""
+    lens = [0] * 256
+    for s in range(maxlen):
+        lens[s] = s + 1
+    lens[maxlen] = maxlen
+    return lens
+
+
+@pytest.mark.parametrize("maxlen", [11, 12, 13])
+@pytest.mark.parametrize("n", [32 * 1024, 70000, 300001])
+def test_huffman_warp_decoder_edges(zc, port, maxlen, n):
+    """Codes at / past the root LUT (12 bits: warp-staged vs per-lane decoder), warps with idle lanes
+    (grain counts not a multiple of 32), a partial last grain, a corrupted companion index (the
+    sequential fixup must reproduce the data) and a truncated payload (failure)."""
+    lens = _kraft_lengths(maxlen)
+    c = zc.HuffmanContext.from_lengths(lens)
+    from oracle import HuffStruct
+    o = HuffStruct()
+    assert port.lib.zo_huff_from_lengths(np.array(lens, np.uint8), C.byref(o)) == 1
+    rng = np.random.default_rng(maxlen * 1000 + n)
+    p = np.array([2.0 ** -min(l, 8) for l in lens[: maxlen + 1]])
+    raw = rng.choice(maxlen + 1, size=n, p=p / p.sum()).astype(np.uint8)
+    cap = 4 * n + 64
+    got, idx = zc.huffman_encode(t(raw), c, cap, with_index=True)
+    assert got.numel() > 0
+    if o is not None:
+        out = np.zeros(cap, np.uint8)
+        pn = port.lib.zo_huffman_encode(raw, n, C.byref(o), out, cap, 0)
+        assert got.numel() == pn and np.array_equal(npy(got), out[:pn])
+    h = hdr(2, n, got.numel(), 0)
+    ok, back = zc.huffman_decode(h, got, c, n, index=idx)
+    assert ok and np.array_equal(npy(back), raw)
+    bad = idx.clone()
+    bad[len(bad) // 2] += 3  # a start bit that is not a code boundary
+    ok, back = zc.huffman_decode(h, got, c, n, index=bad)
+    assert ok and np.array_equal(npy(back), raw)
+    h2 = hdr(2, n, got.numel() - 8, 0)
+    ok, _ = zc.huffman_decode(h2, got[:-8], c, n, index=idx)
+    assert not ok
