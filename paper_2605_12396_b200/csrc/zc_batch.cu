@@ -1024,6 +1024,7 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
       if (2 * lane + 1 < n) uindex[gs0 + 2 * lane + 1] = b0 + c0;
     }
     __syncthreads();
+#pragma unroll 1
     for (uint32_t gi = warp; gi < n; gi += NW) {
       const uint32_t gidx = gs0 + gi;
       const uint32_t B = s_start[gi], E = s_start[gi + 1];
