@@ -284,17 +284,31 @@ __global__ void qsgd_norm_kernel(const float* x, uint64_t n, double* norm, uint3
   double s = 0.0;
   bool bad = false;
   uint64_t i = 0;
-  // loads run 16 elements ahead of the (sequential, in-order) additions
-  constexpr int U = 16;
+  // The additions are one dependent chain; what must not sit on it is memory latency.  Lines are
+  // prefetched into L1 kPre elements ahead (one per 32 elements, so a few hundred misses are in
+  // flight from this one thread), and each 32-element step reads them as 16-byte vectors.
+  constexpr int U = 32;
+  constexpr uint64_t kPre = 16384;  // 64 KiB ahead
+  for (; i < n && (reinterpret_cast<uintptr_t>(x + i) & 15) != 0; ++i) {
+    const double v = static_cast<double>(x[i]);
+    bad |= !isfinite(v);
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  for (uint64_t j = i; j < i + kPre && j < n; j += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + j));
   for (; i + U <= n; i += U) {
-    float f[U];
+    if (i + kPre < n) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + i + kPre));
+    float4 q[U / 4];
 #pragma unroll
-    for (int k = 0; k < U; ++k) f[k] = __ldg(x + i + k);
+    for (int k = 0; k < U / 4; ++k) q[k] = __ldg(reinterpret_cast<const float4*>(x + i) + k);
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const double v = static_cast<double>(f[k]);
-      bad |= !isfinite(v);
-      s = __dadd_rn(s, __dmul_rn(v, v));
+    for (int k = 0; k < U / 4; ++k) {
+      const float f4[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double v = static_cast<double>(f4[e]);
+        bad |= !isfinite(v);
+        s = __dadd_rn(s, __dmul_rn(v, v));
+      }
     }
   }
   for (; i < n; ++i) {

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-PINS=huffman REPS=20 timeout 300 python tools/codec_probe.py > gpurun_out/probe_new.txt 2>&1; cat gpurun_out/probe_new.txt
+timeout 600 python tools/qsgd_probe.py > gpurun_out/qsgd_probe.txt 2>&1; tail -5 gpurun_out/qsgd_probe.txt
+timeout 900 python -m pytest tests -m gpu -x -q -k "qsgd or QSGD" 2>&1 | tail -2
