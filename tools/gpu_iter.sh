@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python tools/qsgd_probe.py > gpurun_out/qsgd_probe.txt 2>&1; tail -5 gpurun_out/qsgd_probe.txt
-timeout 900 python -m pytest tests -m gpu -x -q -k "qsgd or QSGD" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+PINS=huffman,auto REPS=10 timeout 300 python tools/codec_probe.py 2>&1 | tail -2
