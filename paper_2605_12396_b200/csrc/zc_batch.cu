@@ -1040,14 +1040,22 @@ __global__ void __launch_bounds__(NT, 2) huff_emit_kernel(const EncParams p, BUn
       uint32_t prevtail = 0;
       if (sh0 != 0 && gidx > 0) {
         const uint64_t b = static_cast<uint64_t>(gidx) * kIndexGrain - 32 + lane;
-        RawVec pv;
-        fetch<SRC, false>(p, uoff, R, b / 16, pv);
-        uint32_t w[4];
-        if (pv.nb == 16)
-          words_full<SRC>(p, pv, w, err);
-        else
-          to_words<SRC>(p, pv, w, err);
-        const unsigned long long e = s_enc[byte_of(w, static_cast<uint32_t>(b & 15))];
+        uint32_t byte;
+        if (SRC == SRC_F32) {  // only the lane's own element: one load (4 lanes share it), one quantization
+          const uint32_t u = __float_as_uint(__ldg(static_cast<const float*>(p.src) + (uoff + b) / 4));
+          const uint32_t q = static_cast<uint32_t>(quantize_f32bits(u, enc_scale(p), enc_rcp(p), err));
+          byte = (q >> (8 * static_cast<uint32_t>(b & 3))) & 0xFFu;
+        } else {
+          RawVec pv;
+          fetch<SRC, false>(p, uoff, R, b / 16, pv);
+          uint32_t w[4];
+          if (pv.nb == 16)
+            words_full<SRC>(p, pv, w, err);
+          else
+            to_words<SRC>(p, pv, w, err);
+          byte = byte_of(w, static_cast<uint32_t>(b & 15));
+        }
+        const unsigned long long e = s_enc[byte];
         const uint32_t l = static_cast<uint32_t>(e >> 32), c = static_cast<uint32_t>(e);
         uint32_t x = l;
         for (int o = 1; o < 32; o <<= 1) {
