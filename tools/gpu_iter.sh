@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-PINS=huffman REPS=20 timeout 300 python tools/codec_probe.py 2>&1 | tail -1
-timeout 600 python -m pytest tests -m gpu -x -q -k "huff or Huff or golden or codec or ring" 2>&1 | tail -1
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 400 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; cat gpurun_out/bench_final.json
